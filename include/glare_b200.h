@@ -1,0 +1,128 @@
+/* glare_b200 -- C ABI of the B200-native exact readability-metric kernels.
+ *
+ * The reference (glare, /root/reference/pkg/src/glare) is pure Python and has
+ * no FFI; its "operator API" for this path is the set of Python functions
+ * re-exported by glare.metrics (metrics/__init__.py:11-25) and called by the
+ * oracle mode of the engine (engine.py:74-94).  Each entry point below
+ * replaces the numpy body of one of those functions; the Python package
+ * paper_2411_09809_b200 binds them with ctypes and keeps the reference
+ * signatures, validation and degenerate-case returns.
+ *
+ * Conventions
+ *  - every pointer argument named d_* is a DEVICE pointer owned by the caller;
+ *    the library never frees caller memory and allocates only stream-ordered
+ *    scratch (cudaMallocAsync on `stream`) that it releases before returning;
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *    calls are asynchronous on it unless stated otherwise;
+ *  - xy is float64 (n,2) row-major (interleaved double2), edges is int64
+ *    (m,2) row-major index pairs normalised exactly as LayoutGraph does
+ *    (model.py:56-132: small index first, lexicographically sorted, unique,
+ *    no loops, no zero-length edges);
+ *  - return value: GLR_OK (0) or an error code; glr_last_error() returns a
+ *    thread-local message for the last failing call on this thread.
+ *
+ * Sharding: the O(m^2)/O(n^2) passes enumerate an upper-triangular space of
+ * tile pairs ("units", glr_*_units).  A call processes units
+ * [unit_begin, unit_end); partial results of disjoint ranges add up to the
+ * full result, so ranks of a multi-GPU job each take one contiguous range and
+ * sum their partials with one allreduce.
+ */
+#ifndef GLARE_B200_H
+#define GLARE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GLR_OK = 0,
+  GLR_EARG = 1,       /* invalid argument (ParameterError / InputError side) */
+  GLR_ECUDA = 2,      /* CUDA runtime error */
+  GLR_EINVARIANT = 4  /* internal consistency check failed (InvariantError) */
+};
+
+/* ABI version: (major << 16) | minor. */
+int glr_version(void);
+
+/* Thread-local message describing the last error on this thread. */
+const char *glr_last_error(void);
+
+/* ---- node occlusion: reference metrics/exact.py:55-74 -------------------- */
+
+/* Number of vertex tile-pair units for n vertices. */
+uint64_t glr_occlusion_units(int64_t n);
+
+/* Adds to d_out[0] (float64, exact below 2^53) the number of unordered vertex
+ * pairs inside units [unit_begin, unit_end) with
+ *     fl(fl(dx*dx) + fl(dy*dy)) < thr,  dx = x_i - x_j, dy = y_i - y_j,
+ * where thr = (2.0*r)**2 computed by the caller exactly as exact.py:63.
+ * d_out is overwritten (not accumulated). */
+int glr_occlusion_count(const double *d_xy, int64_t n, double thr,
+                        uint64_t unit_begin, uint64_t unit_end,
+                        double *d_out, void *stream);
+
+/* ---- edge crossing / crossing angle: exact.py:145-238, geometry.py:62-110 */
+
+/* Number of edge tile-pair units for m edges. */
+uint64_t glr_crossing_units(int64_t m);
+
+/* Bytes of the per-edge record buffer glr_crossing_prepare fills. */
+size_t glr_crossing_records_bytes(int64_t m);
+
+/* Builds the per-edge records (endpoint coordinates a = xy[edges[:,0]],
+ * b = xy[edges[:,1]], b - a, exact order-preserving 32-bit bbox ranks, axis
+ * angle theta = mod(atan2(by-ay, bx-ax), pi), endpoint ids) into d_records
+ * (glr_crossing_records_bytes(m) bytes, 16-byte aligned).  Also decides
+ * whether the input admits the fast sign path; the decision
+ * is stored in the records header. */
+int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges,
+                         int64_t m, void *d_records, void *stream);
+
+/* Writes to d_out[0..1] the partial (count, dev_sum) of the crossing scan
+ * over units [unit_begin, unit_end) of prepared records: count of unordered
+ * edge pairs with closed-bbox overlap, no shared vertex index and the
+ * straddle predicate of geometry.py:62-79; dev_sum = sum over those pairs of
+ * |ideal - min(d, pi - d)|, d = |theta_i - theta_j| (0 when !with_angle).
+ * If unit_begin == 0 the partial also carries the whole-graph terms, so
+ * partials of a disjoint cover of [0, units) sum to exact.py's result. */
+int glr_crossing_pairs(const void *d_records, int64_t m, int with_angle,
+                       double ideal, uint64_t unit_begin, uint64_t unit_end,
+                       double *d_out, void *stream);
+
+/* prepare + pairs over [unit_begin, unit_end) with internal scratch. */
+int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,
+                      int64_t m, int with_angle, double ideal,
+                      uint64_t unit_begin, uint64_t unit_end, double *d_out,
+                      void *stream);
+
+/* ---- edge length variation: exact.py:127-142 ----------------------------- */
+
+/* d_out[0] = M_l (0.0 when m <= 1). */
+int glr_edge_length_variation(const double *d_xy, int64_t n,
+                              const int64_t *d_edges, int64_t m, double *d_out,
+                              void *stream);
+
+/* ---- minimum angle: exact.py:88-124, geometry.py:82-85 -------------------- */
+
+/* d_out[0] = M_a (1.0 when m == 0). */
+int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges,
+                      int64_t m, double *d_out, void *stream);
+
+/* ---- introspection (tests / bench) --------------------------------------- */
+
+/* 1 if the prepared records take the fast sign path, 0 for the general
+ * exact-comparison path (synchronous: reads the records header). */
+int glr_crossing_fast_path(const void *d_records, void *stream);
+
+/* Number of kernel launches issued by this thread since the last call
+ * (counter is reset by the call). */
+uint64_t glr_take_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GLARE_B200_H */

@@ -1,0 +1,260 @@
+"""CPU oracle for the exact readability-metric hot path -- TEST INFRASTRUCTURE.
+
+This module is the checker, never the product.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import it.  The product path
+(``paper_2411_09809_b200``) never imports anything under ``oracle/`` and fails
+loudly when its CUDA library is missing.
+
+It restates, in numpy, the reference's serial oracle (the ``"oracle"`` mode of
+``glare``; /root/reference/pkg/src/glare/engine.py:74-94) for the five exact
+metrics, using the same IEEE ufunc sequence so counts are bit-identical and
+reals agree to the last few ulps:
+
+* ``node_occlusion``        -- reference src/metrics/exact.py:55-74
+* ``minimum_angle``         -- reference src/metrics/exact.py:88-124, geometry.py:82-85
+* ``edge_length_variation`` -- reference src/metrics/exact.py:127-142
+* ``crossing_scan``         -- reference src/metrics/exact.py:145-222, geometry.py:62-79, 94-110
+* ``edge_crossing`` / ``edge_crossing_angle`` -- src/metrics/exact.py:225-238
+
+``crossing_scan`` is restated in the *dense tiled* form (no x-sort): for every
+unordered pair (i < j) in original edge order it evaluates closed-bbox overlap
+AND index-disjointness AND the four-cross-product straddle test.  The
+reference's x-sort only prunes pairs whose bboxes cannot overlap, so the count
+is identical; the deviation sum differs only in
+summation order.
+
+Parity pinning: tests/test_oracle_golden.py checks this module against the
+reference's own known-answer tests and against golden values produced by the
+reference itself (tests/golden/make_golden.py).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+TWO_PI = 2.0 * math.pi
+_PAIR_BUDGET = 2_000_000
+
+
+def occlusion_threshold(r: float) -> float:
+    """(2r)^2 exactly as the reference computes it (src/metrics/exact.py:63)."""
+    return (2.0 * r) ** 2
+
+
+def node_occlusion(xy: np.ndarray, r: float) -> int:
+    """Unordered vertex pairs with fl(fl(dx*dx)+fl(dy*dy)) < (2r)^2.
+
+    Follows src/metrics/exact.py:55-74 (strict inequality, no FMA, every
+    vertex including isolated ones).
+    """
+    n = len(xy)
+    if n < 2:
+        return 0
+    x = np.ascontiguousarray(xy[:, 0])
+    y = np.ascontiguousarray(xy[:, 1])
+    thr = occlusion_threshold(r)
+    total = 0
+    block = max(1, _PAIR_BUDGET // n)
+    for s in range(0, n - 1, block):
+        e = min(n - 1, s + block)
+        # rows s..e-1 against columns strictly to their right
+        cols = slice(s + 1, n)
+        dx = x[s:e, None] - x[None, cols]
+        dy = y[s:e, None] - y[None, cols]
+        close = dx * dx + dy * dy < thr
+        upper = np.arange(s + 1, n)[None, :] > np.arange(s, e)[:, None]
+        total += int(np.count_nonzero(close & upper))
+    return total
+
+
+def incident_angles(vx, vy, ux, uy):
+    """Angle of u - v in [0, 2pi) -- src/geometry.py:82-85."""
+    ang = np.arctan2(np.asarray(uy) - vy, np.asarray(ux) - vx)
+    return np.where(ang < 0.0, ang + TWO_PI, ang)
+
+
+def axis_angles(ax, ay, bx, by):
+    """Undirected line angle mod pi -- src/geometry.py:94-97."""
+    ang = np.arctan2(np.asarray(by) - ay, np.asarray(bx) - ax)
+    return np.mod(ang, np.pi)
+
+
+def crossing_angles(t1, t2):
+    """Acute angle between two axis angles -- src/geometry.py:107-110."""
+    d = np.abs(np.asarray(t1) - t2)
+    return np.minimum(d, np.pi - d)
+
+
+def vertex_angle_deviations(xy: np.ndarray, edges: np.ndarray) -> np.ndarray:
+    """d_v per vertex of degree >= 1 -- src/metrics/exact.py:88-116."""
+    v = np.concatenate([edges[:, 0], edges[:, 1]])
+    u = np.concatenate([edges[:, 1], edges[:, 0]])
+    ang = incident_angles(xy[v, 0], xy[v, 1], xy[u, 0], xy[u, 1])
+    order = np.lexsort((ang, v))
+    sv = v[order]
+    sa = ang[order]
+    starts = np.flatnonzero(np.concatenate(([True], sv[1:] != sv[:-1])))
+    degs = np.diff(np.append(starts, len(sv)))
+    wrap = TWO_PI - sa[starts + degs - 1] + sa[starts]
+    diffs = np.diff(sa)
+    diffs = np.where(sv[1:] == sv[:-1], diffs, np.inf)
+    diffs = np.append(diffs, np.inf)
+    inner = np.minimum.reduceat(diffs, starts)
+    gap = np.minimum(inner, wrap)
+    phi = TWO_PI / degs
+    return (phi - gap) / phi
+
+
+def minimum_angle(xy: np.ndarray, edges: np.ndarray) -> float:
+    """1 - mean(d_v) over vertices of degree >= 1; 1.0 without edges
+    (src/metrics/exact.py:119-124)."""
+    if len(edges) == 0:
+        return 1.0
+    return 1.0 - float(np.mean(vertex_angle_deviations(xy, edges)))
+
+
+def edge_lengths(xy: np.ndarray, edges: np.ndarray) -> np.ndarray:
+    """sqrt(dx*dx + dy*dy) with d = b - a (src/metrics/exact.py:127-131)."""
+    d = xy[edges[:, 1]] - xy[edges[:, 0]]
+    return np.sqrt(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1])
+
+
+def edge_length_variation(xy: np.ndarray, edges: np.ndarray) -> float:
+    """Two-pass spread of edge lengths (src/metrics/exact.py:134-142)."""
+    m = len(edges)
+    if m <= 1:
+        return 0.0
+    lengths = edge_lengths(xy, edges)
+    mean = float(np.mean(lengths))
+    la = math.sqrt(float(np.sum((lengths - mean) ** 2)) / (m * mean * mean))
+    return la / math.sqrt(m - 1)
+
+
+def straddle_mask(ax, ay, bx, by, cx, cy, dx, dy):
+    """The four cross products and straddle tests of src/geometry.py:62-79,
+    same operand order, each product compared against zero separately."""
+    abx = bx - ax
+    aby = by - ay
+    c1 = abx * (cy - ay) - aby * (cx - ax)
+    c2 = abx * (dy - ay) - aby * (dx - ax)
+    cdx = dx - cx
+    cdy = dy - cy
+    c3 = cdx * (ay - cy) - cdy * (ax - cx)
+    c4 = cdx * (by - cy) - cdy * (bx - cx)
+    s_cd = ((c1 <= 0.0) & (c2 >= 0.0)) | ((c1 >= 0.0) & (c2 <= 0.0))
+    s_ab = ((c3 <= 0.0) & (c4 >= 0.0)) | ((c3 >= 0.0) & (c4 <= 0.0))
+    return s_cd & s_ab
+
+
+def crossing_scan(xy: np.ndarray, edges: np.ndarray, ideal=None):
+    """(count, dev_sum) over unordered non-adjacent edge pairs.
+
+    The predicate of src/metrics/exact.py:182-221 evaluated densely over the
+    upper triangle in original edge order: closed bbox overlap in x and y,
+    no shared vertex index, proper_intersection_mask.  dev_sum accumulates
+    |ideal - crossing_angle| over hits (0.0 when ideal is None).
+    """
+    m = len(edges)
+    if m < 2:
+        return 0, 0.0
+    e0 = edges[:, 0]
+    e1 = edges[:, 1]
+    ax, ay = xy[e0, 0], xy[e0, 1]
+    bx, by = xy[e1, 0], xy[e1, 1]
+    xmin = np.minimum(ax, bx)
+    xmax = np.maximum(ax, bx)
+    ymin = np.minimum(ay, by)
+    ymax = np.maximum(ay, by)
+    theta = axis_angles(ax, ay, bx, by) if ideal is not None else None
+    total = 0
+    dev = 0.0
+    block = max(1, _PAIR_BUDGET // m)
+    for s in range(0, m - 1, block):
+        e = min(m - 1, s + block)
+        i = np.arange(s, e)[:, None]
+        j = np.arange(s + 1, m)[None, :]
+        js = slice(s + 1, m)
+        ok = j > i
+        ok &= (xmax[None, js] >= xmin[s:e, None]) & (xmax[s:e, None] >= xmin[None, js])
+        ok &= (ymax[None, js] >= ymin[s:e, None]) & (ymax[s:e, None] >= ymin[None, js])
+        ok &= (e0[s:e, None] != e0[None, js]) & (e0[s:e, None] != e1[None, js])
+        ok &= (e1[s:e, None] != e0[None, js]) & (e1[s:e, None] != e1[None, js])
+        ii, jj = np.nonzero(ok)
+        if len(ii) == 0:
+            continue
+        ii = ii + s
+        jj = jj + s + 1
+        hit = straddle_mask(ax[ii], ay[ii], bx[ii], by[ii], ax[jj], ay[jj], bx[jj], by[jj])
+        total += int(np.count_nonzero(hit))
+        if ideal is not None and np.any(hit):
+            a = crossing_angles(theta[ii[hit]], theta[jj[hit]])
+            dev += float(np.sum(np.abs(ideal - a)))
+    return total, dev
+
+
+def edge_crossing(xy, edges) -> int:
+    """src/metrics/exact.py:225-227."""
+    return crossing_scan(xy, edges)[0]
+
+
+def edge_crossing_angle(xy, edges, ideal: float) -> float:
+    """src/metrics/exact.py:230-238 (1.0 when there are no crossings)."""
+    total, dev = crossing_scan(xy, edges, ideal)
+    if total == 0:
+        return 1.0
+    return 1.0 - (dev / ideal) / total
+
+
+def node_occlusion_grid(xy: np.ndarray, r: float) -> int:
+    """Exact occlusion via cell bucketing, for sizes the dense oracle cannot
+    reach.  Same predicate as node_occlusion; candidate pairs come from a
+    2r-wide grid (the reference's exact grid variant, src/metrics/enhanced.py:
+    56-127, is pinned to equal the dense oracle by its tests; this restates
+    its idea with a 3x3 neighbourhood scan instead of multi-cell insertion).
+    """
+    n = len(xy)
+    if n < 2:
+        return 0
+    thr = occlusion_threshold(r)
+    w = 2.0 * r
+    x = xy[:, 0]
+    y = xy[:, 1]
+    cx = np.floor((x - x.min()) / w).astype(np.int64)
+    cy = np.floor((y - y.min()) / w).astype(np.int64)
+    # floor rounding can misplace a point by one cell; scanning a 5x5
+    # neighbourhood (offsets -2..2) makes the candidate set a safe superset
+    ncy = int(cy.max()) + 5
+    key = (cx + 2) * ncy + (cy + 2)
+    order = np.argsort(key, kind="stable")
+    skey = key[order]
+    uniq, starts, counts = np.unique(skey, return_index=True, return_counts=True)
+    total = 0
+    for ox in range(-2, 3):
+        for oy in range(-2, 3):
+            off = ox * ncy + oy
+            if (ox, oy) < (0, 0):
+                continue
+            # pair each point with points in the offset cell
+            tgt = skey + off
+            lo = np.searchsorted(skey, tgt, side="left")
+            hi = np.searchsorted(skey, tgt, side="right")
+            cnt = hi - lo
+            src = np.repeat(np.arange(n), cnt)
+            if len(src) == 0:
+                continue
+            base = np.repeat(lo, cnt)
+            local = np.arange(len(src)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+            dst = base + local
+            if off == 0:
+                keep = dst > src
+                src = src[keep]
+                dst = dst[keep]
+            p = order[src]
+            q = order[dst]
+            ddx = x[p] - x[q]
+            ddy = y[p] - y[q]
+            total += int(np.count_nonzero(ddx * ddx + ddy * ddy < thr))
+    return total

@@ -1,0 +1,532 @@
+// Edge crossing E_c and crossing angle E_ca: the O(|E|^2) all-pairs pass.
+//
+// Replaces the numpy body of the reference's _crossing_scan
+// (/root/reference/pkg/src/glare/metrics/exact.py:145-222) and the vectorised
+// predicate proper_intersection_mask (geometry.py:62-79).  A pair (i < j)
+// counts when (exact.py:187-217)
+//   closed bbox overlap in x and y  AND  no shared vertex index  AND
+//   straddle(c1, c2) AND straddle(c3, c4)
+// with c1..c4 the reference's four cross products evaluated with the same
+// IEEE operations and operand order (no FMA), each compared against zero
+// separately.  dev_sum accumulates |ideal - min(d, pi - d)| over hits
+// (exact.py:219-221, geometry.py:107-110).
+//
+// Work decomposition: edges are cut into tiles of kTile = kThreads*K; a
+// "unit" is an upper-triangular tile pair (ti <= tj).  Persistent CTAs take a
+// contiguous unit range; each thread keeps K i-edges in registers and streams
+// the j-tile from shared memory (broadcast LDS, no bank conflicts).
+//
+// FP64 budget per pair (fast path): 6 DADD coordinate differences, 8 DMUL,
+// 4 DADD for c1..c4 = 18 FP64 instructions (c3 reuses the c1 differences:
+// fl(ay-cy) = -fl(cy-ay) exactly).  Everything else runs on the ALU/FMA pipes:
+//  - bbox: exact 32-bit dense ranks of xmin/xmax/ymin/ymax (rank order ==
+//    double order, built by glr_crossing_prepare), 4 ISETP;
+//  - signs: the high word of each c, viewed as a float, has the sign of c and
+//    is zero iff c == 0 whenever every nonzero |coordinate| lies in
+//    [2^-400, 2^500]; straddle(c1,c2) AND
+//    straddle(c3,c4) == max(min(f1,f2), min(f3,f4)) <= 0 <= min(max(f1,f2),
+//    max(f3,f4)).  Inputs outside that range use the general kernel, which
+//    compares the doubles themselves.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace glr {
+namespace {
+
+constexpr int kThreads = 128;  // threads per CTA
+constexpr int kK = 4;          // i-edges per thread
+constexpr int kTile = kThreads * kK;
+constexpr int kMinBlocks = 3;  // CTAs per SM
+
+// Fast sign path admissibility bounds on nonzero |coordinate|.
+constexpr double kMaxAbsFast = 0x1p500;
+constexpr double kMinAbsFast = 0x1p-400;
+
+struct __align__(16) EdgeRec {
+  double ax, ay, bx, by;  // a = xy[edges[:,0]], b = xy[edges[:,1]]
+  double abx, aby;        // b - a  (geometry.py:69-70)
+  int rxmin, rxmax, rymin, rymax;  // exact order-preserving bbox ranks
+};
+static_assert(sizeof(EdgeRec) == 64, "EdgeRec must be 64 bytes");
+
+struct __align__(16) RecHeader {
+  int fast;          // 1: fast sign path admissible
+  int pad0;
+  long long m;
+  long long m_pad;
+  unsigned long long maxabs_bits;   // max |coord| (bit pattern)
+  unsigned long long minabs_bits;   // min nonzero |coord| (bit pattern)
+  char pad[216];
+};
+static_assert(sizeof(RecHeader) == 256, "RecHeader must be 256 bytes");
+
+struct RecView {
+  RecHeader *hdr;
+  EdgeRec *rec;
+  double *theta;
+  int2 *ids;
+};
+
+inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; }
+
+inline size_t records_bytes(int64_t m) {
+  int64_t mp = pad_edges(m < 1 ? 1 : m);
+  return sizeof(RecHeader) + (size_t)mp * (sizeof(EdgeRec) + sizeof(double) + sizeof(int2));
+}
+
+inline RecView view(void *base, int64_t m) {
+  int64_t mp = pad_edges(m < 1 ? 1 : m);
+  char *p = reinterpret_cast<char *>(base);
+  RecView v;
+  v.hdr = reinterpret_cast<RecHeader *>(p);
+  v.rec = reinterpret_cast<EdgeRec *>(p + sizeof(RecHeader));
+  v.theta = reinterpret_cast<double *>(p + sizeof(RecHeader) + mp * sizeof(EdgeRec));
+  v.ids = reinterpret_cast<int2 *>(p + sizeof(RecHeader) + mp * (sizeof(EdgeRec) + sizeof(double)));
+  return v;
+}
+
+// np.mod(x, pi) for b = pi > 0 (numpy npy_divmod): fmod, shift negatives
+// into range, +0.0 for a zero remainder.
+__device__ inline double mod_pi(double x) {
+  const double PI = 3.141592653589793;
+  double r = fmod(x, PI);
+  if (r != 0.0) {
+    if (r < 0.0) r = __dadd_rn(r, PI);
+  } else {
+    r = 0.0;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------- prepare --
+
+__global__ void gather_kernel(const double2 *__restrict__ xy, const longlong2 *__restrict__ edges,
+                              int64_t m, int64_t m_pad, RecView rv, double *xs, double *ys) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m_pad;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    EdgeRec r;
+    if (e < m) {
+      longlong2 uv = edges[e];
+      double2 a = xy[uv.x], b = xy[uv.y];
+      r.ax = a.x; r.ay = a.y; r.bx = b.x; r.by = b.y;
+      r.abx = __dsub_rn(b.x, a.x);
+      r.aby = __dsub_rn(b.y, a.y);
+      r.rxmin = r.rxmax = r.rymin = r.rymax = 0;
+      // axis angle of a->b, geometry.py:94-97
+      rv.theta[e] = mod_pi(atan2(r.aby, r.abx));
+      rv.ids[e] = make_int2((int)uv.x, (int)uv.y);
+      xs[e] = fmin(a.x, b.x);
+      xs[m + e] = fmax(a.x, b.x);
+      ys[e] = fmin(a.y, b.y);
+      ys[m + e] = fmax(a.y, b.y);
+    } else {
+      // padding: zero coordinates, empty bbox (never overlaps), unique ids
+      r.ax = r.ay = r.bx = r.by = r.abx = r.aby = 0.0;
+      r.rxmin = r.rymin = 0x7fffffff;
+      r.rxmax = r.rymax = -1;
+      rv.theta[e] = 0.0;
+      rv.ids[e] = make_int2(-1 - (int)(e - m), -1 - (int)(e - m));
+    }
+    rv.rec[e] = r;
+  }
+}
+
+// lower_bound with double comparisons: equal values (and -0.0/+0.0) share a
+// rank and rank order equals double order.
+__device__ inline int lower_rank(const double *sorted, int64_t len, double v) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return (int)lo;
+}
+
+__global__ void rank_kernel(int64_t m, RecView rv, const double *xs, const double *ys,
+                            const double *sx, const double *sy) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    EdgeRec *r = &rv.rec[e];
+    r->rxmin = lower_rank(sx, 2 * m, xs[e]);
+    r->rxmax = lower_rank(sx, 2 * m, xs[m + e]);
+    r->rymin = lower_rank(sy, 2 * m, ys[e]);
+    r->rymax = lower_rank(sy, 2 * m, ys[m + e]);
+  }
+}
+
+// max |c| and min nonzero |c| over all coordinates, as ordered bit patterns.
+__global__ void magnitude_kernel(const double *__restrict__ xy, int64_t count,
+                                 unsigned long long *maxb, unsigned long long *minb) {
+  unsigned long long mx = 0, mn = ~0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(xy[i]));
+    mx = b > mx ? b : mx;
+    if (b != 0) mn = b < mn ? b : mn;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a = __shfl_down_sync(0xffffffffu, mx, o);
+    unsigned long long c = __shfl_down_sync(0xffffffffu, mn, o);
+    mx = a > mx ? a : mx;
+    mn = c < mn ? c : mn;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(maxb, mx);
+    atomicMin(minb, mn);
+  }
+}
+
+__global__ void header_kernel(RecHeader *hdr, int64_t m, int64_t m_pad,
+                              const unsigned long long *maxb, const unsigned long long *minb) {
+  unsigned long long mx = *maxb, mn = *minb;
+  double dmx = __longlong_as_double((long long)mx);
+  double dmn = mn == ~0ull ? 1.0 : __longlong_as_double((long long)mn);
+  hdr->m = m;
+  hdr->m_pad = m_pad;
+  hdr->maxabs_bits = mx;
+  hdr->minabs_bits = mn;
+  hdr->fast = (dmx <= kMaxAbsFast && dmn >= kMinAbsFast) ? 1 : 0;
+}
+
+// ------------------------------------------------------------ pair kernels --
+
+struct IRegs {
+  double ax[kK], ay[kK], bx[kK], by[kK], abx[kK], aby[kK], th[kK];
+  int rx0[kK], rx1[kK], ry0[kK], ry1[kK], u[kK], v[kK];
+};
+
+template <bool ANGLE>
+__device__ inline void load_i(IRegs &R, const EdgeRec *__restrict__ rec,
+                              const double *__restrict__ theta, const int2 *__restrict__ ids,
+                              uint64_t ti) {
+#pragma unroll
+  for (int k = 0; k < kK; ++k) {
+    const int64_t e = (int64_t)ti * kTile + threadIdx.x + k * kThreads;
+    const double4 *p = reinterpret_cast<const double4 *>(rec + e);
+    double4 q0 = p[0];
+    double2 q1 = reinterpret_cast<const double2 *>(rec + e)[2];
+    int4 rk = reinterpret_cast<const int4 *>(rec + e)[3];
+    R.ax[k] = q0.x; R.ay[k] = q0.y; R.bx[k] = q0.z; R.by[k] = q0.w;
+    R.abx[k] = q1.x; R.aby[k] = q1.y;
+    R.rx0[k] = rk.x; R.rx1[k] = rk.y; R.ry0[k] = rk.z; R.ry1[k] = rk.w;
+    int2 id = ids[e];
+    R.u[k] = id.x; R.v[k] = id.y;
+    R.th[k] = ANGLE ? theta[e] : 0.0;
+  }
+}
+
+__device__ inline float hi_view(double c) { return __int_as_float(__double2hiint(c)); }
+
+// |ideal - min(d, pi - d)| with d = |t1 - t2|, written as
+// || pi/2 - d | - kappa|, kappa = pi/2 - ideal (4 DADD, no DMNMX).
+__device__ inline double angle_dev(double t1, double t2, double kappa) {
+  const double HALF_PI = 1.5707963267948966;
+  double d = __dsub_rn(t1, t2);
+  double e = __dsub_rn(HALF_PI, fabs(d));
+  return fabs(__dsub_rn(fabs(e), kappa));
+}
+
+// One j-edge against the thread's K i-edges.  FAST selects the float-view
+// sign test; otherwise the doubles are compared directly (NaN -> false, as
+// numpy).  DIAG masks pairs with j <= i inside a diagonal tile.
+template <bool FAST, bool ANGLE, bool DIAG>
+__device__ inline void pair_row(const IRegs &R, const EdgeRec *sj, const double *sth,
+                                const int2 *sid, int jj, unsigned (&cnt)[kK],
+                                double (&dev)[kK], double kappa) {
+  const double4 cq = reinterpret_cast<const double4 *>(sj + jj)[0];
+  const double2 cdq = reinterpret_cast<const double2 *>(sj + jj)[2];
+  const int4 rk = reinterpret_cast<const int4 *>(sj + jj)[3];
+  const int2 idj = sid[jj];
+  const double cx = cq.x, cy = cq.y, dx = cq.z, dy = cq.w;
+  const double cdx = cdq.x, cdy = cdq.y;
+  const double thj = ANGLE ? sth[jj] : 0.0;
+#pragma unroll
+  for (int k = 0; k < kK; ++k) {
+    // closed bbox overlap via exact ranks (exact.py:191-194)
+    bool ok = (rk.y >= R.rx0[k]) & (R.rx1[k] >= rk.x) & (rk.w >= R.ry0[k]) & (R.ry1[k] >= rk.z);
+    // no shared vertex index (exact.py:205-210)
+    ok &= (R.u[k] != idj.x) & (R.u[k] != idj.y) & (R.v[k] != idj.x) & (R.v[k] != idj.y);
+    if (DIAG) ok &= jj > (int)threadIdx.x + k * kThreads;
+    // coordinate differences: (cx-ax), (cy-ay), (dx-ax), (dy-ay), (bx-cx), (by-cy)
+    const double dcx = __dsub_rn(cx, R.ax[k]);
+    const double dcy = __dsub_rn(cy, R.ay[k]);
+    const double ddx = __dsub_rn(dx, R.ax[k]);
+    const double ddy = __dsub_rn(dy, R.ay[k]);
+    const double ebx = __dsub_rn(R.bx[k], cx);
+    const double eby = __dsub_rn(R.by[k], cy);
+    // geometry.py:71-76, same roundings:
+    const double c1 = __dsub_rn(__dmul_rn(R.abx[k], dcy), __dmul_rn(R.aby[k], dcx));
+    const double c2 = __dsub_rn(__dmul_rn(R.abx[k], ddy), __dmul_rn(R.aby[k], ddx));
+    const double c3 = __dsub_rn(__dmul_rn(cdy, dcx), __dmul_rn(cdx, dcy));
+    const double c4 = __dsub_rn(__dmul_rn(cdx, eby), __dmul_rn(cdy, ebx));
+    bool hit;
+    if (FAST) {
+      const float f1 = hi_view(c1), f2 = hi_view(c2), f3 = hi_view(c3), f4 = hi_view(c4);
+      const float lo = fmaxf(fminf(f1, f2), fminf(f3, f4));
+      const float hi = fminf(fmaxf(f1, f2), fmaxf(f3, f4));
+      hit = ok & (lo <= 0.0f) & (hi >= 0.0f);
+    } else {
+      const bool s_cd = ((c1 <= 0.0) & (c2 >= 0.0)) | ((c1 >= 0.0) & (c2 <= 0.0));
+      const bool s_ab = ((c3 <= 0.0) & (c4 >= 0.0)) | ((c3 >= 0.0) & (c4 <= 0.0));
+      hit = ok & s_cd & s_ab;
+    }
+    cnt[k] += hit ? 1u : 0u;
+    if (ANGLE) {
+      const double t = angle_dev(R.th[k], thj, kappa);
+      if (hit) dev[k] = __dadd_rn(dev[k], t);
+    }
+  }
+}
+
+template <bool FAST, bool ANGLE>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
+                   const double *__restrict__ theta, const int2 *__restrict__ ids, uint64_t T,
+                   uint64_t ubeg, uint64_t uend, double kappa,
+                   unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
+  if (hdr->fast != (FAST ? 1 : 0)) return;
+  __shared__ __align__(16) EdgeRec sj[kTile];
+  __shared__ double sth[ANGLE ? kTile : 1];
+  __shared__ int2 sid[kTile];
+  __shared__ unsigned long long red_u[kThreads / 32];
+  __shared__ double red_d[kThreads / 32];
+
+  const uint64_t span = uend - ubeg;
+  const uint64_t b = ubeg + span * blockIdx.x / gridDim.x;
+  const uint64_t e = ubeg + span * (blockIdx.x + 1) / gridDim.x;
+
+  unsigned long long total = 0;
+  double dsum = 0.0, dcomp = 0.0;  // Kahan over per-unit partials
+  IRegs R;
+  uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
+  if (b < e) tri_unit_coords(b, T, &ti, &tj);
+  for (uint64_t u = b; u < e; ++u) {
+    if (ti != cur_ti) {
+      load_i<ANGLE>(R, rec, theta, ids, ti);
+      cur_ti = ti;
+    }
+    __syncthreads();  // previous tile fully consumed
+    {
+      const int4 *src = reinterpret_cast<const int4 *>(rec + (int64_t)tj * kTile);
+      int4 *dst = reinterpret_cast<int4 *>(sj);
+#pragma unroll 4
+      for (int q = threadIdx.x; q < kTile * 4; q += kThreads) dst[q] = src[q];
+      for (int q = threadIdx.x; q < kTile; q += kThreads) {
+        sid[q] = ids[(int64_t)tj * kTile + q];
+        if (ANGLE) sth[q] = theta[(int64_t)tj * kTile + q];
+      }
+    }
+    __syncthreads();
+    unsigned cnt[kK];
+    double dev[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+    if (ti == tj) {
+      for (int jj = 0; jj < kTile; ++jj)
+        pair_row<FAST, ANGLE, true>(R, sj, sth, sid, jj, cnt, dev, kappa);
+    } else {
+#pragma unroll 2
+      for (int jj = 0; jj < kTile; ++jj)
+        pair_row<FAST, ANGLE, false>(R, sj, sth, sid, jj, cnt, dev, kappa);
+    }
+    unsigned c = 0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
+    total += c;
+    if (ANGLE) {
+      double y = __dsub_rn(s, dcomp);
+      double t = __dadd_rn(dsum, y);
+      dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
+      dsum = t;
+    }
+    if (++tj == T) { ++ti; tj = ti; }
+  }
+  unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
+  double bd = block_sum<kThreads>(dsum, red_d);
+  if (threadIdx.x == 0) {
+    cta_cnt[blockIdx.x] = bc;
+    cta_dev[blockIdx.x] = bd;
+  }
+}
+
+__global__ void cross_finalize_kernel(const unsigned long long *cta_cnt, const double *cta_dev,
+                                      int ncta, double *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long c = 0;
+    for (int i = 0; i < ncta; ++i) c += cta_cnt[i];
+    out[0] = (double)c;
+    out[1] = kahan_sum(cta_dev, ncta);
+  }
+}
+
+int grid_for(uint64_t units) {
+  uint64_t g = (uint64_t)sm_count() * kMinBlocks;
+  if (units < g) g = units;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                     void *d_records, cudaStream_t st) {
+  if (m < 0 || n < 0 || d_records == nullptr || (m > 0 && (d_xy == nullptr || d_edges == nullptr))) {
+    set_error("glr_crossing_prepare: invalid arguments (n=%lld, m=%lld)", (long long)n,
+              (long long)m);
+    return GLR_EARG;
+  }
+  if (m >= (int64_t)1 << 30) {
+    set_error("glr_crossing_prepare: m=%lld exceeds the int32 rank range", (long long)m);
+    return GLR_EARG;
+  }
+  if (reinterpret_cast<uintptr_t>(d_records) % 16 != 0) {
+    set_error("glr_crossing_prepare: records buffer must be 16-byte aligned");
+    return GLR_EARG;
+  }
+  const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
+  RecView rv = view(d_records, m);
+  const int64_t mm = m < 1 ? 0 : m;
+  // scratch: xs[2m], ys[2m], sorted xs/ys [2m each], 2 magnitude words, cub temp
+  size_t cub_bytes = 0;
+  if (mm > 0)
+    GLR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, (const double *)nullptr,
+                                            (double *)nullptr, (int)(2 * mm), 0, 64, st));
+  const size_t arr = (size_t)(2 * mm) * sizeof(double);
+  const size_t arr_al = (arr + 255) & ~(size_t)255;
+  Scratch scr(4 * arr_al + 256 + cub_bytes, st);
+  GLR_CUDA(scr.err);
+  char *base = scr.as<char>();
+  double *xs = reinterpret_cast<double *>(base);
+  double *ys = reinterpret_cast<double *>(base + arr_al);
+  double *sx = reinterpret_cast<double *>(base + 2 * arr_al);
+  double *sy = reinterpret_cast<double *>(base + 3 * arr_al);
+  unsigned long long *mag = reinterpret_cast<unsigned long long *>(base + 4 * arr_al);
+  void *cub_tmp = base + 4 * arr_al + 256;
+
+  const int nt = 256;
+  int blocks = (int)((m_pad + nt - 1) / nt);
+  if (blocks > sm_count() * 16) blocks = sm_count() * 16;
+  gather_kernel<<<blocks, nt, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
+                                       reinterpret_cast<const longlong2 *>(d_edges), mm, m_pad,
+                                       rv, xs, ys);
+  GLR_LAUNCHED("gather_kernel");
+  if (mm > 0) {
+    size_t tb = cub_bytes;
+    GLR_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, xs, sx, (int)(2 * mm), 0, 64, st));
+    count_launch(4);
+    tb = cub_bytes;
+    GLR_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, ys, sy, (int)(2 * mm), 0, 64, st));
+    count_launch(4);
+    int rb = (int)((mm + nt - 1) / nt);
+    if (rb > sm_count() * 16) rb = sm_count() * 16;
+    rank_kernel<<<rb, nt, 0, st>>>(mm, rv, xs, ys, sx, sy);
+    GLR_LAUNCHED("rank_kernel");
+  }
+  GLR_CUDA(cudaMemsetAsync(mag, 0x00, sizeof(unsigned long long), st));
+  GLR_CUDA(cudaMemsetAsync(mag + 1, 0xff, sizeof(unsigned long long), st));
+  if (n > 0) {
+    int mb = (int)((2 * n + nt - 1) / nt);
+    if (mb > sm_count() * 8) mb = sm_count() * 8;
+    magnitude_kernel<<<mb, nt, 0, st>>>(d_xy, 2 * n, mag, mag + 1);
+    GLR_LAUNCHED("magnitude_kernel");
+  }
+  header_kernel<<<1, 1, 0, st>>>(rv.hdr, mm, m_pad, mag, mag + 1);
+  GLR_LAUNCHED("header_kernel");
+  return GLR_OK;
+}
+
+int crossing_pairs(const void *d_records, int64_t m, int with_angle, double ideal,
+                   uint64_t ubeg, uint64_t uend, double *d_out, cudaStream_t st) {
+  if (d_records == nullptr || d_out == nullptr || m < 0) {
+    set_error("glr_crossing_pairs: invalid arguments");
+    return GLR_EARG;
+  }
+  const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
+  const uint64_t T = (uint64_t)(m_pad / kTile);
+  const uint64_t U = tri_units(T);
+  if (ubeg > uend || uend > U) {
+    set_error("glr_crossing_pairs: unit range [%llu, %llu) outside [0, %llu)",
+              (unsigned long long)ubeg, (unsigned long long)uend, (unsigned long long)U);
+    return GLR_EARG;
+  }
+  if (with_angle && !(ideal > 0.0 && ideal <= 1.5707963267948966)) {
+    set_error("glr_crossing_pairs: ideal angle must lie in (0, pi/2], got %g", ideal);
+    return GLR_EARG;
+  }
+  if (m < 2 || ubeg == uend) {
+    GLR_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), st));
+    return GLR_OK;
+  }
+  RecView rv = view(const_cast<void *>(d_records), m);
+  const int grid = grid_for(uend - ubeg);
+  Scratch scr((size_t)grid * (sizeof(unsigned long long) + sizeof(double)), st);
+  GLR_CUDA(scr.err);
+  unsigned long long *cc = scr.as<unsigned long long>();
+  double *cd = reinterpret_cast<double *>(cc + grid);
+  const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
+  if (with_angle) {
+    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+                                                              ubeg, uend, kappa, cc, cd);
+    GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
+    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+                                                               ubeg, uend, kappa, cc, cd);
+    GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
+  } else {
+    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+                                                               ubeg, uend, 0.0, cc, cd);
+    GLR_LAUNCHED("cross_pairs_kernel<fast>");
+    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+                                                                ubeg, uend, 0.0, cc, cd);
+    GLR_LAUNCHED("cross_pairs_kernel<general>");
+  }
+  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, d_out);
+  GLR_LAUNCHED("cross_finalize_kernel");
+  return GLR_OK;
+}
+
+}  // namespace glr
+
+extern "C" {
+
+uint64_t glr_crossing_units(int64_t m) {
+  const int64_t m_pad = glr::pad_edges(m < 1 ? 1 : m);
+  return glr::tri_units((uint64_t)(m_pad / glr::kTile));
+}
+
+size_t glr_crossing_records_bytes(int64_t m) { return glr::records_bytes(m); }
+
+int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                         void *d_records, void *stream) {
+  return glr::crossing_prepare(d_xy, n, d_edges, m, d_records, glr::as_stream(stream));
+}
+
+int glr_crossing_pairs(const void *d_records, int64_t m, int with_angle, double ideal,
+                       uint64_t unit_begin, uint64_t unit_end, double *d_out, void *stream) {
+  return glr::crossing_pairs(d_records, m, with_angle, ideal, unit_begin, unit_end, d_out,
+                             glr::as_stream(stream));
+}
+
+int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                      int with_angle, double ideal, uint64_t unit_begin, uint64_t unit_end,
+                      double *d_out, void *stream) {
+  cudaStream_t st = glr::as_stream(stream);
+  glr::Scratch rec(glr::records_bytes(m), st);
+  GLR_CUDA(rec.err);
+  int rc = glr::crossing_prepare(d_xy, n, d_edges, m, rec.ptr, st);
+  if (rc != GLR_OK) return rc;
+  return glr::crossing_pairs(rec.ptr, m, with_angle, ideal, unit_begin, unit_end, d_out, st);
+}
+
+int glr_crossing_fast_path(const void *d_records, void *stream) {
+  int fast = -1;
+  cudaStream_t st = glr::as_stream(stream);
+  if (cudaMemcpyAsync(&fast, d_records, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    glr::set_error("glr_crossing_fast_path: copy failed");
+    return -1;
+  }
+  return fast;
+}
+
+}  // extern "C"

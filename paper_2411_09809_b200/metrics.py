@@ -1,0 +1,251 @@
+"""Drop-in exact readability metrics on B200.
+
+Same names, signatures, validation, degenerate-case returns and scalar types
+as the reference's serial oracle functions
+(/root/reference/pkg/src/glare/metrics/exact.py, re-exported by
+metrics/__init__.py:11-25):
+
+    node_occlusion(g, r) -> int                      exact.py:55-74
+    minimum_angle(g) -> float                        exact.py:119-124
+    edge_length_variation(g) -> float                exact.py:134-142
+    edge_crossing(g) -> int                          exact.py:225-227
+    edge_crossing_angle(g, ideal_angle=7pi/18)       exact.py:230-238
+    _crossing_scan(g, ideal_angle=None)              exact.py:145-222
+
+``g`` is this package's ``LayoutGraph``, the reference's own ``LayoutGraph``
+(duck-typed on ``xy``/``edges``), or a ``DeviceGraph`` whose arrays already
+live in HBM.  The arithmetic runs in the hand-written sm_100a kernels of
+``libglare_b200.so``; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import IDEAL_ANGLE_DEFAULT, check_ideal_angle, check_radius
+
+
+class DeviceGraph:
+    """Positions and normalised edge index pairs resident on a CUDA device.
+
+    ``xy``: float64 (n, 2) contiguous; ``edges``: int64 (m, 2) contiguous,
+    normalised as ``LayoutGraph`` does (small index first, sorted, unique).
+    """
+
+    __slots__ = ("xy", "edges")
+
+    def __init__(self, xy: torch.Tensor, edges: torch.Tensor):
+        if xy.dtype != torch.float64 or xy.dim() != 2 or xy.shape[1] != 2 or not xy.is_cuda:
+            raise ValueError("DeviceGraph.xy must be a CUDA float64 (n, 2) tensor")
+        if edges.dtype != torch.int64 or edges.dim() != 2 or edges.shape[1] != 2:
+            raise ValueError("DeviceGraph.edges must be an int64 (m, 2) tensor")
+        if edges.device != xy.device:
+            raise ValueError("DeviceGraph tensors must share a device")
+        self.xy = xy.contiguous()
+        self.edges = edges.contiguous()
+
+    @classmethod
+    def from_graph(cls, g, device=None, pin: bool = False) -> "DeviceGraph":
+        if isinstance(g, DeviceGraph):
+            return g
+        device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        xy = torch.from_numpy(np.ascontiguousarray(g.xy, dtype=np.float64))
+        ed = torch.from_numpy(np.ascontiguousarray(g.edges, dtype=np.int64).reshape(-1, 2))
+        if pin:
+            xy = xy.pin_memory()
+            ed = ed.pin_memory()
+        return cls(xy.to(device, non_blocking=pin), ed.to(device, non_blocking=pin))
+
+    @property
+    def num_vertices(self) -> int:
+        return int(self.xy.shape[0])
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.edges.shape[0])
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(g) -> DeviceGraph:
+    _lib.lib()  # fail loudly before any work if the CUDA library is unusable
+    return DeviceGraph.from_graph(g)
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+# ---- unit-range kernels (device results, no host sync) ----------------------
+
+
+def occlusion_units(n: int) -> int:
+    return int(_lib.lib().glr_occlusion_units(n))
+
+
+def crossing_units(m: int) -> int:
+    return int(_lib.lib().glr_crossing_units(m))
+
+
+def occlusion_threshold(r: float) -> float:
+    """(2r)^2 with the reference's own expression (exact.py:63)."""
+    return (2.0 * r) ** 2
+
+
+def occlusion_partial(dg: DeviceGraph, thr: float, unit_begin: int, unit_end: int,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device float64[1]: occluding pairs inside units [unit_begin, unit_end)."""
+    L = _lib.lib()
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
+    rc = L.glr_occlusion_count(_ptr(dg.xy), dg.num_vertices, float(thr), int(unit_begin),
+                               int(unit_end), _ptr(out), _stream())
+    _lib.check(rc, "glr_occlusion_count")
+    return out
+
+
+class CrossingRecords:
+    """Prepared per-edge records (glr_crossing_prepare) kept in HBM so that
+    several unit ranges / both E_c and E_ca reuse one prologue."""
+
+    def __init__(self, dg: DeviceGraph):
+        L = _lib.lib()
+        self.m = dg.num_edges
+        nbytes = int(L.glr_crossing_records_bytes(self.m))
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dg.xy.device)
+        rc = L.glr_crossing_prepare(_ptr(dg.xy), dg.num_vertices,
+                                    _ptr(dg.edges) if self.m else None, self.m,
+                                    _ptr(self.buf), _stream())
+        _lib.check(rc, "glr_crossing_prepare")
+
+    @property
+    def units(self) -> int:
+        return crossing_units(self.m)
+
+    def fast_path(self) -> bool:
+        return _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream()) == 1
+
+    def partial(self, ideal: float | None, unit_begin: int, unit_end: int,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+        """Device float64[2] = (count, dev_sum) over units [unit_begin, unit_end)."""
+        if out is None:
+            out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
+        rc = _lib.lib().glr_crossing_pairs(
+            _ptr(self.buf), self.m, 0 if ideal is None else 1,
+            0.0 if ideal is None else float(ideal), int(unit_begin), int(unit_end),
+            _ptr(out), _stream())
+        _lib.check(rc, "glr_crossing_pairs")
+        return out
+
+
+def length_variation_device(dg: DeviceGraph, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
+    rc = _lib.lib().glr_edge_length_variation(
+        _ptr(dg.xy), dg.num_vertices, _ptr(dg.edges) if dg.num_edges else None,
+        dg.num_edges, _ptr(out), _stream())
+    _lib.check(rc, "glr_edge_length_variation")
+    return out
+
+
+def minimum_angle_device(dg: DeviceGraph, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
+    rc = _lib.lib().glr_minimum_angle(
+        _ptr(dg.xy), dg.num_vertices, _ptr(dg.edges) if dg.num_edges else None,
+        dg.num_edges, _ptr(out), _stream())
+    _lib.check(rc, "glr_minimum_angle")
+    return out
+
+
+# ---- drop-in metric functions ------------------------------------------------
+
+
+def _num_vertices(g) -> int:
+    return int(g.num_vertices)
+
+
+def _num_edges(g) -> int:
+    return int(g.num_edges)
+
+
+def node_occlusion(g, r: float) -> int:
+    """Unordered vertex pairs with squared distance strictly below (2r)^2."""
+    r = check_radius(r)
+    n = _num_vertices(g)
+    if n < 2:
+        return 0
+    dg = _dev(g)
+    out = occlusion_partial(dg, occlusion_threshold(r), 0, occlusion_units(n))
+    return int(out.item())
+
+
+def minimum_angle(g) -> float:
+    """1 minus the mean normalised deviation from each vertex's ideal gap."""
+    if _num_edges(g) == 0:
+        return 1.0
+    return float(minimum_angle_device(_dev(g)).item())
+
+
+def edge_length_variation(g) -> float:
+    """Coefficient-of-variation style spread of edge lengths, in [0, 1]."""
+    if _num_edges(g) <= 1:
+        return 0.0
+    return float(length_variation_device(_dev(g)).item())
+
+
+def _crossing_scan(g, ideal_angle: float | None = None) -> tuple[int, float]:
+    """(crossing count, sum of |ideal - crossing angle| over crossings)."""
+    m = _num_edges(g)
+    if m < 2:
+        return 0, 0.0
+    rec = CrossingRecords(_dev(g))
+    out = rec.partial(ideal_angle, 0, rec.units)
+    count, dev = out.tolist()
+    return int(count), (float(dev) if ideal_angle is not None else 0.0)
+
+
+def edge_crossing(g) -> int:
+    """Count of non-adjacent edge pairs that properly intersect."""
+    return _crossing_scan(g)[0]
+
+
+def edge_crossing_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT) -> float:
+    """1 minus the mean normalised deviation of crossing angles from ideal."""
+    ideal_angle = check_ideal_angle(ideal_angle)
+    total, dev_sum = _crossing_scan(g, ideal_angle)
+    if total == 0:
+        return 1.0
+    return 1.0 - (dev_sum / ideal_angle) / total
+
+
+def crossing_count_and_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT) -> tuple[int, float]:
+    """E_c and E_ca from ONE fused scan (the engine uses this when both are
+    requested; the reference runs _crossing_scan twice, engine.py:85-92)."""
+    ideal_angle = check_ideal_angle(ideal_angle)
+    total, dev_sum = _crossing_scan(g, ideal_angle)
+    eca = 1.0 if total == 0 else 1.0 - (dev_sum / ideal_angle) / total
+    return total, eca
+
+
+__all__ = [
+    "DeviceGraph",
+    "CrossingRecords",
+    "node_occlusion",
+    "minimum_angle",
+    "edge_length_variation",
+    "edge_crossing",
+    "edge_crossing_angle",
+    "_crossing_scan",
+    "crossing_count_and_angle",
+    "occlusion_partial",
+    "occlusion_units",
+    "crossing_units",
+    "occlusion_threshold",
+    "length_variation_device",
+    "minimum_angle_device",
+]
