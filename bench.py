@@ -1,0 +1,370 @@
+"""Benchmark: edge-pair crossing tests/s (and node-pair occlusion tests/s) on
+BASELINE.json config 5 -- the strong-scaling configuration -- at N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL): every rank builds
+the same seeded synthetic C5 graph, takes its contiguous share of the
+upper-triangular tile-pair unit space, and the partials are combined with one
+allreduce; scaling is strong (fixed total work).
+
+Step = one fused E_c + E_ca pass (glr_crossing_pairs with the angle sum) over
+the whole C5 edge set, inputs resident in HBM (records 320 MB > 126 MB L2, so
+no L2 flush is needed).  `value` = m(m-1)/2 algorithmic edge-pair tests per
+second over the K timed steps (max over ranks).  `e2e` = the same metric
+through the public API with host (pinned) inputs: H2D of xy+edges, prologue,
+pair pass, allreduce, D2H of the result.  `occlusion` = node-pair tests/s of
+the N_c pass timed the same way.
+
+`--impl reference` times the reference algorithm on the host CPU instead: the
+oracle port (oracle/sweep_oracle.c, the reference's x-sorted crossing scan
+restated in C, all host threads) on a bounded sample of the same workload; the
+reference itself is pure Python and cannot travel to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG = 5
+FP64_PER_PAIR_EC = 18      # DADD/DMUL of the bit-exact predicate
+FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
+FP64_PER_PAIR_NC = 5
+CPU_SAMPLE_EDGES = 120_000
+CPU_SAMPLE_SEED = 99
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        reasons = [v for k, v in self.NAMES.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model
+
+
+def cpu_baseline_sample(g, ideal, threads):
+    """Reference algorithm (C port of the x-sorted oracle scan) on a fixed
+    random subset of the config's edges, all given host threads."""
+    from oracle import sweep as S
+
+    rng = np.random.default_rng(CPU_SAMPLE_SEED)
+    m = min(CPU_SAMPLE_EDGES, g.num_edges)
+    sub = np.sort(rng.choice(g.num_edges, size=m, replace=False))
+    edges = g.edges[sub]
+    t0 = time.perf_counter()
+    count, dev = S.crossing_scan(g.xy, edges, ideal, threads=threads)
+    dt = time.perf_counter() - t0
+    pairs = m * (m - 1) / 2
+    return pairs / dt, dt, m, count
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU reference algorithm on this box's host."""
+    if rank != 0:
+        return 0
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import configs
+
+    g, p = configs.make(CONFIG)
+    threads = S.default_threads()
+    for _ in range(args.warmup):
+        cpu_baseline_sample(g, p["ideal"], threads)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, dt, m, _ = cpu_baseline_sample(g, p["ideal"], threads)
+        vals.append(v)
+        t_all += dt
+    value = args.steps * (CPU_SAMPLE_EDGES * (CPU_SAMPLE_EDGES - 1) / 2) / t_all
+    sample = (f"random {CPU_SAMPLE_EDGES}-edge subset of C5 (seed {CPU_SAMPLE_SEED}), "
+              f"fused E_c+E_ca x-sorted sweep; pairs counted as m(m-1)/2")
+    line = {
+        "impl": "reference", "metric": "edge-pair crossing tests/s (E_c+E_ca fused)",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config_desc(g, p, world),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "sample": sample, "cpu": _cpu_info()},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_desc(g, p, world):
+    return {"workload": "C5: Chung-Lu gamma 2.3, 4,000,000 edges / 1,500,000 vertices on the "
+                        "2^16 integer lattice (fp64); E_c + E_ca fused pass; N_c at r=8",
+            "config_index": CONFIG, "edges": int(g.num_edges), "vertices": int(g.num_vertices),
+            "edge_pairs": int(g.num_edges) * (int(g.num_edges) - 1) // 2,
+            "node_pairs": int(g.num_vertices) * (int(g.num_vertices) - 1) // 2,
+            "ideal_deg": 70.0, "radius": p["radius"], "parallelism": f"units{world}",
+            "l2": "inputs (320 MB records) exceed the 126 MB L2; no flush needed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_09809_b200 import _lib, configs, sharding
+    from paper_2411_09809_b200 import metrics as M
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+
+    g, p = configs.make(CONFIG)
+    ideal, radius = p["ideal"], p["radius"]
+    m, n = g.num_edges, g.num_vertices
+    P_E = m * (m - 1) / 2
+    P_V = n * (n - 1) / 2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    dg = M.DeviceGraph.from_graph(g, device=dev)
+    out = torch.zeros(3, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def crossing_step():
+        rec = M.CrossingRecords(dg)
+        b, e = sharding.shard_range(rec.units, rank, world)
+        rec.partial(ideal, b, e, out=out[0:2])
+        sharding.allreduce_partials(out[0:2])
+
+    def occlusion_step():
+        U = M.occlusion_units(n)
+        b, e = sharding.shard_range(U, rank, world)
+        M.occlusion_partial(dg, M.occlusion_threshold(radius), b, e, out=out[2:3])
+        sharding.allreduce_partials(out[2:3])
+
+    # ---- device-resident crossing pass ----
+    for _ in range(args.warmup):
+        crossing_step()
+    barrier()
+    L.glr_take_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern_ms = []
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rec = M.CrossingRecords(dg)
+            b, e = sharding.shard_range(rec.units, rank, world)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record(stream)
+            rec.partial(ideal, b, e, out=out[0:2])
+            k1.record(stream)
+            sharding.allreduce_partials(out[0:2])
+            kern_ms.append((k0, k1))
+        ev1.record(stream)
+        barrier()
+    launches = int(L.glr_take_launch_count())
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    kernel_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kern_ms))
+    count, dev_sum = out[0:2].tolist()
+    value = P_E / (step_ms * 1e-3)
+
+    # ---- occlusion pass ----
+    for _ in range(args.warmup):
+        occlusion_step()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        occlusion_step()
+    ev1.record(stream)
+    barrier()
+    occ_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    occ_count = out[2].item()
+
+    # ---- end-to-end through the public API with pinned host inputs ----
+    xy_h = torch.from_numpy(g.xy).pin_memory()
+    ed_h = torch.from_numpy(g.edges).pin_memory()
+    h2d = xy_h.numel() * 8 + ed_h.numel() * 8
+    e2e_times = []
+    for i in range(args.e2e_steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        dge = M.DeviceGraph(xy_h.to(dev, non_blocking=True), ed_h.to(dev, non_blocking=True))
+        res = sharding.sharded_evaluate(dge, None, ideal, rank, world)
+        c_e2e, d_e2e, _ = res.tolist()  # D2H of the step's result
+        dt = time.perf_counter() - t0
+        if i > 0:  # first iteration warms the pinned-copy path
+            e2e_times.append(dt)
+        assert c_e2e == count, (c_e2e, count)
+    e2e_ms = max_over_ranks(1e3 * statistics.mean(e2e_times))
+    e2e_value = P_E / (e2e_ms * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # FP64 roofline of the dominant kernel (cross_pairs_kernel<fast, angle>)
+    clk = clocks.summary()
+    fast = M.CrossingRecords(dg).fast_path()
+    pairs_per_launch = P_E / world
+    achieved = FP64_PER_PAIR_ECA * pairs_per_launch / (kernel_ms * 1e-3) / 1e12
+    peak_max = 64 * 148 * 1965e6 / 1e12
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    peak_run = 64 * 148 * sm_mhz * 1e6 / 1e12
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import sweep as S
+
+        threads = S.default_threads()
+        v, dt, ms_, _ = cpu_baseline_sample(g, ideal, threads)
+        cpu = {"value": v, "unit": "pairs/s", "cores": threads, "kind": "port",
+               "sample": f"random {ms_}-edge subset of C5, fused E_c+E_ca x-sorted sweep "
+                         f"(oracle/sweep_oracle.c), {dt:.1f} s",
+               "cpu": _cpu_info()}
+    line = {
+        "metric": "edge-pair crossing tests/s (E_c+E_ca fused)",
+        "value": value,
+        "unit": "pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": _config_desc(g, p, world),
+        "result": {"edge_crossing": int(count), "dev_sum": dev_sum,
+                   "edge_crossing_angle": 1.0 - (dev_sum / ideal) / count if count else 1.0,
+                   "node_occlusion": int(occ_count), "fast_sign_path": fast},
+        "occlusion": {"metric": "node-pair occlusion tests/s", "value": P_V / (occ_ms * 1e-3),
+                      "unit": "pairs/s", "ms_per_step": occ_ms,
+                      "fp64_tflops": FP64_PER_PAIR_NC * P_V / world / (occ_ms * 1e-3) / 1e12},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_run,
+                     "unit": "TFLOP/s (FP64 DADD/DMUL instr, 1 per lane)",
+                     "frac": achieved / peak_run,
+                     "frac_at_max_clock": achieved / peak_max, "peak_at_max_clock": peak_max,
+                     "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x median SM clock "
+                                    "under load (microbenchmarked DADD/DMUL: 61.7 "
+                                    "lanes/clk/SM, profiles/r01_pipes.txt); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "kernel": "cross_pairs_kernel<fast,angle>",
+                     "kernel_ms": kernel_ms,
+                     "fp64_per_pair": FP64_PER_PAIR_ECA,
+                     "traffic": None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 3 * 8},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -52,21 +52,29 @@ const char *glr_last_error(void);
 
 /* ---- node occlusion: reference metrics/exact.py:55-74 -------------------- */
 
-/* Number of vertex tile-pair units for n vertices. */
+/* Vertices per tile of the occlusion unit space. */
+int glr_occlusion_tile(void);
+
+/* Number of vertex tile-pair units for n vertices: T(T+1)/2 with
+ * T = ceil(n / glr_occlusion_tile()), unit u = (ti, tj), ti <= tj, row-major. */
 uint64_t glr_occlusion_units(int64_t n);
 
-/* Adds to d_out[0] (float64, exact below 2^53) the number of unordered vertex
- * pairs inside units [unit_begin, unit_end) with
+/* Writes to d_out[0] (float64, exact below 2^53) the number of unordered
+ * vertex pairs (i < j) whose tile pair lies in units [unit_begin, unit_end)
+ * and satisfies
  *     fl(fl(dx*dx) + fl(dy*dy)) < thr,  dx = x_i - x_j, dy = y_i - y_j,
- * where thr = (2.0*r)**2 computed by the caller exactly as exact.py:63.
- * d_out is overwritten (not accumulated). */
+ * where thr = (2.0*r)**2 computed by the caller exactly as exact.py:63. */
 int glr_occlusion_count(const double *d_xy, int64_t n, double thr,
                         uint64_t unit_begin, uint64_t unit_end,
                         double *d_out, void *stream);
 
 /* ---- edge crossing / crossing angle: exact.py:145-238, geometry.py:62-110 */
 
-/* Number of edge tile-pair units for m edges. */
+/* Edges per tile of the crossing unit space. */
+int glr_crossing_tile(void);
+
+/* Number of edge tile-pair units for m edges (same enumeration as
+ * glr_occlusion_units with T = ceil(m / glr_crossing_tile())). */
 uint64_t glr_crossing_units(int64_t m);
 
 /* Bytes of the per-edge record buffer glr_crossing_prepare fills. */
@@ -100,14 +108,18 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,
 
 /* ---- edge length variation: exact.py:127-142 ----------------------------- */
 
-/* d_out[0] = M_l (0.0 when m <= 1). */
+/* d_out[0..2] = (mean length, sum of (l - mean)^2, M_l); M_l = 0.0 and the
+ * sums 0.0 when m <= 1.  Callers that need the reference's Python-level
+ * exceptions (ZeroDivisionError when every length underflows to 0) apply
+ * exact.py:141-142 to d_out[0..1] on the host. */
 int glr_edge_length_variation(const double *d_xy, int64_t n,
                               const int64_t *d_edges, int64_t m, double *d_out,
                               void *stream);
 
 /* ---- minimum angle: exact.py:88-124, geometry.py:82-85 -------------------- */
 
-/* d_out[0] = M_a (1.0 when m == 0). */
+/* d_out[0..2] = (sum of d_v over vertices of degree >= 1, number of such
+ * vertices, M_a); M_a = 1.0 when m == 0. */
 int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges,
                       int64_t m, double *d_out, void *stream);
 

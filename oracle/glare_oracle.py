@@ -258,3 +258,65 @@ def node_occlusion_grid(xy: np.ndarray, r: float) -> int:
             ddy = y[p] - y[q]
             total += int(np.count_nonzero(ddx * ddx + ddy * ddy < thr))
     return total
+
+
+# -- unit-range partials (checks the kernels' tile-pair sharding contract) ----
+
+def _tri_coords(u: int, T: int):
+    """(ti, tj) of unit u in the row-major upper-triangular tile-pair order
+    used by the kernels (paper_2411_09809_b200/csrc/common.cuh)."""
+    ti = 0
+    while u >= T - ti:
+        u -= T - ti
+        ti += 1
+    return ti, ti + u
+
+
+def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int):
+    """(count, dev_sum) restricted to pairs whose tile pair (i//tile, j//tile)
+    has a unit index in [ubeg, uend).  Summing over a partition of
+    [0, T(T+1)/2) gives crossing_scan()."""
+    m = len(edges)
+    T = max(1, -(-m // tile))
+    e0, e1 = edges[:, 0], edges[:, 1]
+    ax, ay, bx, by = xy[e0, 0], xy[e0, 1], xy[e1, 0], xy[e1, 1]
+    xmin, xmax = np.minimum(ax, bx), np.maximum(ax, bx)
+    ymin, ymax = np.minimum(ay, by), np.maximum(ay, by)
+    theta = axis_angles(ax, ay, bx, by) if ideal is not None else None
+    total, dev = 0, 0.0
+    for u in range(ubeg, uend):
+        ti, tj = _tri_coords(u, T)
+        I = np.arange(ti * tile, min(m, (ti + 1) * tile))[:, None]
+        J = np.arange(tj * tile, min(m, (tj + 1) * tile))[None, :]
+        if I.size == 0 or J.size == 0:
+            continue
+        ok = J > I
+        ok &= (xmax[J] >= xmin[I]) & (xmax[I] >= xmin[J]) & (ymax[J] >= ymin[I]) & (ymax[I] >= ymin[J])
+        ok &= (e0[I] != e0[J]) & (e0[I] != e1[J]) & (e1[I] != e0[J]) & (e1[I] != e1[J])
+        ii, jj = np.nonzero(ok)
+        ii = I[ii, 0]
+        jj = J[0, jj]
+        hit = straddle_mask(ax[ii], ay[ii], bx[ii], by[ii], ax[jj], ay[jj], bx[jj], by[jj])
+        total += int(np.count_nonzero(hit))
+        if ideal is not None and np.any(hit):
+            dev += float(np.sum(np.abs(ideal - crossing_angles(theta[ii[hit]], theta[jj[hit]]))))
+    return total, dev
+
+
+def node_occlusion_units(xy, r, tile: int, ubeg: int, uend: int) -> int:
+    """Occluding pairs restricted to vertex tile-pair units [ubeg, uend)."""
+    n = len(xy)
+    T = max(1, -(-n // tile))
+    thr = occlusion_threshold(r)
+    x, y = xy[:, 0], xy[:, 1]
+    total = 0
+    for u in range(ubeg, uend):
+        ti, tj = _tri_coords(u, T)
+        I = np.arange(ti * tile, min(n, (ti + 1) * tile))[:, None]
+        J = np.arange(tj * tile, min(n, (tj + 1) * tile))[None, :]
+        if I.size == 0 or J.size == 0:
+            continue
+        dx = x[I] - x[J]
+        dy = y[I] - y[J]
+        total += int(np.count_nonzero((dx * dx + dy * dy < thr) & (J > I)))
+    return total

@@ -24,11 +24,13 @@ _c = ctypes
 SIGNATURES = {
     "glr_version": (_c.c_int, []),
     "glr_last_error": (_c.c_char_p, []),
+    "glr_occlusion_tile": (_c.c_int, []),
     "glr_occlusion_units": (_c.c_uint64, [_c.c_int64]),
     "glr_occlusion_count": (
         _c.c_int,
         [_c.c_void_p, _c.c_int64, _c.c_double, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_void_p],
     ),
+    "glr_crossing_tile": (_c.c_int, []),
     "glr_crossing_units": (_c.c_uint64, [_c.c_int64]),
     "glr_crossing_records_bytes": (_c.c_size_t, [_c.c_int64]),
     "glr_crossing_prepare": (

@@ -489,6 +489,8 @@ int crossing_pairs(const void *d_records, int64_t m, int with_angle, double idea
 
 extern "C" {
 
+int glr_crossing_tile(void) { return glr::kTile; }
+
 uint64_t glr_crossing_units(int64_t m) {
   const int64_t m_pad = glr::pad_edges(m < 1 ? 1 : m);
   return glr::tri_units((uint64_t)(m_pad / glr::kTile));

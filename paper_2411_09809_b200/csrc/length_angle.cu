@@ -23,8 +23,12 @@ namespace {
 constexpr int kRedThreads = 256;
 constexpr double kTwoPi = 6.283185307179586;  // 2.0 * math.pi
 
-__global__ void set_value_kernel(double *out, double v) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = v;
+__global__ void set_value_kernel(double *out, double a, double b, double c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+    out[2] = c;
+  }
 }
 
 __global__ void __launch_bounds__(kRedThreads)
@@ -71,7 +75,9 @@ __global__ void ml_finalize_kernel(const double *part, int nb, int64_t m, const 
     const double mu = mean[0];
     // exact.py:141-142: sqrt(S / (m*mean*mean)) / sqrt(m - 1)
     const double la = sqrt(S / ((double)m * mu * mu));
-    out[0] = la / sqrt((double)(m - 1));
+    out[0] = mu;
+    out[1] = S;
+    out[2] = la / sqrt((double)(m - 1));
   }
 }
 
@@ -144,7 +150,9 @@ __global__ void ma_finalize_kernel(const double *part_sum, const unsigned long l
     unsigned long long c = 0;
     for (int i = 0; i < nb; ++i) c += part_cnt[i];
     const double s = kahan_sum(part_sum, nb);
-    out[0] = 1.0 - s / (double)c;
+    out[0] = s;
+    out[1] = (double)c;
+    out[2] = 1.0 - s / (double)c;
   }
 }
 
@@ -169,7 +177,7 @@ int glr_edge_length_variation(const double *d_xy, int64_t n, const int64_t *d_ed
     return GLR_EARG;
   }
   if (m <= 1) {
-    set_value_kernel<<<1, 1, 0, st>>>(d_out, 0.0);
+    set_value_kernel<<<1, 1, 0, st>>>(d_out, 0.0, 0.0, 0.0);
     GLR_LAUNCHED("set_value_kernel");
     return GLR_OK;
   }
@@ -202,7 +210,7 @@ int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges, int
     return GLR_EARG;
   }
   if (m == 0) {
-    set_value_kernel<<<1, 1, 0, st>>>(d_out, 1.0);
+    set_value_kernel<<<1, 1, 0, st>>>(d_out, 0.0, 0.0, 1.0);
     GLR_LAUNCHED("set_value_kernel");
     return GLR_OK;
   }

@@ -105,6 +105,8 @@ __global__ void occ_finalize_kernel(const unsigned long long *cta_cnt, int ncta,
 
 extern "C" {
 
+int glr_occlusion_tile(void) { return glr::kTile; }
+
 uint64_t glr_occlusion_units(int64_t n) {
   const int64_t np = glr::pad_vertices(n < 1 ? 1 : n);
   return glr::tri_units((uint64_t)(np / glr::kTile));

@@ -20,6 +20,8 @@ live in HBM.  The arithmetic runs in the hand-written sm_100a kernels of
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 
@@ -143,8 +145,9 @@ class CrossingRecords:
 
 
 def length_variation_device(dg: DeviceGraph, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device float64[3] = (mean length, sum (l - mean)^2, M_l)."""
     if out is None:
-        out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
+        out = torch.empty(3, dtype=torch.float64, device=dg.xy.device)
     rc = _lib.lib().glr_edge_length_variation(
         _ptr(dg.xy), dg.num_vertices, _ptr(dg.edges) if dg.num_edges else None,
         dg.num_edges, _ptr(out), _stream())
@@ -153,8 +156,9 @@ def length_variation_device(dg: DeviceGraph, out: torch.Tensor | None = None) ->
 
 
 def minimum_angle_device(dg: DeviceGraph, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device float64[3] = (sum of d_v, vertices with degree >= 1, M_a)."""
     if out is None:
-        out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
+        out = torch.empty(3, dtype=torch.float64, device=dg.xy.device)
     rc = _lib.lib().glr_minimum_angle(
         _ptr(dg.xy), dg.num_vertices, _ptr(dg.edges) if dg.num_edges else None,
         dg.num_edges, _ptr(out), _stream())
@@ -188,14 +192,20 @@ def minimum_angle(g) -> float:
     """1 minus the mean normalised deviation from each vertex's ideal gap."""
     if _num_edges(g) == 0:
         return 1.0
-    return float(minimum_angle_device(_dev(g)).item())
+    s, count, _ = minimum_angle_device(_dev(g)).tolist()
+    return 1.0 - s / count  # exact.py:124: 1 - mean(d_v)
 
 
 def edge_length_variation(g) -> float:
     """Coefficient-of-variation style spread of edge lengths, in [0, 1]."""
-    if _num_edges(g) <= 1:
+    m = _num_edges(g)
+    if m <= 1:
         return 0.0
-    return float(length_variation_device(_dev(g)).item())
+    mean, sq, _ = length_variation_device(_dev(g)).tolist()
+    # exact.py:141-142 on the host, so degenerate inputs raise what the
+    # reference raises (ZeroDivisionError when every length is 0.0)
+    la = math.sqrt(sq / (m * mean * mean))
+    return la / math.sqrt(m - 1)
 
 
 def _crossing_scan(g, ideal_angle: float | None = None) -> tuple[int, float]:
