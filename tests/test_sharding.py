@@ -1,0 +1,91 @@
+"""Multi-rank path on CPU: world-size-2 gloo process group running the same
+shard plan and allreduce code the NCCL ranks run (paper_2411_09809_b200/
+sharding.py); per-rank partials come from the oracle's unit-range
+restatement (the CUDA kernels' contract, checked against them in
+tests/test_gpu_parity.py)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_09809_b200 import sharding
+
+IDEAL = 7.0 * np.pi / 18.0
+TILE_E = 512
+TILE_V = 1024
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import cases
+        from conftest import graph_from
+        from oracle import glare_oracle as O
+
+        g = graph_from(cases.lattice_stress)
+        Te = -(-g.num_edges // TILE_E)
+        Tv = -(-g.num_vertices // TILE_V)
+        b, e = sharding.shard_range(Te * (Te + 1) // 2, rank, world)
+        c, d = O.crossing_scan_units(g.xy, g.edges, IDEAL, TILE_E, b, e)
+        bv, ev = sharding.shard_range(Tv * (Tv + 1) // 2, rank, world)
+        occ = O.node_occlusion_units(g.xy, 1.0, TILE_V, bv, ev)
+        buf = torch.tensor([float(c), d, float(occ)], dtype=torch.float64)
+        sharding.allreduce_partials(buf)
+        q.put((rank, buf.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_plan_tiles_unit_space():
+    for U in (1, 2, 7, 55, 30_517_578):
+        for world in (1, 2, 4, 8):
+            plan = sharding.shard_plan(U, world)
+            assert sum(e - b for b, e in plan) == U
+            sizes = [e - b for b, e in plan]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        sharding.shard_range(10, 2, 2)
+
+
+def test_gloo_world2_partials_sum_to_oracle():
+    import cases
+    from conftest import graph_from
+    from oracle import glare_oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = graph_from(cases.lattice_stress)
+    c, d = O.crossing_scan(g.xy, g.edges, IDEAL)
+    occ = O.node_occlusion(g.xy, 1.0)
+    for rank in (0, 1):
+        rc, rd, ro = results[rank]
+        assert rc == c == 4194903
+        assert abs(rd - d) <= 1e-9 * abs(d)
+        assert ro == occ == 9588
