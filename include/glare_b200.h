@@ -77,28 +77,29 @@ int glr_crossing_tile(void);
  * glr_occlusion_units with T = ceil(m / glr_crossing_tile())). */
 uint64_t glr_crossing_units(int64_t m);
 
-/* Bytes of the per-edge record buffer glr_crossing_prepare fills. */
-size_t glr_crossing_records_bytes(int64_t m);
+/* Bytes of the record buffer glr_crossing_prepare fills for n vertices and
+ * m edges (caller allocates, 256-byte aligned). */
+size_t glr_crossing_records_bytes(int64_t n, int64_t m);
 
 /* Builds the per-edge records (endpoint coordinates a = xy[edges[:,0]],
  * b = xy[edges[:,1]], b - a, exact order-preserving 32-bit bbox ranks, axis
- * angle theta = mod(atan2(by-ay, bx-ax), pi), endpoint ids) into d_records
- * (glr_crossing_records_bytes(m) bytes, 16-byte aligned).  Also decides
- * whether the input admits the fast sign path; the decision
- * is stored in the records header. */
+ * angle theta = mod(atan2(by-ay, bx-ax), pi), endpoint ids) and the
+ * per-vertex incidence lists into d_records.  Also decides whether the input
+ * admits the fast sign path (every nonzero |coordinate| in [2^-160, 2^500],
+ * see DESIGN.md); the decision is stored in the records header. */
 int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges,
                          int64_t m, void *d_records, void *stream);
 
 /* Writes to d_out[0..1] the partial (count, dev_sum) of the crossing scan
- * over units [unit_begin, unit_end) of prepared records: count of unordered
- * edge pairs with closed-bbox overlap, no shared vertex index and the
- * straddle predicate of geometry.py:62-79; dev_sum = sum over those pairs of
- * |ideal - min(d, pi - d)|, d = |theta_i - theta_j| (0 when !with_angle).
- * If unit_begin == 0 the partial also carries the whole-graph terms, so
- * partials of a disjoint cover of [0, units) sum to exact.py's result. */
-int glr_crossing_pairs(const void *d_records, int64_t m, int with_angle,
-                       double ideal, uint64_t unit_begin, uint64_t unit_end,
-                       double *d_out, void *stream);
+ * restricted to edge pairs (i < j) whose tile pair (i / tile, j / tile) lies
+ * in units [unit_begin, unit_end): count of pairs with closed-bbox overlap,
+ * no shared vertex index and the straddle predicate of geometry.py:62-79;
+ * dev_sum = sum over those pairs of |ideal - min(d, pi - d)|,
+ * d = |theta_i - theta_j| (0 when !with_angle).  Partials of a disjoint cover
+ * of [0, glr_crossing_units(m)) sum exactly (counts) to exact.py's result. */
+int glr_crossing_pairs(const void *d_records, int64_t n, int64_t m,
+                       int with_angle, double ideal, uint64_t unit_begin,
+                       uint64_t unit_end, double *d_out, void *stream);
 
 /* prepare + pairs over [unit_begin, unit_end) with internal scratch. */
 int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,

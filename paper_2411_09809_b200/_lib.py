@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libglare_b200.so")
+# GLARE_B200_LIB points at an alternative build (tuning sweeps in tools/).
+LIB_PATH = os.environ.get("GLARE_B200_LIB") or os.path.join(_HERE, "_lib", "libglare_b200.so")
 
 GLR_OK = 0
 GLR_EARG = 1
@@ -32,15 +33,15 @@ SIGNATURES = {
     ),
     "glr_crossing_tile": (_c.c_int, []),
     "glr_crossing_units": (_c.c_uint64, [_c.c_int64]),
-    "glr_crossing_records_bytes": (_c.c_size_t, [_c.c_int64]),
+    "glr_crossing_records_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int64]),
     "glr_crossing_prepare": (
         _c.c_int,
         [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p],
     ),
     "glr_crossing_pairs": (
         _c.c_int,
-        [_c.c_void_p, _c.c_int64, _c.c_int, _c.c_double, _c.c_uint64, _c.c_uint64,
-         _c.c_void_p, _c.c_void_p],
+        [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_double, _c.c_uint64,
+         _c.c_uint64, _c.c_void_p, _c.c_void_p],
     ),
     "glr_crossing_scan": (
         _c.c_int,

@@ -16,17 +16,25 @@
 // contiguous unit range; each thread keeps K i-edges in registers and streams
 // the j-tile from shared memory (broadcast LDS, no bank conflicts).
 //
-// FP64 budget per pair (fast path): 6 DADD coordinate differences, 8 DMUL,
-// 4 DADD for c1..c4 = 18 FP64 instructions (c3 reuses the c1 differences:
+// FP64 budget per pair: 6 DADD coordinate differences, 8 DMUL, 4 DADD for
+// c1..c4 = 18 FP64 instructions (c3 reuses the c1 differences:
 // fl(ay-cy) = -fl(cy-ay) exactly).  Everything else runs on the ALU/FMA pipes:
-//  - bbox: exact 32-bit dense ranks of xmin/xmax/ymin/ymax (rank order ==
-//    double order, built by glr_crossing_prepare), 4 ISETP;
-//  - signs: the high word of each c, viewed as a float, has the sign of c and
-//    is zero iff c == 0 whenever every nonzero |coordinate| lies in
-//    [2^-400, 2^500]; straddle(c1,c2) AND
-//    straddle(c3,c4) == max(min(f1,f2), min(f3,f4)) <= 0 <= min(max(f1,f2),
-//    max(f3,f4)).  Inputs outside that range use the general kernel, which
-//    compares the doubles themselves.
+//  - bbox: exact 32-bit ranks of xmin/xmax/ymin/ymax (rank order == double
+//    order, built by glr_crossing_prepare), 4 ISETP;
+//  - signs (fast path): the high word of each c, viewed as a float f, has the
+//    sign of c, is zero iff c == 0 and lies in [2^-53, 2^127) whenever every
+//    nonzero |coordinate| lies in [2^-160, 2^500] (DESIGN.md "fast sign
+//    path"), so straddle(c1,c2) == (f1*f2 <= 0) with an FP32 FMUL that cannot
+//    underflow: 2 FMUL (FMA pipe) + 2 FSETP;
+//  - shared vertices (fast path): NOT tested per pair.  Two distinct edges
+//    that share a vertex index always pass the fast predicate (their bboxes
+//    share the point, and one of c1/c2 and one of c3/c4 is exactly 0 --
+//    DESIGN.md), so the kernel counts them and adj_kernel subtracts them:
+//    sum over vertices of C(deg, 2) pairs, each assigned to its tile-pair
+//    unit so unit-range partials stay exact.
+// Inputs outside the fast window use the general instantiation, which
+// compares the doubles themselves (numpy's NaN-is-false semantics) and tests
+// vertex ids per pair.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -34,55 +42,89 @@
 namespace glr {
 namespace {
 
-constexpr int kThreads = 128;  // threads per CTA
-constexpr int kK = 4;          // i-edges per thread
+// Tunables (overridable at build time for the tuning sweeps in tools/).
+#ifndef GLR_XTHREADS
+#define GLR_XTHREADS 128
+#endif
+#ifndef GLR_XK
+#define GLR_XK 4
+#endif
+#ifndef GLR_XMINB
+#define GLR_XMINB 3
+#endif
+constexpr int kThreads = GLR_XTHREADS;  // threads per CTA
+constexpr int kK = GLR_XK;              // i-edges per thread
 constexpr int kTile = kThreads * kK;
-constexpr int kMinBlocks = 3;  // CTAs per SM
+constexpr int kMinBlocks = GLR_XMINB;   // CTAs per SM
+constexpr int kAdjTile = 128;           // incidence-list tile of adj_kernel
 
-// Fast sign path admissibility bounds on nonzero |coordinate|.
+// Fast sign path admissibility bounds on nonzero |coordinate| (DESIGN.md 4).
 constexpr double kMaxAbsFast = 0x1p500;
-constexpr double kMinAbsFast = 0x1p-400;
+constexpr double kMinAbsFast = 0x1p-160;
 
 struct __align__(16) EdgeRec {
-  double ax, ay, bx, by;  // a = xy[edges[:,0]], b = xy[edges[:,1]]
-  double abx, aby;        // b - a  (geometry.py:69-70)
+  double ax, ay, bx, by;           // a = xy[edges[:,0]], b = xy[edges[:,1]]
+  double abx, aby;                 // b - a  (geometry.py:69-70)
   int rxmin, rxmax, rymin, rymax;  // exact order-preserving bbox ranks
 };
 static_assert(sizeof(EdgeRec) == 64, "EdgeRec must be 64 bytes");
 
 struct __align__(16) RecHeader {
-  int fast;          // 1: fast sign path admissible
+  int fast;  // 1: fast sign path admissible
   int pad0;
+  long long n;
   long long m;
   long long m_pad;
-  unsigned long long maxabs_bits;   // max |coord| (bit pattern)
-  unsigned long long minabs_bits;   // min nonzero |coord| (bit pattern)
-  char pad[216];
+  unsigned long long maxabs_bits;  // max |coord| (bit pattern)
+  unsigned long long minabs_bits;  // min nonzero |coord| (bit pattern)
+  char pad[208];
 };
 static_assert(sizeof(RecHeader) == 256, "RecHeader must be 256 bytes");
 
+// Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
+// inc[2m] (incident edge ids grouped by vertex) | offs[n+1] | wofs[n+1].
 struct RecView {
   RecHeader *hdr;
   EdgeRec *rec;
   double *theta;
   int2 *ids;
+  int *inc;
+  int *offs;
+  long long *wofs;
 };
 
 inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; }
+inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-inline size_t records_bytes(int64_t m) {
-  int64_t mp = pad_edges(m < 1 ? 1 : m);
-  return sizeof(RecHeader) + (size_t)mp * (sizeof(EdgeRec) + sizeof(double) + sizeof(int2));
+struct Layout {
+  size_t rec, theta, ids, inc, offs, wofs, total;
+};
+
+inline Layout layout(int64_t n, int64_t m) {
+  const int64_t mp = pad_edges(m < 1 ? 1 : m);
+  const int64_t nn = n < 0 ? 0 : n;
+  Layout L;
+  L.rec = sizeof(RecHeader);
+  L.theta = L.rec + al256((size_t)mp * sizeof(EdgeRec));
+  L.ids = L.theta + al256((size_t)mp * sizeof(double));
+  L.inc = L.ids + al256((size_t)mp * sizeof(int2));
+  L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
+  L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
+  L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
+  return L;
 }
 
-inline RecView view(void *base, int64_t m) {
-  int64_t mp = pad_edges(m < 1 ? 1 : m);
+inline RecView view(void *base, int64_t n, int64_t m) {
+  const Layout L = layout(n, m);
   char *p = reinterpret_cast<char *>(base);
   RecView v;
   v.hdr = reinterpret_cast<RecHeader *>(p);
-  v.rec = reinterpret_cast<EdgeRec *>(p + sizeof(RecHeader));
-  v.theta = reinterpret_cast<double *>(p + sizeof(RecHeader) + mp * sizeof(EdgeRec));
-  v.ids = reinterpret_cast<int2 *>(p + sizeof(RecHeader) + mp * (sizeof(EdgeRec) + sizeof(double)));
+  v.rec = reinterpret_cast<EdgeRec *>(p + L.rec);
+  v.theta = reinterpret_cast<double *>(p + L.theta);
+  v.ids = reinterpret_cast<int2 *>(p + L.ids);
+  v.inc = reinterpret_cast<int *>(p + L.inc);
+  v.offs = reinterpret_cast<int *>(p + L.offs);
+  v.wofs = reinterpret_cast<long long *>(p + L.wofs);
   return v;
 }
 
@@ -102,7 +144,8 @@ __device__ inline double mod_pi(double x) {
 // ---------------------------------------------------------------- prepare --
 
 __global__ void gather_kernel(const double2 *__restrict__ xy, const longlong2 *__restrict__ edges,
-                              int64_t m, int64_t m_pad, RecView rv, double *xs, double *ys) {
+                              int64_t m, int64_t m_pad, RecView rv, double *xs, double *ys,
+                              int *deg, int *keys, int *vals) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m_pad;
        e += (int64_t)gridDim.x * blockDim.x) {
     EdgeRec r;
@@ -120,6 +163,12 @@ __global__ void gather_kernel(const double2 *__restrict__ xy, const longlong2 *_
       xs[m + e] = fmax(a.x, b.x);
       ys[e] = fmin(a.y, b.y);
       ys[m + e] = fmax(a.y, b.y);
+      atomicAdd(&deg[uv.x], 1);
+      atomicAdd(&deg[uv.y], 1);
+      keys[e] = (int)uv.x;
+      keys[m + e] = (int)uv.y;
+      vals[e] = (int)e;
+      vals[m + e] = (int)e;
     } else {
       // padding: zero coordinates, empty bbox (never overlaps), unique ids
       r.ax = r.ay = r.bx = r.by = r.abx = r.aby = 0.0;
@@ -155,6 +204,17 @@ __global__ void rank_kernel(int64_t m, RecView rv, const double *xs, const doubl
   }
 }
 
+// Adjacent-pair work units per vertex: the C(deg,2) pairs of its incidence
+// list, tiled kAdjTile x kAdjTile over the upper triangle.
+__global__ void adj_units_kernel(const int *__restrict__ deg, int64_t n, long long *wunits) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    long long d = v < n ? deg[v] : 0;
+    long long T = (d + kAdjTile - 1) / kAdjTile;
+    wunits[v] = d >= 2 ? T * (T + 1) / 2 : 0;
+  }
+}
+
 // max |c| and min nonzero |c| over all coordinates, as ordered bit patterns.
 __global__ void magnitude_kernel(const double *__restrict__ xy, int64_t count,
                                  unsigned long long *maxb, unsigned long long *minb) {
@@ -177,11 +237,12 @@ __global__ void magnitude_kernel(const double *__restrict__ xy, int64_t count,
   }
 }
 
-__global__ void header_kernel(RecHeader *hdr, int64_t m, int64_t m_pad,
+__global__ void header_kernel(RecHeader *hdr, int64_t n, int64_t m, int64_t m_pad,
                               const unsigned long long *maxb, const unsigned long long *minb) {
   unsigned long long mx = *maxb, mn = *minb;
   double dmx = __longlong_as_double((long long)mx);
   double dmn = mn == ~0ull ? 1.0 : __longlong_as_double((long long)mn);
+  hdr->n = n;
   hdr->m = m;
   hdr->m_pad = m_pad;
   hdr->maxabs_bits = mx;
@@ -191,13 +252,15 @@ __global__ void header_kernel(RecHeader *hdr, int64_t m, int64_t m_pad,
 
 // ------------------------------------------------------------ pair kernels --
 
+template <bool IDS>
 struct IRegs {
   double ax[kK], ay[kK], bx[kK], by[kK], abx[kK], aby[kK], th[kK];
-  int rx0[kK], rx1[kK], ry0[kK], ry1[kK], u[kK], v[kK];
+  int rx0[kK], rx1[kK], ry0[kK], ry1[kK];
+  int u[IDS ? kK : 1], v[IDS ? kK : 1];
 };
 
-template <bool ANGLE>
-__device__ inline void load_i(IRegs &R, const EdgeRec *__restrict__ rec,
+template <bool IDS, bool ANGLE>
+__device__ inline void load_i(IRegs<IDS> &R, const EdgeRec *__restrict__ rec,
                               const double *__restrict__ theta, const int2 *__restrict__ ids,
                               uint64_t ti) {
 #pragma unroll
@@ -210,8 +273,10 @@ __device__ inline void load_i(IRegs &R, const EdgeRec *__restrict__ rec,
     R.ax[k] = q0.x; R.ay[k] = q0.y; R.bx[k] = q0.z; R.by[k] = q0.w;
     R.abx[k] = q1.x; R.aby[k] = q1.y;
     R.rx0[k] = rk.x; R.rx1[k] = rk.y; R.ry0[k] = rk.z; R.ry1[k] = rk.w;
-    int2 id = ids[e];
-    R.u[k] = id.x; R.v[k] = id.y;
+    if (IDS) {
+      int2 id = ids[e];
+      R.u[k] = id.x; R.v[k] = id.y;
+    }
     R.th[k] = ANGLE ? theta[e] : 0.0;
   }
 }
@@ -220,6 +285,7 @@ __device__ inline float hi_view(double c) { return __int_as_float(__double2hiint
 
 // |ideal - min(d, pi - d)| with d = |t1 - t2|, written as
 // || pi/2 - d | - kappa|, kappa = pi/2 - ideal (4 DADD, no DMNMX).
+// Symmetric in (t1, t2) bit for bit.
 __device__ inline double angle_dev(double t1, double t2, double kappa) {
   const double HALF_PI = 1.5707963267948966;
   double d = __dsub_rn(t1, t2);
@@ -228,25 +294,27 @@ __device__ inline double angle_dev(double t1, double t2, double kappa) {
 }
 
 // One j-edge against the thread's K i-edges.  FAST selects the float-view
-// sign test; otherwise the doubles are compared directly (NaN -> false, as
-// numpy).  DIAG masks pairs with j <= i inside a diagonal tile.
+// sign test and skips the vertex-id test (corrected by adj_kernel); otherwise
+// the doubles are compared directly (NaN -> false, as numpy) and ids are
+// tested.  DIAG masks pairs with j <= i inside a diagonal tile.
 template <bool FAST, bool ANGLE, bool DIAG>
-__device__ inline void pair_row(const IRegs &R, const EdgeRec *sj, const double *sth,
+__device__ inline void pair_row(const IRegs<!FAST> &R, const EdgeRec *sj, const double *sth,
                                 const int2 *sid, int jj, unsigned (&cnt)[kK],
                                 double (&dev)[kK], double kappa) {
   const double4 cq = reinterpret_cast<const double4 *>(sj + jj)[0];
   const double2 cdq = reinterpret_cast<const double2 *>(sj + jj)[2];
   const int4 rk = reinterpret_cast<const int4 *>(sj + jj)[3];
-  const int2 idj = sid[jj];
   const double cx = cq.x, cy = cq.y, dx = cq.z, dy = cq.w;
   const double cdx = cdq.x, cdy = cdq.y;
   const double thj = ANGLE ? sth[jj] : 0.0;
+  int2 idj = make_int2(0, 0);
+  if (!FAST) idj = sid[jj];
 #pragma unroll
   for (int k = 0; k < kK; ++k) {
     // closed bbox overlap via exact ranks (exact.py:191-194)
     bool ok = (rk.y >= R.rx0[k]) & (R.rx1[k] >= rk.x) & (rk.w >= R.ry0[k]) & (R.ry1[k] >= rk.z);
-    // no shared vertex index (exact.py:205-210)
-    ok &= (R.u[k] != idj.x) & (R.u[k] != idj.y) & (R.v[k] != idj.x) & (R.v[k] != idj.y);
+    if (!FAST)  // no shared vertex index (exact.py:205-210)
+      ok &= (R.u[k] != idj.x) & (R.u[k] != idj.y) & (R.v[k] != idj.x) & (R.v[k] != idj.y);
     if (DIAG) ok &= jj > (int)threadIdx.x + k * kThreads;
     // coordinate differences: (cx-ax), (cy-ay), (dx-ax), (dy-ay), (bx-cx), (by-cy)
     const double dcx = __dsub_rn(cx, R.ax[k]);
@@ -262,10 +330,11 @@ __device__ inline void pair_row(const IRegs &R, const EdgeRec *sj, const double 
     const double c4 = __dsub_rn(__dmul_rn(cdx, eby), __dmul_rn(cdy, ebx));
     bool hit;
     if (FAST) {
-      const float f1 = hi_view(c1), f2 = hi_view(c2), f3 = hi_view(c3), f4 = hi_view(c4);
-      const float lo = fmaxf(fminf(f1, f2), fminf(f3, f4));
-      const float hi = fminf(fmaxf(f1, f2), fmaxf(f3, f4));
-      hit = ok & (lo <= 0.0f) & (hi >= 0.0f);
+      // sign(f1*f2) = sign(c1)*sign(c2), zero iff c1 or c2 is zero; the
+      // product never underflows or turns NaN inside the fast window
+      const float p12 = __fmul_rn(hi_view(c1), hi_view(c2));
+      const float p34 = __fmul_rn(hi_view(c3), hi_view(c4));
+      hit = ok & (p12 <= 0.0f) & (p34 <= 0.0f);
     } else {
       const bool s_cd = ((c1 <= 0.0) & (c2 >= 0.0)) | ((c1 >= 0.0) & (c2 <= 0.0));
       const bool s_ab = ((c3 <= 0.0) & (c4 >= 0.0)) | ((c3 >= 0.0) & (c4 <= 0.0));
@@ -286,9 +355,10 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                    uint64_t ubeg, uint64_t uend, double kappa,
                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != (FAST ? 1 : 0)) return;
+  constexpr bool IDS = !FAST;
   __shared__ __align__(16) EdgeRec sj[kTile];
   __shared__ double sth[ANGLE ? kTile : 1];
-  __shared__ int2 sid[kTile];
+  __shared__ int2 sid[IDS ? kTile : 1];
   __shared__ unsigned long long red_u[kThreads / 32];
   __shared__ double red_d[kThreads / 32];
 
@@ -298,12 +368,12 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
 
   unsigned long long total = 0;
   double dsum = 0.0, dcomp = 0.0;  // Kahan over per-unit partials
-  IRegs R;
+  IRegs<IDS> R;
   uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
   if (b < e) tri_unit_coords(b, T, &ti, &tj);
   for (uint64_t u = b; u < e; ++u) {
     if (ti != cur_ti) {
-      load_i<ANGLE>(R, rec, theta, ids, ti);
+      load_i<IDS, ANGLE>(R, rec, theta, ids, ti);
       cur_ti = ti;
     }
     __syncthreads();  // previous tile fully consumed
@@ -313,7 +383,7 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
 #pragma unroll 4
       for (int q = threadIdx.x; q < kTile * 4; q += kThreads) dst[q] = src[q];
       for (int q = threadIdx.x; q < kTile; q += kThreads) {
-        sid[q] = ids[(int64_t)tj * kTile + q];
+        if (IDS) sid[q] = ids[(int64_t)tj * kTile + q];
         if (ANGLE) sth[q] = theta[(int64_t)tj * kTile + q];
       }
     }
@@ -351,13 +421,97 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   }
 }
 
+// Adjacent edge pairs (sharing a vertex index) whose tile-pair unit lies in
+// [ubeg, uend): count and angle-deviation sum, subtracted from the fast
+// kernel's totals.  One CTA per (vertex, incidence tile pair) work item,
+// grid-stride; fixed grid and order, so results are deterministic.
+template <bool ANGLE>
+__global__ void __launch_bounds__(kAdjTile)
+adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
+           const int *__restrict__ inc, const int *__restrict__ offs,
+           const long long *__restrict__ wofs, uint64_t T, uint64_t ubeg, uint64_t uend,
+           double kappa, unsigned long long *__restrict__ part_cnt,
+           double *__restrict__ part_dev) {
+  __shared__ int s_e[kAdjTile];
+  __shared__ double s_t[kAdjTile];
+  __shared__ long long s_v;
+  __shared__ unsigned long long red_u[kAdjTile / 32];
+  __shared__ double red_d[kAdjTile / 32];
+  if (hdr->fast != 1) {  // general path tests ids per pair: nothing to remove
+    if (threadIdx.x == 0) {
+      part_cnt[blockIdx.x] = 0;
+      part_dev[blockIdx.x] = 0.0;
+    }
+    return;
+  }
+  const long long n = hdr->n;
+  const long long W = wofs[n];
+  unsigned long long cnt = 0;
+  double dsum = 0.0, dcomp = 0.0;
+  for (long long w = blockIdx.x; w < W; w += gridDim.x) {
+    if (threadIdx.x == 0) {  // vertex owning work item w: last v with wofs[v] <= w
+      long long lo = 0, hi = n;
+      while (lo < hi) {
+        long long mid = (lo + hi + 1) >> 1;
+        if (wofs[mid] <= w) lo = mid; else hi = mid - 1;
+      }
+      s_v = lo;
+    }
+    __syncthreads();
+    const long long v = s_v;
+    const int base = offs[v];
+    const int d = offs[v + 1] - base;
+    const uint64_t Tv = (uint64_t)(d + kAdjTile - 1) / kAdjTile;
+    uint64_t ti, tj;
+    tri_unit_coords((uint64_t)(w - wofs[v]), Tv, &ti, &tj);
+    const int q0 = (int)tj * kAdjTile;
+    if (q0 + (int)threadIdx.x < d) {
+      const int ej = inc[base + q0 + threadIdx.x];
+      s_e[threadIdx.x] = ej;
+      s_t[threadIdx.x] = ANGLE ? theta[ej] : 0.0;
+    }
+    __syncthreads();
+    const int p = (int)ti * kAdjTile + threadIdx.x;
+    double s = 0.0;
+    if (p < d) {
+      const int e1 = inc[base + p];
+      const double t1 = ANGLE ? theta[e1] : 0.0;
+      const int qn = min(kAdjTile, d - q0);
+      for (int qq = (ti == tj) ? (int)threadIdx.x + 1 : 0; qq < qn; ++qq) {
+        const int e2 = s_e[qq];
+        const uint64_t lo = (uint64_t)min(e1, e2) / kTile, hi = (uint64_t)max(e1, e2) / kTile;
+        const uint64_t unit = tri_row_start(lo, T) + (hi - lo);
+        if (unit >= ubeg && unit < uend) {
+          ++cnt;
+          if (ANGLE) s = __dadd_rn(s, angle_dev(t1, s_t[qq], kappa));
+        }
+      }
+    }
+    if (ANGLE) {
+      double y = __dsub_rn(s, dcomp);
+      double t = __dadd_rn(dsum, y);
+      dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
+      dsum = t;
+    }
+    __syncthreads();
+  }
+  unsigned long long bc = block_sum_u64<kAdjTile>(cnt, red_u);
+  double bd = block_sum<kAdjTile>(dsum, red_d);
+  if (threadIdx.x == 0) {
+    part_cnt[blockIdx.x] = bc;
+    part_dev[blockIdx.x] = bd;
+  }
+}
+
 __global__ void cross_finalize_kernel(const unsigned long long *cta_cnt, const double *cta_dev,
-                                      int ncta, double *out) {
+                                      int ncta, const unsigned long long *adj_cnt,
+                                      const double *adj_dev, int nadj, double *out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    unsigned long long c = 0;
+    unsigned long long c = 0, a = 0;
     for (int i = 0; i < ncta; ++i) c += cta_cnt[i];
-    out[0] = (double)c;
-    out[1] = kahan_sum(cta_dev, ncta);
+    for (int i = 0; i < nadj; ++i) a += adj_cnt[i];
+    out[0] = (double)(c - a);
+    out[1] = __dsub_rn(kahan_sum(cta_dev, ncta), kahan_sum(adj_dev, nadj));
   }
 }
 
@@ -365,6 +519,19 @@ int grid_for(uint64_t units) {
   uint64_t g = (uint64_t)sm_count() * kMinBlocks;
   if (units < g) g = units;
   return (int)(g < 1 ? 1 : g);
+}
+
+int blocks_for(int64_t work, int nt, int per_sm) {
+  int64_t b = (work + nt - 1) / nt;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 31 && ((int64_t)1 << b) <= n) ++b;
+  return b;
 }
 
 }  // namespace
@@ -376,69 +543,103 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
               (long long)m);
     return GLR_EARG;
   }
-  if (m >= (int64_t)1 << 30) {
-    set_error("glr_crossing_prepare: m=%lld exceeds the int32 rank range", (long long)m);
+  if (m >= (int64_t)1 << 29 || n >= (int64_t)1 << 31) {
+    set_error("glr_crossing_prepare: n=%lld, m=%lld exceed the 32-bit index range",
+              (long long)n, (long long)m);
     return GLR_EARG;
   }
-  if (reinterpret_cast<uintptr_t>(d_records) % 16 != 0) {
-    set_error("glr_crossing_prepare: records buffer must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(d_records) % 256 != 0) {
+    set_error("glr_crossing_prepare: records buffer must be 256-byte aligned");
     return GLR_EARG;
   }
   const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
-  RecView rv = view(d_records, m);
-  const int64_t mm = m < 1 ? 0 : m;
-  // scratch: xs[2m], ys[2m], sorted xs/ys [2m each], 2 magnitude words, cub temp
-  size_t cub_bytes = 0;
-  if (mm > 0)
-    GLR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, cub_bytes, (const double *)nullptr,
+  RecView rv = view(d_records, n, m);
+  const int64_t mm = m;
+  // scratch: xs, ys, sorted xs, sorted ys (2m f64 each); deg (n+1), sort keys
+  // in/out (2m i32 each), sort values in (2m), work units (n+1 i64); two
+  // magnitude words; CUB temp
+  size_t t_sort = 0, t_pairs = 0, t_scan = 0, t_scan64 = 0;
+  if (mm > 0) {
+    GLR_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t_sort, (const double *)nullptr,
                                             (double *)nullptr, (int)(2 * mm), 0, 64, st));
-  const size_t arr = (size_t)(2 * mm) * sizeof(double);
-  const size_t arr_al = (arr + 255) & ~(size_t)255;
-  Scratch scr(4 * arr_al + 256 + cub_bytes, st);
+    GLR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_pairs, (const int *)nullptr, (int *)nullptr,
+                                             (const int *)nullptr, (int *)nullptr, (int)(2 * mm), 0,
+                                             bits_for(n), st));
+  }
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (int *)nullptr, (int *)nullptr,
+                                         (int)(n + 1), st));
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan64, (long long *)nullptr,
+                                         (long long *)nullptr, (int)(n + 1), st));
+  size_t t_cub = t_sort;
+  if (t_pairs > t_cub) t_cub = t_pairs;
+  if (t_scan > t_cub) t_cub = t_scan;
+  if (t_scan64 > t_cub) t_cub = t_scan64;
+  const size_t a_f64 = al256((size_t)(2 * mm) * sizeof(double));
+  const size_t a_i32 = al256((size_t)(2 * mm) * sizeof(int));
+  const size_t a_deg = al256((size_t)(n + 1) * sizeof(int));
+  const size_t a_wu = al256((size_t)(n + 1) * sizeof(long long));
+  Scratch scr(4 * a_f64 + 3 * a_i32 + a_deg + a_wu + 256 + t_cub, st);
   GLR_CUDA(scr.err);
   char *base = scr.as<char>();
   double *xs = reinterpret_cast<double *>(base);
-  double *ys = reinterpret_cast<double *>(base + arr_al);
-  double *sx = reinterpret_cast<double *>(base + 2 * arr_al);
-  double *sy = reinterpret_cast<double *>(base + 3 * arr_al);
-  unsigned long long *mag = reinterpret_cast<unsigned long long *>(base + 4 * arr_al);
-  void *cub_tmp = base + 4 * arr_al + 256;
+  double *ys = reinterpret_cast<double *>(base + a_f64);
+  double *sx = reinterpret_cast<double *>(base + 2 * a_f64);
+  double *sy = reinterpret_cast<double *>(base + 3 * a_f64);
+  char *p = base + 4 * a_f64;
+  int *keys = reinterpret_cast<int *>(p);
+  int *keys_out = reinterpret_cast<int *>(p + a_i32);
+  int *vals = reinterpret_cast<int *>(p + 2 * a_i32);
+  p += 3 * a_i32;
+  int *deg = reinterpret_cast<int *>(p);
+  long long *wunits = reinterpret_cast<long long *>(p + a_deg);
+  unsigned long long *mag = reinterpret_cast<unsigned long long *>(p + a_deg + a_wu);
+  void *cub_tmp = p + a_deg + a_wu + 256;
 
   const int nt = 256;
-  int blocks = (int)((m_pad + nt - 1) / nt);
-  if (blocks > sm_count() * 16) blocks = sm_count() * 16;
-  gather_kernel<<<blocks, nt, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
-                                       reinterpret_cast<const longlong2 *>(d_edges), mm, m_pad,
-                                       rv, xs, ys);
+  GLR_CUDA(cudaMemsetAsync(deg, 0, (size_t)(n + 1) * sizeof(int), st));
+  gather_kernel<<<blocks_for(m_pad, nt, 16), nt, 0, st>>>(
+      reinterpret_cast<const double2 *>(d_xy), reinterpret_cast<const longlong2 *>(d_edges), mm,
+      m_pad, rv, xs, ys, deg, keys, vals);
   GLR_LAUNCHED("gather_kernel");
+  size_t tb;
   if (mm > 0) {
-    size_t tb = cub_bytes;
+    tb = t_cub;
     GLR_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, xs, sx, (int)(2 * mm), 0, 64, st));
     count_launch(4);
-    tb = cub_bytes;
+    tb = t_cub;
     GLR_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, ys, sy, (int)(2 * mm), 0, 64, st));
     count_launch(4);
-    int rb = (int)((mm + nt - 1) / nt);
-    if (rb > sm_count() * 16) rb = sm_count() * 16;
-    rank_kernel<<<rb, nt, 0, st>>>(mm, rv, xs, ys, sx, sy);
+    rank_kernel<<<blocks_for(mm, nt, 16), nt, 0, st>>>(mm, rv, xs, ys, sx, sy);
     GLR_LAUNCHED("rank_kernel");
+    // incidence lists grouped by vertex; stable, so each list is ordered
+    // (edges where the vertex is first, then where it is second, by edge id)
+    tb = t_cub;
+    GLR_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, keys, keys_out, vals, rv.inc,
+                                             (int)(2 * mm), 0, bits_for(n), st));
+    count_launch(4);
   }
+  tb = t_cub;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, deg, rv.offs, (int)(n + 1), st));
+  count_launch(2);
+  adj_units_kernel<<<blocks_for(n + 1, nt, 8), nt, 0, st>>>(deg, n, wunits);
+  GLR_LAUNCHED("adj_units_kernel");
+  tb = t_cub;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, wunits, rv.wofs, (int)(n + 1), st));
+  count_launch(2);
   GLR_CUDA(cudaMemsetAsync(mag, 0x00, sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(mag + 1, 0xff, sizeof(unsigned long long), st));
   if (n > 0) {
-    int mb = (int)((2 * n + nt - 1) / nt);
-    if (mb > sm_count() * 8) mb = sm_count() * 8;
-    magnitude_kernel<<<mb, nt, 0, st>>>(d_xy, 2 * n, mag, mag + 1);
+    magnitude_kernel<<<blocks_for(2 * n, nt, 8), nt, 0, st>>>(d_xy, 2 * n, mag, mag + 1);
     GLR_LAUNCHED("magnitude_kernel");
   }
-  header_kernel<<<1, 1, 0, st>>>(rv.hdr, mm, m_pad, mag, mag + 1);
+  header_kernel<<<1, 1, 0, st>>>(rv.hdr, n, mm, m_pad, mag, mag + 1);
   GLR_LAUNCHED("header_kernel");
   return GLR_OK;
 }
 
-int crossing_pairs(const void *d_records, int64_t m, int with_angle, double ideal,
+int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                    uint64_t ubeg, uint64_t uend, double *d_out, cudaStream_t st) {
-  if (d_records == nullptr || d_out == nullptr || m < 0) {
+  if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0) {
     set_error("glr_crossing_pairs: invalid arguments");
     return GLR_EARG;
   }
@@ -458,12 +659,15 @@ int crossing_pairs(const void *d_records, int64_t m, int with_angle, double idea
     GLR_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), st));
     return GLR_OK;
   }
-  RecView rv = view(const_cast<void *>(d_records), m);
+  RecView rv = view(const_cast<void *>(d_records), n, m);
   const int grid = grid_for(uend - ubeg);
-  Scratch scr((size_t)grid * (sizeof(unsigned long long) + sizeof(double)), st);
+  const int agrid = sm_count() * 8;
+  Scratch scr((size_t)(grid + agrid) * (sizeof(unsigned long long) + sizeof(double)), st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
-  double *cd = reinterpret_cast<double *>(cc + grid);
+  unsigned long long *ac = cc + grid;
+  double *cd = reinterpret_cast<double *>(ac + agrid);
+  double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
   if (with_angle) {
     cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
@@ -472,6 +676,9 @@ int crossing_pairs(const void *d_records, int64_t m, int with_angle, double idea
     cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
                                                                ubeg, uend, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
+    adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
+                                                 ubeg, uend, kappa, ac, ad);
+    GLR_LAUNCHED("adj_kernel<angle>");
   } else {
     cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
                                                                ubeg, uend, 0.0, cc, cd);
@@ -479,8 +686,11 @@ int crossing_pairs(const void *d_records, int64_t m, int with_angle, double idea
     cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
                                                                 ubeg, uend, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
+    adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
+                                                  ubeg, uend, 0.0, ac, ad);
+    GLR_LAUNCHED("adj_kernel");
   }
-  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, d_out);
+  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, ac, ad, agrid, d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
   return GLR_OK;
 }
@@ -496,16 +706,16 @@ uint64_t glr_crossing_units(int64_t m) {
   return glr::tri_units((uint64_t)(m_pad / glr::kTile));
 }
 
-size_t glr_crossing_records_bytes(int64_t m) { return glr::records_bytes(m); }
+size_t glr_crossing_records_bytes(int64_t n, int64_t m) { return glr::layout(n, m).total; }
 
 int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
                          void *d_records, void *stream) {
   return glr::crossing_prepare(d_xy, n, d_edges, m, d_records, glr::as_stream(stream));
 }
 
-int glr_crossing_pairs(const void *d_records, int64_t m, int with_angle, double ideal,
+int glr_crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                        uint64_t unit_begin, uint64_t unit_end, double *d_out, void *stream) {
-  return glr::crossing_pairs(d_records, m, with_angle, ideal, unit_begin, unit_end, d_out,
+  return glr::crossing_pairs(d_records, n, m, with_angle, ideal, unit_begin, unit_end, d_out,
                              glr::as_stream(stream));
 }
 
@@ -513,11 +723,11 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
                       int with_angle, double ideal, uint64_t unit_begin, uint64_t unit_end,
                       double *d_out, void *stream) {
   cudaStream_t st = glr::as_stream(stream);
-  glr::Scratch rec(glr::records_bytes(m), st);
+  glr::Scratch rec(glr::layout(n, m).total, st);
   GLR_CUDA(rec.err);
   int rc = glr::crossing_prepare(d_xy, n, d_edges, m, rec.ptr, st);
   if (rc != GLR_OK) return rc;
-  return glr::crossing_pairs(rec.ptr, m, with_angle, ideal, unit_begin, unit_end, d_out, st);
+  return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, unit_begin, unit_end, d_out, st);
 }
 
 int glr_crossing_fast_path(const void *d_records, void *stream) {

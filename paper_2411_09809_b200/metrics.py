@@ -117,7 +117,8 @@ class CrossingRecords:
     def __init__(self, dg: DeviceGraph):
         L = _lib.lib()
         self.m = dg.num_edges
-        nbytes = int(L.glr_crossing_records_bytes(self.m))
+        self.n = dg.num_vertices
+        nbytes = int(L.glr_crossing_records_bytes(self.n, self.m))
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dg.xy.device)
         rc = L.glr_crossing_prepare(_ptr(dg.xy), dg.num_vertices,
                                     _ptr(dg.edges) if self.m else None, self.m,
@@ -137,7 +138,7 @@ class CrossingRecords:
         if out is None:
             out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
         rc = _lib.lib().glr_crossing_pairs(
-            _ptr(self.buf), self.m, 0 if ideal is None else 1,
+            _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
             0.0 if ideal is None else float(ideal), int(unit_begin), int(unit_end),
             _ptr(out), _stream())
         _lib.check(rc, "glr_crossing_pairs")

@@ -221,7 +221,8 @@ ADVERSARIAL_ARRAYS = {
     "huge_coords": lambda: scaled_lattice(2.0 ** 660),
     "tiny_coords": lambda: scaled_lattice(2.0 ** -990),
     "big_fast": lambda: scaled_lattice(2.0 ** 400),
-    "small_fast": lambda: scaled_lattice(2.0 ** -380),
+    "small_fast": lambda: scaled_lattice(2.0 ** -150),
+    "small_general": lambda: scaled_lattice(2.0 ** -300),
     "signed_zero_mix": signed_zero_mix,
 }
 
@@ -232,7 +233,8 @@ ADVERSARIAL_RADIUS = {
     "huge_coords": 2.0 ** 500,
     "tiny_coords": 2.0 ** -990,
     "big_fast": 2.0 ** 400,
-    "small_fast": 2.0 ** -380,
+    "small_fast": 2.0 ** -150,
+    "small_general": 2.0 ** -300,
     "signed_zero_mix": 0.25,
 }
 

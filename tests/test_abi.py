@@ -54,12 +54,12 @@ def test_host_only_entry_points(L):
     for n in (1, 2, vt, 3 * vt + 7, 1_500_000):
         T = -(-n // vt)
         assert L.glr_occlusion_units(n) == T * (T + 1) // 2
-    assert L.glr_crossing_records_bytes(1000) >= 1000 * 64
+    assert L.glr_crossing_records_bytes(500, 1000) >= 1000 * 64
 
 
 def test_argument_errors_reported_without_gpu(L):
     # invalid arguments are rejected before any CUDA call
-    rc = L.glr_crossing_pairs(None, 10, 0, 0.0, 0, 1, None, None)
+    rc = L.glr_crossing_pairs(None, 5, 10, 0, 0.0, 0, 1, None, None)
     assert rc == _lib.GLR_EARG
     assert b"invalid" in L.glr_last_error()
     rc = L.glr_occlusion_count(None, -1, 1.0, 0, 1, None, None)

@@ -81,7 +81,8 @@ def test_fast_and_general_sign_paths_selected(gpu):
     from paper_2411_09809_b200 import metrics as M
 
     for name, fast in (("lattice_stress", True), ("big_fast", True), ("small_fast", True),
-                       ("huge_coords", False), ("tiny_coords", False)):
+                       ("huge_coords", False), ("tiny_coords", False),
+                       ("small_general", False)):
         g = graph_from(cases.ADVERSARIAL_ARRAYS[name])
         assert M.CrossingRecords(M.DeviceGraph.from_graph(g)).fast_path() is fast, name
 
