@@ -52,10 +52,14 @@ namespace {
 #ifndef GLR_XMINB
 #define GLR_XMINB 3
 #endif
+#ifndef GLR_XUNROLL
+#define GLR_XUNROLL 2
+#endif
 constexpr int kThreads = GLR_XTHREADS;  // threads per CTA
 constexpr int kK = GLR_XK;              // i-edges per thread
 constexpr int kTile = kThreads * kK;
 constexpr int kMinBlocks = GLR_XMINB;   // CTAs per SM
+constexpr int kUnroll = GLR_XUNROLL;    // j-loop unroll of the off-diagonal tiles
 constexpr int kAdjTile = 128;           // incidence-list tile of adj_kernel
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
@@ -88,6 +92,7 @@ struct RecView {
   EdgeRec *rec;
   double *theta;
   int2 *ids;
+  int *newc;  // 1 if edge e starts a run of edges sharing endpoint a (or a tile)
   int *inc;
   int *offs;
   long long *wofs;
@@ -97,7 +102,7 @@ inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; 
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t rec, theta, ids, inc, offs, wofs, total;
+  size_t rec, theta, ids, newc, inc, offs, wofs, total;
 };
 
 inline Layout layout(int64_t n, int64_t m) {
@@ -107,7 +112,8 @@ inline Layout layout(int64_t n, int64_t m) {
   L.rec = sizeof(RecHeader);
   L.theta = L.rec + al256((size_t)mp * sizeof(EdgeRec));
   L.ids = L.theta + al256((size_t)mp * sizeof(double));
-  L.inc = L.ids + al256((size_t)mp * sizeof(int2));
+  L.newc = L.ids + al256((size_t)mp * sizeof(int2));
+  L.inc = L.newc + al256((size_t)mp * sizeof(int));
   L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
   L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
   L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
@@ -122,6 +128,7 @@ inline RecView view(void *base, int64_t n, int64_t m) {
   v.rec = reinterpret_cast<EdgeRec *>(p + L.rec);
   v.theta = reinterpret_cast<double *>(p + L.theta);
   v.ids = reinterpret_cast<int2 *>(p + L.ids);
+  v.newc = reinterpret_cast<int *>(p + L.newc);
   v.inc = reinterpret_cast<int *>(p + L.inc);
   v.offs = reinterpret_cast<int *>(p + L.offs);
   v.wofs = reinterpret_cast<long long *>(p + L.wofs);
@@ -159,6 +166,8 @@ __global__ void gather_kernel(const double2 *__restrict__ xy, const longlong2 *_
       // axis angle of a->b, geometry.py:94-97
       rv.theta[e] = mod_pi(atan2(r.aby, r.abx));
       rv.ids[e] = make_int2((int)uv.x, (int)uv.y);
+      // edges are sorted by their first endpoint: runs share a = xy[u]
+      rv.newc[e] = (e % kTile == 0 || edges[e - 1].x != uv.x) ? 1 : 0;
       xs[e] = fmin(a.x, b.x);
       xs[m + e] = fmax(a.x, b.x);
       ys[e] = fmin(a.y, b.y);
@@ -176,6 +185,7 @@ __global__ void gather_kernel(const double2 *__restrict__ xy, const longlong2 *_
       r.rxmax = r.rymax = -1;
       rv.theta[e] = 0.0;
       rv.ids[e] = make_int2(-1 - (int)(e - m), -1 - (int)(e - m));
+      rv.newc[e] = 1;
     }
     rv.rec[e] = r;
   }
@@ -348,17 +358,71 @@ __device__ inline void pair_row(const IRegs<!FAST> &R, const EdgeRec *sj, const 
   }
 }
 
+// Terms of a pair that depend on the i-edge and only the FIRST endpoint c of
+// the j-edge: (a,c) and (b,c) differences and c1 (as its float view).  The
+// j-tile is sorted by first endpoint, so consecutive j-edges sharing c reuse
+// them -- the `snew` flag is the same for every lane (j is broadcast), so the
+// branch never diverges.  Per pair this leaves 2 DADD (d - a) + 3 x (2 DMUL +
+// 1 DADD) for c2, c3, c4 = 11 FP64 instead of 18, bit-identical values.
+struct SRegs {
+  double dcx[kK], dcy[kK], ebx[kK], eby[kK];
+  float f1[kK];
+};
+
+template <bool ANGLE, bool DIAG>
+__device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const EdgeRec *sj,
+                                     const double *sth, const int *snew, int jj,
+                                     unsigned (&cnt)[kK], double (&dev)[kK], double kappa) {
+  const double4 cq = reinterpret_cast<const double4 *>(sj + jj)[0];
+  const double2 cdq = reinterpret_cast<const double2 *>(sj + jj)[2];
+  const int4 rk = reinterpret_cast<const int4 *>(sj + jj)[3];
+  const double cx = cq.x, cy = cq.y, dx = cq.z, dy = cq.w;
+  const double cdx = cdq.x, cdy = cdq.y;
+  const double thj = ANGLE ? sth[jj] : 0.0;
+  if (snew[jj]) {
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      S.dcx[k] = __dsub_rn(cx, R.ax[k]);
+      S.dcy[k] = __dsub_rn(cy, R.ay[k]);
+      S.ebx[k] = __dsub_rn(R.bx[k], cx);
+      S.eby[k] = __dsub_rn(R.by[k], cy);
+      S.f1[k] = hi_view(__dsub_rn(__dmul_rn(R.abx[k], S.dcy[k]), __dmul_rn(R.aby[k], S.dcx[k])));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kK; ++k) {
+    bool ok = (rk.y >= R.rx0[k]) & (R.rx1[k] >= rk.x) & (rk.w >= R.ry0[k]) & (R.ry1[k] >= rk.z);
+    if (DIAG) ok &= jj > (int)threadIdx.x + k * kThreads;
+    const double ddx = __dsub_rn(dx, R.ax[k]);
+    const double ddy = __dsub_rn(dy, R.ay[k]);
+    const double c2 = __dsub_rn(__dmul_rn(R.abx[k], ddy), __dmul_rn(R.aby[k], ddx));
+    const double c3 = __dsub_rn(__dmul_rn(cdy, S.dcx[k]), __dmul_rn(cdx, S.dcy[k]));
+    const double c4 = __dsub_rn(__dmul_rn(cdx, S.eby[k]), __dmul_rn(cdy, S.ebx[k]));
+    const float p12 = __fmul_rn(S.f1[k], hi_view(c2));
+    const float p34 = __fmul_rn(hi_view(c3), hi_view(c4));
+    const bool hit = ok & (p12 <= 0.0f) & (p34 <= 0.0f);
+    cnt[k] += hit ? 1u : 0u;
+    if (ANGLE) {
+      const double t = angle_dev(R.th[k], thj, kappa);
+      if (hit) dev[k] = __dadd_rn(dev[k], t);
+    }
+  }
+}
+
 template <bool FAST, bool ANGLE>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
-                   const double *__restrict__ theta, const int2 *__restrict__ ids, uint64_t T,
-                   uint64_t ubeg, uint64_t uend, double kappa,
-                   unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
+                   const double *__restrict__ theta, const int2 *__restrict__ ids,
+                   const int *__restrict__ newc, uint64_t T, uint64_t ubeg, uint64_t uend,
+                   double kappa, unsigned long long *__restrict__ cta_cnt,
+                   double *__restrict__ cta_dev) {
   if (hdr->fast != (FAST ? 1 : 0)) return;
   constexpr bool IDS = !FAST;
   __shared__ __align__(16) EdgeRec sj[kTile];
   __shared__ double sth[ANGLE ? kTile : 1];
   __shared__ int2 sid[IDS ? kTile : 1];
+  __shared__ int snew[FAST ? kTile : 1];
+  SRegs S;
   __shared__ unsigned long long red_u[kThreads / 32];
   __shared__ double red_d[kThreads / 32];
 
@@ -384,6 +448,7 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
       for (int q = threadIdx.x; q < kTile * 4; q += kThreads) dst[q] = src[q];
       for (int q = threadIdx.x; q < kTile; q += kThreads) {
         if (IDS) sid[q] = ids[(int64_t)tj * kTile + q];
+        if (FAST) snew[q] = newc[(int64_t)tj * kTile + q];
         if (ANGLE) sth[q] = theta[(int64_t)tj * kTile + q];
       }
     }
@@ -392,13 +457,24 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
     double dev[kK];
 #pragma unroll
     for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
-    if (ti == tj) {
-      for (int jj = 0; jj < kTile; ++jj)
-        pair_row<FAST, ANGLE, true>(R, sj, sth, sid, jj, cnt, dev, kappa);
+    if constexpr (FAST) {
+      if (ti == tj) {
+        for (int jj = 0; jj < kTile; ++jj)
+          pair_row_fast<ANGLE, true>(R, S, sj, sth, snew, jj, cnt, dev, kappa);
+      } else {
+#pragma unroll kUnroll
+        for (int jj = 0; jj < kTile; ++jj)
+          pair_row_fast<ANGLE, false>(R, S, sj, sth, snew, jj, cnt, dev, kappa);
+      }
     } else {
-#pragma unroll 2
-      for (int jj = 0; jj < kTile; ++jj)
-        pair_row<FAST, ANGLE, false>(R, sj, sth, sid, jj, cnt, dev, kappa);
+      if (ti == tj) {
+        for (int jj = 0; jj < kTile; ++jj)
+          pair_row<FAST, ANGLE, true>(R, sj, sth, sid, jj, cnt, dev, kappa);
+      } else {
+#pragma unroll kUnroll
+        for (int jj = 0; jj < kTile; ++jj)
+          pair_row<FAST, ANGLE, false>(R, sj, sth, sid, jj, cnt, dev, kappa);
+      }
     }
     unsigned c = 0;
     double s = 0.0;
@@ -670,20 +746,20 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
   if (with_angle) {
-    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
                                                               ubeg, uend, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
-    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
                                                                ubeg, uend, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
                                                  ubeg, uend, kappa, ac, ad);
     GLR_LAUNCHED("adj_kernel<angle>");
   } else {
-    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
                                                                ubeg, uend, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast>");
-    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, T,
+    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
                                                                 ubeg, uend, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
