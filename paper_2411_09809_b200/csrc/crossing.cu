@@ -42,18 +42,24 @@
 namespace glr {
 namespace {
 
-// Tunables (overridable at build time for the tuning sweeps in tools/).
+// Tunables (overridable at build time for the tuning sweeps in tools/;
+// defaults chosen by tools/variant_bench.py on a C5-shaped graph, see
+// profiles/r01_variants.txt: K=2 i-edges/thread, 4 CTAs/SM (16 warps), j-loop
+// unrolled 4x, PTX predicate tail).
 #ifndef GLR_XTHREADS
 #define GLR_XTHREADS 128
 #endif
 #ifndef GLR_XK
-#define GLR_XK 4
+#define GLR_XK 2
 #endif
 #ifndef GLR_XMINB
-#define GLR_XMINB 3
+#define GLR_XMINB 4
 #endif
 #ifndef GLR_XUNROLL
-#define GLR_XUNROLL 2
+#define GLR_XUNROLL 4
+#endif
+#ifndef GLR_XNOPTXTAIL
+#define GLR_XPTXTAIL 1
 #endif
 constexpr int kThreads = GLR_XTHREADS;  // threads per CTA
 constexpr int kK = GLR_XK;              // i-edges per thread
@@ -369,6 +375,43 @@ struct SRegs {
   float f1[kK];
 };
 
+// Hit test tail in PTX so it maps 1:1 onto ISETP/FSETP predicate chains and
+// predicated adds: bbox ranks (4 compares) AND p12 <= 0 AND p34 <= 0 AND the
+// diagonal mask, then @hit cnt += 1 (and dev += t).
+__device__ inline void tail_count(unsigned &cnt, int jx1, int ix0, int ix1, int jx0, int jy1,
+                                  int iy0, int iy1, int jy0, float p12, float p34, int diag_ok) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.s32 p, %1, %2;\n\t"
+      "setp.ge.and.s32 p, %3, %4, p;\n\t"
+      "setp.ge.and.s32 p, %5, %6, p;\n\t"
+      "setp.ge.and.s32 p, %7, %8, p;\n\t"
+      "setp.le.and.f32 p, %9, 0f00000000, p;\n\t"
+      "setp.le.and.f32 p, %10, 0f00000000, p;\n\t"
+      "setp.ne.and.s32 p, %11, 0, p;\n\t"
+      "@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(cnt)
+      : "r"(jx1), "r"(ix0), "r"(ix1), "r"(jx0), "r"(jy1), "r"(iy0), "r"(iy1), "r"(jy0),
+        "f"(p12), "f"(p34), "r"(diag_ok));
+}
+
+__device__ inline void tail_count_dev(unsigned &cnt, double &dev, double t, int jx1, int ix0,
+                                      int ix1, int jx0, int jy1, int iy0, int iy1, int jy0,
+                                      float p12, float p34, int diag_ok) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.s32 p, %2, %3;\n\t"
+      "setp.ge.and.s32 p, %4, %5, p;\n\t"
+      "setp.ge.and.s32 p, %6, %7, p;\n\t"
+      "setp.ge.and.s32 p, %8, %9, p;\n\t"
+      "setp.le.and.f32 p, %10, 0f00000000, p;\n\t"
+      "setp.le.and.f32 p, %11, 0f00000000, p;\n\t"
+      "setp.ne.and.s32 p, %12, 0, p;\n\t"
+      "@p add.u32 %0, %0, 1;\n\t"
+      "@p add.rn.f64 %1, %1, %13;\n\t}"
+      : "+r"(cnt), "+d"(dev)
+      : "r"(jx1), "r"(ix0), "r"(ix1), "r"(jx0), "r"(jy1), "r"(iy0), "r"(iy1), "r"(jy0),
+        "f"(p12), "f"(p34), "r"(diag_ok), "d"(t));
+}
+
 template <bool ANGLE, bool DIAG>
 __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const EdgeRec *sj,
                                      const double *sth, const int *snew, int jj,
@@ -400,12 +443,23 @@ __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const Edge
     const double c4 = __dsub_rn(__dmul_rn(cdx, S.eby[k]), __dmul_rn(cdy, S.ebx[k]));
     const float p12 = __fmul_rn(S.f1[k], hi_view(c2));
     const float p34 = __fmul_rn(hi_view(c3), hi_view(c4));
+#ifdef GLR_XPTXTAIL
+    (void)ok;
+    const int diag_ok = DIAG ? (jj > (int)threadIdx.x + k * kThreads) : 1;
+    if (ANGLE)
+      tail_count_dev(cnt[k], dev[k], angle_dev(R.th[k], thj, kappa), rk.y, R.rx0[k], R.rx1[k],
+                     rk.x, rk.w, R.ry0[k], R.ry1[k], rk.z, p12, p34, diag_ok);
+    else
+      tail_count(cnt[k], rk.y, R.rx0[k], R.rx1[k], rk.x, rk.w, R.ry0[k], R.ry1[k], rk.z, p12,
+                 p34, diag_ok);
+#else
     const bool hit = ok & (p12 <= 0.0f) & (p34 <= 0.0f);
     cnt[k] += hit ? 1u : 0u;
     if (ANGLE) {
       const double t = angle_dev(R.th[k], thj, kappa);
       if (hit) dev[k] = __dadd_rn(dev[k], t);
     }
+#endif
   }
 }
 
