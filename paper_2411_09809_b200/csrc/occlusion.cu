@@ -33,9 +33,15 @@ __device__ inline void occ_row(const double (&xi)[kK], const double (&yi)[kK], d
     const double dx = __dsub_rn(xi[k], pj.x);
     const double dy = __dsub_rn(yi[k], pj.y);
     const double s = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-    bool hit = (unsigned long long)__double_as_longlong(s) < thr_bits;
-    if (DIAG) hit &= jj > (int)threadIdx.x + k * kThreads;
-    cnt[k] += hit ? 1u : 0u;
+    const int diag_ok = DIAG ? (jj > (int)threadIdx.x + k * kThreads) : 1;
+    // s < thr as a 64-bit unsigned compare of bit patterns, then a predicated
+    // add (PTX keeps it to 2 ISETP + 1 IADD)
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.u64 p, %1, %2;\n\t"
+        "setp.ne.and.s32 p, %3, 0, p;\n\t"
+        "@p add.u32 %0, %0, 1;\n\t}"
+        : "+r"(cnt[k])
+        : "l"((unsigned long long)__double_as_longlong(s)), "l"(thr_bits), "r"(diag_ok));
   }
 }
 
