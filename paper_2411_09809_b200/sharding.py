@@ -52,7 +52,7 @@ def allreduce_partials(buf, group=None):
     group in place (NCCL on GPU ranks, gloo in the CPU tests)."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return buf
 
