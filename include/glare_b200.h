@@ -107,6 +107,52 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,
                       uint64_t unit_begin, uint64_t unit_end, double *d_out,
                       void *stream);
 
+/* ---- culled variants (results identical) ---------- */
+
+/* Writes to d_edges_out the edge list reordered by the Morton code of each
+ * edge's bbox centre (rows unchanged, only their order).  The metrics do not
+ * depend on edge order; spatially compact tiles let most tile pairs be
+ * skipped by glr_crossing_candidates. */
+int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
+                           int64_t m, int64_t *d_edges_out, void *stream);
+
+/* Writes to d_xy_out the vertex positions reordered by Morton code (node
+ * occlusion does not depend on vertex order). */
+int glr_spatial_sort_vertices(const double *d_xy, int64_t n, double *d_xy_out,
+                              void *stream);
+
+/* Candidate tile pairs of prepared records: every (ti <= tj) whose tile rank
+ * boxes overlap, row-major sorted, as int32 pairs (int2).  Synchronous:
+ * *h_count receives the number of candidates; the list is written only when
+ * d_list != NULL and capacity >= *h_count.  A pair with overlapping edge
+ * bboxes always lies in a candidate tile pair, so scanning the candidates
+ * gives exactly the dense result. */
+int glr_crossing_candidates(const void *d_records, int64_t n, int64_t m,
+                            void *d_list, uint64_t capacity, uint64_t *h_count,
+                            void *stream);
+
+/* glr_crossing_pairs over units [unit_begin, unit_end) of a candidate list
+ * (unit u = tile pair d_list[u]); partials of a disjoint cover of
+ * [0, list_len) sum to the dense result. */
+int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m,
+                            int with_angle, double ideal, const void *d_list,
+                            uint64_t list_len, uint64_t unit_begin,
+                            uint64_t unit_end, double *d_out, void *stream);
+
+/* Candidate vertex tile pairs: (ti <= tj) whose tile boxes are closer than
+ * reach = 2r on both axes (fl(gap) < reach); same protocol as
+ * glr_crossing_candidates.  Pairs in skipped tile pairs provably fail the
+ * strict test fl(fl(dx*dx)+fl(dy*dy)) < (2r)^2. */
+int glr_occlusion_candidates(const double *d_xy, int64_t n, double reach,
+                             void *d_list, uint64_t capacity, uint64_t *h_count,
+                             void *stream);
+
+/* glr_occlusion_count over units [unit_begin, unit_end) of a candidate list. */
+int glr_occlusion_count_list(const double *d_xy, int64_t n, double thr,
+                             const void *d_list, uint64_t list_len,
+                             uint64_t unit_begin, uint64_t unit_end,
+                             double *d_out, void *stream);
+
 /* ---- edge length variation: exact.py:127-142 ----------------------------- */
 
 /* d_out[0..2] = (mean length, sum of (l - mean)^2, M_l); M_l = 0.0 and the

@@ -58,6 +58,32 @@ SIGNATURES = {
     ),
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_take_launch_count": (_c.c_uint64, []),
+    "glr_spatial_sort_edges": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p],
+    ),
+    "glr_spatial_sort_vertices": (
+        _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p]),
+    "glr_crossing_candidates": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_uint64,
+         _c.POINTER(_c.c_uint64), _c.c_void_p],
+    ),
+    "glr_crossing_pairs_list": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_double, _c.c_void_p,
+         _c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_void_p],
+    ),
+    "glr_occlusion_candidates": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_double, _c.c_void_p, _c.c_uint64,
+         _c.POINTER(_c.c_uint64), _c.c_void_p],
+    ),
+    "glr_occlusion_count_list": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_double, _c.c_void_p, _c.c_uint64, _c.c_uint64,
+         _c.c_uint64, _c.c_void_p, _c.c_void_p],
+    ),
 }
 
 _lock = threading.Lock()

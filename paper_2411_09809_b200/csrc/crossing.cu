@@ -467,9 +467,11 @@ template <bool FAST, bool ANGLE>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                    const double *__restrict__ theta, const int2 *__restrict__ ids,
-                   const int *__restrict__ newc, uint64_t T, uint64_t ubeg, uint64_t uend,
-                   double kappa, unsigned long long *__restrict__ cta_cnt,
-                   double *__restrict__ cta_dev) {
+                   const int *__restrict__ newc, const int2 *__restrict__ ulist, uint64_t T,
+                   uint64_t ubeg, uint64_t uend, double kappa,
+                   unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
+  // ulist == nullptr: units are the implicit upper triangle of tile pairs;
+  // otherwise unit u is the explicit tile pair ulist[u] (culled candidates).
   if (hdr->fast != (FAST ? 1 : 0)) return;
   constexpr bool IDS = !FAST;
   __shared__ __align__(16) EdgeRec sj[kTile];
@@ -488,8 +490,13 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   double dsum = 0.0, dcomp = 0.0;  // Kahan over per-unit partials
   IRegs<IDS> R;
   uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
-  if (b < e) tri_unit_coords(b, T, &ti, &tj);
+  if (b < e && ulist == nullptr) tri_unit_coords(b, T, &ti, &tj);
   for (uint64_t u = b; u < e; ++u) {
+    if (ulist != nullptr) {
+      const int2 p = ulist[u];
+      ti = (uint64_t)p.x;
+      tj = (uint64_t)p.y;
+    }
     if (ti != cur_ti) {
       load_i<IDS, ANGLE>(R, rec, theta, ids, ti);
       cur_ti = ti;
@@ -559,9 +566,31 @@ template <bool ANGLE>
 __global__ void __launch_bounds__(kAdjTile)
 adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
            const int *__restrict__ inc, const int *__restrict__ offs,
-           const long long *__restrict__ wofs, uint64_t T, uint64_t ubeg, uint64_t uend,
-           double kappa, unsigned long long *__restrict__ part_cnt,
-           double *__restrict__ part_dev) {
+           const long long *__restrict__ wofs, const int2 *__restrict__ ulist, uint64_t ulen,
+           uint64_t T, uint64_t ubeg, uint64_t uend, double kappa,
+           unsigned long long *__restrict__ part_cnt, double *__restrict__ part_dev) {
+  // Units are tile pairs in row-major (lexicographic) order, both for the
+  // implicit triangle and for a culled candidate list (sorted, and containing
+  // every tile pair whose tile bboxes overlap -- hence every adjacent pair's).
+  // A range [ubeg, uend) is therefore the key interval [key(ubeg), key(uend))
+  // with key(ti, tj) = ti*T + tj.
+  uint64_t key_lo, key_hi;
+  {
+    uint64_t a, c;
+    if (ulist == nullptr) {
+      tri_unit_coords(ubeg, T, &a, &c);
+      key_lo = a * T + c;
+      if (uend >= ulen) {
+        key_hi = T * T;
+      } else {
+        tri_unit_coords(uend, T, &a, &c);
+        key_hi = a * T + c;
+      }
+    } else {
+      key_lo = (uint64_t)ulist[ubeg].x * T + (uint64_t)ulist[ubeg].y;
+      key_hi = uend >= ulen ? T * T : (uint64_t)ulist[uend].x * T + (uint64_t)ulist[uend].y;
+    }
+  }
   __shared__ int s_e[kAdjTile];
   __shared__ double s_t[kAdjTile];
   __shared__ long long s_v;
@@ -610,8 +639,8 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
       for (int qq = (ti == tj) ? (int)threadIdx.x + 1 : 0; qq < qn; ++qq) {
         const int e2 = s_e[qq];
         const uint64_t lo = (uint64_t)min(e1, e2) / kTile, hi = (uint64_t)max(e1, e2) / kTile;
-        const uint64_t unit = tri_row_start(lo, T) + (hi - lo);
-        if (unit >= ubeg && unit < uend) {
+        const uint64_t key = lo * T + hi;
+        if (key >= key_lo && key < key_hi) {
           ++cnt;
           if (ANGLE) s = __dadd_rn(s, angle_dev(t1, s_t[qq], kappa));
         }
@@ -642,6 +671,57 @@ __global__ void cross_finalize_kernel(const unsigned long long *cta_cnt, const d
     for (int i = 0; i < nadj; ++i) a += adj_cnt[i];
     out[0] = (double)(c - a);
     out[1] = __dsub_rn(kahan_sum(cta_dev, ncta), kahan_sum(adj_dev, nadj));
+  }
+}
+
+// ---- culled candidate list: tile pairs whose tile rank boxes overlap ------
+
+// per tile: (min rxmin, max rxmax, min rymin, max rymax); pad edges hold
+// (INT_MAX, -1, INT_MAX, -1), so an all-pad tile's box is empty
+__global__ void __launch_bounds__(kTile)
+tile_box_kernel(const EdgeRec *__restrict__ rec, int4 *__restrict__ box) {
+  __shared__ int4 red[kTile / 32];
+  const EdgeRec &r = rec[(int64_t)blockIdx.x * kTile + threadIdx.x];
+  int x0 = r.rxmin, x1 = r.rxmax, y0 = r.rymin, y1 = r.rymax;
+  for (int o = 16; o > 0; o >>= 1) {
+    x0 = min(x0, __shfl_down_sync(0xffffffffu, x0, o));
+    x1 = max(x1, __shfl_down_sync(0xffffffffu, x1, o));
+    y0 = min(y0, __shfl_down_sync(0xffffffffu, y0, o));
+    y1 = max(y1, __shfl_down_sync(0xffffffffu, y1, o));
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_int4(x0, x1, y0, y1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int4 b = red[0];
+    for (int w = 1; w < kTile / 32; ++w) {
+      b.x = min(b.x, red[w].x); b.y = max(b.y, red[w].y);
+      b.z = min(b.z, red[w].z); b.w = max(b.w, red[w].w);
+    }
+    box[blockIdx.x] = b;
+  }
+}
+
+__device__ inline bool boxes_overlap(int4 a, int4 b) {
+  return b.y >= a.x && a.y >= b.x && b.w >= a.z && a.w >= b.z;
+}
+
+// FILL == false: count candidates of row ti; FILL == true: write them at
+// offs[ti] (row-major, so the list is sorted by (ti, tj)).
+template <bool FILL>
+__global__ void tile_pairs_kernel(const int4 *__restrict__ box, int64_t T,
+                                  unsigned long long *__restrict__ counts,
+                                  const unsigned long long *__restrict__ offs, int2 *list) {
+  for (int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ti < T;
+       ti += (int64_t)gridDim.x * blockDim.x) {
+    const int4 a = box[ti];
+    unsigned long long c = 0, o = FILL ? offs[ti] : 0;
+    for (int64_t tj = ti; tj < T; ++tj) {
+      if (boxes_overlap(a, box[tj])) {
+        if (FILL) list[o + c] = make_int2((int)ti, (int)tj);
+        ++c;
+      }
+    }
+    if (!FILL) counts[ti] = c;
   }
 }
 
@@ -768,14 +848,15 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
 }
 
 int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
-                   uint64_t ubeg, uint64_t uend, double *d_out, cudaStream_t st) {
+                   const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
+                   double *d_out, cudaStream_t st) {
   if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0) {
     set_error("glr_crossing_pairs: invalid arguments");
     return GLR_EARG;
   }
   const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
   const uint64_t T = (uint64_t)(m_pad / kTile);
-  const uint64_t U = tri_units(T);
+  const uint64_t U = d_list != nullptr ? list_len : tri_units(T);
   if (ubeg > uend || uend > U) {
     set_error("glr_crossing_pairs: unit range [%llu, %llu) outside [0, %llu)",
               (unsigned long long)ubeg, (unsigned long long)uend, (unsigned long long)U);
@@ -800,28 +881,69 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
   if (with_angle) {
-    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
-                                                              ubeg, uend, kappa, cc, cd);
+    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
-    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
-                                                               ubeg, uend, kappa, cc, cd);
+    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
-    adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
-                                                 ubeg, uend, kappa, ac, ad);
+    adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
+                                                 d_list, U, T, ubeg, uend, kappa, ac, ad);
     GLR_LAUNCHED("adj_kernel<angle>");
   } else {
-    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
-                                                               ubeg, uend, 0.0, cc, cd);
+    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast>");
-    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, T,
-                                                                ubeg, uend, 0.0, cc, cd);
+    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
-    adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs, T,
-                                                  ubeg, uend, 0.0, ac, ad);
+    adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
+                                                  d_list, U, T, ubeg, uend, 0.0, ac, ad);
     GLR_LAUNCHED("adj_kernel");
   }
   cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, ac, ad, agrid, d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
+  return GLR_OK;
+}
+
+int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_list,
+                        uint64_t capacity, uint64_t *h_count, cudaStream_t st) {
+  if (d_records == nullptr || h_count == nullptr || m < 0 || n < 0) {
+    set_error("glr_crossing_candidates: invalid arguments");
+    return GLR_EARG;
+  }
+  const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
+  const int64_t T = m_pad / kTile;
+  RecView rv = view(const_cast<void *>(d_records), n, m);
+  size_t t_scan = 0;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (unsigned long long *)nullptr,
+                                         (unsigned long long *)nullptr, (int)(T + 1), st));
+  const size_t a_box = al256((size_t)T * sizeof(int4));
+  const size_t a_cnt = al256((size_t)(T + 1) * sizeof(unsigned long long));
+  Scratch scr(a_box + 2 * a_cnt + t_scan, st);
+  GLR_CUDA(scr.err);
+  char *p = scr.as<char>();
+  int4 *box = reinterpret_cast<int4 *>(p);
+  unsigned long long *counts = reinterpret_cast<unsigned long long *>(p + a_box);
+  unsigned long long *offs = reinterpret_cast<unsigned long long *>(p + a_box + a_cnt);
+  void *tmp = p + a_box + 2 * a_cnt;
+  tile_box_kernel<<<(unsigned)T, kTile, 0, st>>>(rv.rec, box);
+  GLR_LAUNCHED("tile_box_kernel");
+  GLR_CUDA(cudaMemsetAsync(counts + T, 0, sizeof(unsigned long long), st));
+  const int rb = blocks_for(T, 128, 16);
+  tile_pairs_kernel<false><<<rb, 128, 0, st>>>(box, T, counts, nullptr, nullptr);
+  GLR_LAUNCHED("tile_pairs_kernel<count>");
+  size_t tb = t_scan;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, offs, (int)(T + 1), st));
+  count_launch(2);
+  unsigned long long total = 0;
+  GLR_CUDA(cudaMemcpyAsync(&total, offs + T, sizeof(total), cudaMemcpyDeviceToHost, st));
+  GLR_CUDA(cudaStreamSynchronize(st));
+  *h_count = total;
+  if (d_list != nullptr && capacity >= total && total > 0) {
+    tile_pairs_kernel<true><<<rb, 128, 0, st>>>(box, T, nullptr, offs, d_list);
+    GLR_LAUNCHED("tile_pairs_kernel<fill>");
+  }
   return GLR_OK;
 }
 
@@ -830,6 +952,33 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
 extern "C" {
 
 int glr_crossing_tile(void) { return glr::kTile; }
+
+int glr_crossing_candidates(const void *d_records, int64_t n, int64_t m, void *d_list,
+                            uint64_t capacity, uint64_t *h_count, void *stream) {
+  return glr::crossing_candidates(d_records, n, m, reinterpret_cast<int2 *>(d_list), capacity,
+                                  h_count, glr::as_stream(stream));
+}
+
+int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m, int with_angle,
+                            double ideal, const void *d_list, uint64_t list_len,
+                            uint64_t unit_begin, uint64_t unit_end, double *d_out, void *stream) {
+  if (d_list == nullptr && list_len > 0) {
+    glr::set_error("glr_crossing_pairs_list: null list");
+    return GLR_EARG;
+  }
+  if (list_len == 0) {
+    if (unit_begin != 0 || unit_end != 0) {
+      glr::set_error("glr_crossing_pairs_list: unit range outside an empty list");
+      return GLR_EARG;
+    }
+    cudaStream_t st = glr::as_stream(stream);
+    GLR_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), st));
+    return GLR_OK;
+  }
+  return glr::crossing_pairs(d_records, n, m, with_angle, ideal,
+                             reinterpret_cast<const int2 *>(d_list), list_len, unit_begin,
+                             unit_end, d_out, glr::as_stream(stream));
+}
 
 uint64_t glr_crossing_units(int64_t m) {
   const int64_t m_pad = glr::pad_edges(m < 1 ? 1 : m);
@@ -845,8 +994,8 @@ int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, 
 
 int glr_crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                        uint64_t unit_begin, uint64_t unit_end, double *d_out, void *stream) {
-  return glr::crossing_pairs(d_records, n, m, with_angle, ideal, unit_begin, unit_end, d_out,
-                             glr::as_stream(stream));
+  return glr::crossing_pairs(d_records, n, m, with_angle, ideal, nullptr, 0, unit_begin,
+                             unit_end, d_out, glr::as_stream(stream));
 }
 
 int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
@@ -857,7 +1006,8 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
   GLR_CUDA(rec.err);
   int rc = glr::crossing_prepare(d_xy, n, d_edges, m, rec.ptr, st);
   if (rc != GLR_OK) return rc;
-  return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, unit_begin, unit_end, d_out, st);
+  return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, nullptr, 0, unit_begin, unit_end,
+                             d_out, st);
 }
 
 int glr_crossing_fast_path(const void *d_records, void *stream) {

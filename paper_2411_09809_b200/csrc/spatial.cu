@@ -1,0 +1,203 @@
+// Spatial (Morton / Z-order) reordering of edges and vertices, the first
+// step of the culled variants.
+//
+// The exact metrics do not depend on the order of edges or vertices (the pair
+// predicate is symmetric and every unordered pair is visited once, the
+// adjacency correction uses the same indexing), so a permutation is free to
+// choose.  Sorting by the Morton code of the bbox centre makes each 256- or
+// 1024-element tile spatially compact, so most tile pairs have disjoint tile
+// bounding boxes and are skipped by the candidate lists built in crossing.cu
+// and occlusion.cu.  The permutation only affects speed, never results.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace glr {
+namespace {
+
+// order-preserving 64-bit key of a double (total order, -0 < +0)
+__device__ inline unsigned long long dkey(double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ inline double dunkey(unsigned long long k) {
+  unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// global [xmin, xmax] x [ymin, ymax] of the coordinates as order-preserving keys
+__global__ void bounds_kernel(const double2 *__restrict__ xy, int64_t n, unsigned long long *b) {
+  unsigned long long x0 = ~0ull, x1 = 0, y0 = ~0ull, y1 = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = xy[i];
+    const unsigned long long kx = dkey(p.x), ky = dkey(p.y);
+    x0 = kx < x0 ? kx : x0;
+    x1 = kx > x1 ? kx : x1;
+    y0 = ky < y0 ? ky : y0;
+    y1 = ky > y1 ? ky : y1;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a;
+    a = __shfl_down_sync(0xffffffffu, x0, o); x0 = a < x0 ? a : x0;
+    a = __shfl_down_sync(0xffffffffu, x1, o); x1 = a > x1 ? a : x1;
+    a = __shfl_down_sync(0xffffffffu, y0, o); y0 = a < y0 ? a : y0;
+    a = __shfl_down_sync(0xffffffffu, y1, o); y1 = a > y1 ? a : y1;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&b[0], x0);
+    atomicMax(&b[1], x1);
+    atomicMin(&b[2], y0);
+    atomicMax(&b[3], y1);
+  }
+}
+
+__device__ inline unsigned spread16(unsigned v) {
+  v &= 0xffffu;
+  v = (v | (v << 8)) & 0x00ff00ffu;
+  v = (v | (v << 4)) & 0x0f0f0f0fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+
+__device__ inline unsigned quant16(double v, double lo, double scale) {
+  double q = (v - lo) * scale;  // scale = 65535 / (hi - lo), or 0 for a flat axis
+  if (!(q >= 0.0)) q = 0.0;     // also catches NaN from inf - inf
+  if (q > 65535.0) q = 65535.0;
+  return (unsigned)q;
+}
+
+__device__ inline unsigned morton(double x, double y, const unsigned long long *b) {
+  const double x0 = dunkey(b[0]), x1 = dunkey(b[1]), y0 = dunkey(b[2]), y1 = dunkey(b[3]);
+  const double sx = (x1 > x0 && isfinite(x1 - x0)) ? 65535.0 / (x1 - x0) : 0.0;
+  const double sy = (y1 > y0 && isfinite(y1 - y0)) ? 65535.0 / (y1 - y0) : 0.0;
+  return spread16(quant16(x, x0, sx)) | (spread16(quant16(y, y0, sy)) << 1);
+}
+
+__global__ void edge_keys_kernel(const double2 *__restrict__ xy, const longlong2 *__restrict__ e,
+                                 int64_t m, const unsigned long long *b, unsigned *keys,
+                                 int *idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 uv = e[i];
+    const double2 p = xy[uv.x], q = xy[uv.y];
+    // bbox centre (halves first: no overflow for huge coordinates)
+    keys[i] = morton(0.5 * p.x + 0.5 * q.x, 0.5 * p.y + 0.5 * q.y, b);
+    idx[i] = (int)i;
+  }
+}
+
+__global__ void vertex_keys_kernel(const double2 *__restrict__ xy, int64_t n,
+                                   const unsigned long long *b, unsigned *keys, int *idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = xy[i];
+    keys[i] = morton(p.x, p.y, b);
+    idx[i] = (int)i;
+  }
+}
+
+__global__ void gather_edges_kernel(const longlong2 *__restrict__ e, const int *__restrict__ perm,
+                                    int64_t m, longlong2 *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = e[perm[i]];
+}
+
+__global__ void gather_xy_kernel(const double2 *__restrict__ xy, const int *__restrict__ perm,
+                                 int64_t n, double2 *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = xy[perm[i]];
+}
+
+int grid_of(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// Shared driver: bounds, keys, stable radix sort of (key, index), gather.
+template <bool EDGES>
+int spatial_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t len, void *d_out,
+                 cudaStream_t st) {
+  if (len <= 1) {
+    if (len == 1) {
+      GLR_CUDA(cudaMemcpyAsync(d_out, EDGES ? (const void *)d_edges : (const void *)d_xy, 16,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    return GLR_OK;
+  }
+  size_t t_sort = 0;
+  GLR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const unsigned *)nullptr,
+                                           (unsigned *)nullptr, (const int *)nullptr,
+                                           (int *)nullptr, (int)len, 0, 32, st));
+  const size_t a4 = ((size_t)len * 4 + 255) & ~(size_t)255;
+  Scratch scr(4 * a4 + 256 + t_sort, st);
+  GLR_CUDA(scr.err);
+  char *p = scr.as<char>();
+  unsigned *keys = reinterpret_cast<unsigned *>(p);
+  unsigned *keys_out = reinterpret_cast<unsigned *>(p + a4);
+  int *idx = reinterpret_cast<int *>(p + 2 * a4);
+  int *perm = reinterpret_cast<int *>(p + 3 * a4);
+  unsigned long long *b = reinterpret_cast<unsigned long long *>(p + 4 * a4);
+  void *tmp = p + 4 * a4 + 256;
+  // bound words: min keys start at ~0, max keys at 0 (memsets, no host staging)
+  GLR_CUDA(cudaMemsetAsync(b, 0xff, 8, st));
+  GLR_CUDA(cudaMemsetAsync(b + 1, 0x00, 8, st));
+  GLR_CUDA(cudaMemsetAsync(b + 2, 0xff, 8, st));
+  GLR_CUDA(cudaMemsetAsync(b + 3, 0x00, 8, st));
+  bounds_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n, b);
+  GLR_LAUNCHED("bounds_kernel");
+  if (EDGES) {
+    edge_keys_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
+                                                  reinterpret_cast<const longlong2 *>(d_edges),
+                                                  len, b, keys, idx);
+    GLR_LAUNCHED("edge_keys_kernel");
+  } else {
+    vertex_keys_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
+                                                    len, b, keys, idx);
+    GLR_LAUNCHED("vertex_keys_kernel");
+  }
+  size_t tb = t_sort;
+  GLR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_out, idx, perm, (int)len, 0, 32, st));
+  count_launch(4);
+  if (EDGES) {
+    gather_edges_kernel<<<grid_of(len), 256, 0, st>>>(
+        reinterpret_cast<const longlong2 *>(d_edges), perm, len,
+        reinterpret_cast<longlong2 *>(d_out));
+    GLR_LAUNCHED("gather_edges_kernel");
+  } else {
+    gather_xy_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), perm,
+                                                  len, reinterpret_cast<double2 *>(d_out));
+    GLR_LAUNCHED("gather_xy_kernel");
+  }
+  return GLR_OK;
+}
+
+}  // namespace
+}  // namespace glr
+
+extern "C" {
+
+int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                           int64_t *d_edges_out, void *stream) {
+  if (n < 0 || m < 0 || (m > 0 && (d_xy == nullptr || d_edges == nullptr || d_edges_out == nullptr)) ||
+      m >= ((int64_t)1 << 31)) {
+    glr::set_error("glr_spatial_sort_edges: invalid arguments");
+    return GLR_EARG;
+  }
+  return glr::spatial_sort<true>(d_xy, n, d_edges, m, d_edges_out, glr::as_stream(stream));
+}
+
+int glr_spatial_sort_vertices(const double *d_xy, int64_t n, double *d_xy_out, void *stream) {
+  if (n < 0 || (n > 0 && (d_xy == nullptr || d_xy_out == nullptr)) || n >= ((int64_t)1 << 31)) {
+    glr::set_error("glr_spatial_sort_vertices: invalid arguments");
+    return GLR_EARG;
+  }
+  return glr::spatial_sort<false>(d_xy, n, nullptr, n, d_xy_out, glr::as_stream(stream));
+}
+
+}  // extern "C"

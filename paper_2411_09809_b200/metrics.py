@@ -16,24 +16,39 @@ metrics/__init__.py:11-25):
 (duck-typed on ``xy``/``edges``), or a ``DeviceGraph`` whose arrays already
 live in HBM.  The arithmetic runs in the hand-written sm_100a kernels of
 ``libglare_b200.so``; there is no CPU path.
+
+Each all-pairs metric takes a keyword-only ``strategy``:
+
+* ``"dense"`` -- every tile pair of the upper triangle (the FP64-roofline
+  kernel; edges in input order so runs sharing a first endpoint reuse terms);
+* ``"culled"`` -- elements reordered by Morton code, only tile pairs whose
+  tile bounding boxes can interact are scanned (exactly the same result;
+  orders of magnitude fewer pair tests on spatially local inputs);
+* ``"auto"`` (default) -- culled when the candidate tile pairs are at most
+  ``CULL_FRACTION`` of all tile pairs, dense otherwise.
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
 import torch
 
 from . import _lib
-from .model import IDEAL_ANGLE_DEFAULT, check_ideal_angle, check_radius
+from .model import IDEAL_ANGLE_DEFAULT, ParameterError, check_ideal_angle, check_radius
+
+STRATEGIES = ("auto", "dense", "culled")
+CULL_FRACTION = 0.25      # auto: cull when candidates <= this share of tile pairs
+AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
 
 
 class DeviceGraph:
     """Positions and normalised edge index pairs resident on a CUDA device.
 
     ``xy``: float64 (n, 2) contiguous; ``edges``: int64 (m, 2) contiguous,
-    normalised as ``LayoutGraph`` does (small index first, sorted, unique).
+    normalised as ``LayoutGraph`` does (small index first, unique).
     """
 
     __slots__ = ("xy", "edges")
@@ -82,6 +97,24 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+def _check_strategy(strategy: str) -> str:
+    if strategy not in STRATEGIES:
+        raise ParameterError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
+    return strategy
+
+
+def _candidates(fn, *args) -> torch.Tensor:
+    """Two-phase candidate list: count (synchronous), allocate, fill."""
+    count = ctypes.c_uint64(0)
+    _lib.check(fn(*args, None, 0, ctypes.byref(count), _stream()), fn.__name__)
+    n = int(count.value)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lst = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+    if n:
+        _lib.check(fn(*args, _ptr(lst), n, ctypes.byref(count), _stream()), fn.__name__)
+    return lst[:n]
+
+
 # ---- unit-range kernels (device results, no host sync) ----------------------
 
 
@@ -100,7 +133,7 @@ def occlusion_threshold(r: float) -> float:
 
 def occlusion_partial(dg: DeviceGraph, thr: float, unit_begin: int, unit_end: int,
                       out: torch.Tensor | None = None) -> torch.Tensor:
-    """Device float64[1]: occluding pairs inside units [unit_begin, unit_end)."""
+    """Device float64[1]: occluding pairs inside dense units [unit_begin, unit_end)."""
     L = _lib.lib()
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=dg.xy.device)
@@ -110,24 +143,96 @@ def occlusion_partial(dg: DeviceGraph, thr: float, unit_begin: int, unit_end: in
     return out
 
 
+class OcclusionPlan:
+    """Node-occlusion pass for one radius.  ``culled``: vertices in Morton
+    order and the candidate vertex-tile pairs whose boxes are closer than 2r;
+    otherwise the dense triangle over the input order."""
+
+    def __init__(self, dg: DeviceGraph, r: float, strategy: str = "auto"):
+        L = _lib.lib()
+        self.r = r
+        self.thr = occlusion_threshold(r)
+        self.n = dg.num_vertices
+        self.dense_units = occlusion_units(self.n)
+        self.list = None
+        self.xy = dg.xy
+        strategy = _check_strategy(strategy)
+        if strategy != "dense" and self.n >= 2:
+            xs = torch.empty_like(dg.xy)
+            _lib.check(L.glr_spatial_sort_vertices(_ptr(dg.xy), self.n, _ptr(xs), _stream()),
+                       "glr_spatial_sort_vertices")
+            lst = _candidates(L.glr_occlusion_candidates, _ptr(xs), self.n, 2.0 * r)
+            if strategy == "culled" or len(lst) <= CULL_FRACTION * self.dense_units:
+                self.xy, self.list = xs, lst
+
+    @property
+    def culled(self) -> bool:
+        return self.list is not None
+
+    @property
+    def units(self) -> int:
+        return len(self.list) if self.culled else self.dense_units
+
+    def partial(self, unit_begin: int, unit_end: int,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+        L = _lib.lib()
+        if out is None:
+            out = torch.empty(1, dtype=torch.float64, device=self.xy.device)
+        if self.culled:
+            rc = L.glr_occlusion_count_list(_ptr(self.xy), self.n, self.thr,
+                                            _ptr(self.list) if len(self.list) else None,
+                                            len(self.list), int(unit_begin), int(unit_end),
+                                            _ptr(out), _stream())
+            _lib.check(rc, "glr_occlusion_count_list")
+        else:
+            rc = L.glr_occlusion_count(_ptr(self.xy), self.n, self.thr, int(unit_begin),
+                                       int(unit_end), _ptr(out), _stream())
+            _lib.check(rc, "glr_occlusion_count")
+        return out
+
+
 class CrossingRecords:
     """Prepared per-edge records (glr_crossing_prepare) kept in HBM so that
-    several unit ranges / both E_c and E_ca reuse one prologue."""
+    several unit ranges / both E_c and E_ca reuse one prologue.
 
-    def __init__(self, dg: DeviceGraph):
-        L = _lib.lib()
+    ``strategy`` selects dense or culled scanning (see the module docstring);
+    with culling the records hold the Morton-ordered edge list and ``list``
+    the candidate tile pairs."""
+
+    def __init__(self, dg: DeviceGraph, strategy: str = "dense"):
+        strategy = _check_strategy(strategy)
         self.m = dg.num_edges
         self.n = dg.num_vertices
+        self.list = None
+        if strategy != "dense" and self.m >= 2 and (strategy == "culled"
+                                                    or self.m >= AUTO_MIN_EDGES):
+            L = _lib.lib()
+            es = torch.empty_like(dg.edges)
+            _lib.check(L.glr_spatial_sort_edges(_ptr(dg.xy), self.n, _ptr(dg.edges), self.m,
+                                                _ptr(es), _stream()),
+                       "glr_spatial_sort_edges")
+            self._prepare(dg.xy, es)
+            lst = _candidates(L.glr_crossing_candidates, _ptr(self.buf), self.n, self.m)
+            if strategy == "culled" or len(lst) <= CULL_FRACTION * crossing_units(self.m):
+                self.list = lst
+                return
+        self._prepare(dg.xy, dg.edges)
+
+    def _prepare(self, xy: torch.Tensor, edges: torch.Tensor) -> None:
+        L = _lib.lib()
         nbytes = int(L.glr_crossing_records_bytes(self.n, self.m))
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dg.xy.device)
-        rc = L.glr_crossing_prepare(_ptr(dg.xy), dg.num_vertices,
-                                    _ptr(dg.edges) if self.m else None, self.m,
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=xy.device)
+        rc = L.glr_crossing_prepare(_ptr(xy), self.n, _ptr(edges) if self.m else None, self.m,
                                     _ptr(self.buf), _stream())
         _lib.check(rc, "glr_crossing_prepare")
 
     @property
+    def culled(self) -> bool:
+        return self.list is not None
+
+    @property
     def units(self) -> int:
-        return crossing_units(self.m)
+        return len(self.list) if self.culled else crossing_units(self.m)
 
     def fast_path(self) -> bool:
         return _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream()) == 1
@@ -137,11 +242,19 @@ class CrossingRecords:
         """Device float64[2] = (count, dev_sum) over units [unit_begin, unit_end)."""
         if out is None:
             out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
-        rc = _lib.lib().glr_crossing_pairs(
-            _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
-            0.0 if ideal is None else float(ideal), int(unit_begin), int(unit_end),
-            _ptr(out), _stream())
-        _lib.check(rc, "glr_crossing_pairs")
+        L = _lib.lib()
+        angle = 0 if ideal is None else 1
+        ideal_v = 0.0 if ideal is None else float(ideal)
+        if self.culled:
+            rc = L.glr_crossing_pairs_list(_ptr(self.buf), self.n, self.m, angle, ideal_v,
+                                           _ptr(self.list) if len(self.list) else None,
+                                           len(self.list), int(unit_begin), int(unit_end),
+                                           _ptr(out), _stream())
+            _lib.check(rc, "glr_crossing_pairs_list")
+        else:
+            rc = L.glr_crossing_pairs(_ptr(self.buf), self.n, self.m, angle, ideal_v,
+                                      int(unit_begin), int(unit_end), _ptr(out), _stream())
+            _lib.check(rc, "glr_crossing_pairs")
         return out
 
 
@@ -178,15 +291,16 @@ def _num_edges(g) -> int:
     return int(g.num_edges)
 
 
-def node_occlusion(g, r: float) -> int:
+def node_occlusion(g, r: float, *, strategy: str = "auto") -> int:
     """Unordered vertex pairs with squared distance strictly below (2r)^2."""
     r = check_radius(r)
+    _check_strategy(strategy)
     n = _num_vertices(g)
     if n < 2:
         return 0
-    dg = _dev(g)
-    out = occlusion_partial(dg, occlusion_threshold(r), 0, occlusion_units(n))
-    return int(out.item())
+    occlusion_threshold(r)  # raises OverflowError exactly where exact.py:63 does
+    plan = OcclusionPlan(_dev(g), r, strategy)
+    return int(plan.partial(0, plan.units).item())
 
 
 def minimum_angle(g) -> float:
@@ -209,36 +323,40 @@ def edge_length_variation(g) -> float:
     return la / math.sqrt(m - 1)
 
 
-def _crossing_scan(g, ideal_angle: float | None = None) -> tuple[int, float]:
+def _crossing_scan(g, ideal_angle: float | None = None, *,
+                   strategy: str = "auto") -> tuple[int, float]:
     """(crossing count, sum of |ideal - crossing angle| over crossings)."""
+    _check_strategy(strategy)
     m = _num_edges(g)
     if m < 2:
         return 0, 0.0
-    rec = CrossingRecords(_dev(g))
+    rec = CrossingRecords(_dev(g), strategy)
     out = rec.partial(ideal_angle, 0, rec.units)
     count, dev = out.tolist()
     return int(count), (float(dev) if ideal_angle is not None else 0.0)
 
 
-def edge_crossing(g) -> int:
+def edge_crossing(g, *, strategy: str = "auto") -> int:
     """Count of non-adjacent edge pairs that properly intersect."""
-    return _crossing_scan(g)[0]
+    return _crossing_scan(g, strategy=strategy)[0]
 
 
-def edge_crossing_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT) -> float:
+def edge_crossing_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT, *,
+                        strategy: str = "auto") -> float:
     """1 minus the mean normalised deviation of crossing angles from ideal."""
     ideal_angle = check_ideal_angle(ideal_angle)
-    total, dev_sum = _crossing_scan(g, ideal_angle)
+    total, dev_sum = _crossing_scan(g, ideal_angle, strategy=strategy)
     if total == 0:
         return 1.0
     return 1.0 - (dev_sum / ideal_angle) / total
 
 
-def crossing_count_and_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT) -> tuple[int, float]:
+def crossing_count_and_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT, *,
+                             strategy: str = "auto") -> tuple[int, float]:
     """E_c and E_ca from ONE fused scan (the engine uses this when both are
     requested; the reference runs _crossing_scan twice, engine.py:85-92)."""
     ideal_angle = check_ideal_angle(ideal_angle)
-    total, dev_sum = _crossing_scan(g, ideal_angle)
+    total, dev_sum = _crossing_scan(g, ideal_angle, strategy=strategy)
     eca = 1.0 if total == 0 else 1.0 - (dev_sum / ideal_angle) / total
     return total, eca
 
@@ -246,6 +364,8 @@ def crossing_count_and_angle(g, ideal_angle: float = IDEAL_ANGLE_DEFAULT) -> tup
 __all__ = [
     "DeviceGraph",
     "CrossingRecords",
+    "OcclusionPlan",
+    "STRATEGIES",
     "node_occlusion",
     "minimum_angle",
     "edge_length_variation",
