@@ -127,7 +127,7 @@ class _Evaluator:
                 self._scan = M._crossing_scan(self.dg(), self.p.ideal_angle)
             else:
                 out = sharding.sharded_evaluate(self.dg(), None, self.p.ideal_angle,
-                                                self.rank, self.world)
+                                                self.rank, self.world, strategy="auto")
                 c, d, _ = out.tolist()
                 self._scan = (int(c), float(d))
         return self._scan
@@ -141,7 +141,7 @@ class _Evaluator:
 
             def nc():
                 out = sharding.sharded_evaluate(self.dg(), p.radius, None, self.rank, self.world,
-                                                with_crossing=False)
+                                                with_crossing=False, strategy="auto")
                 return int(out[2].item()), []
 
             return nc

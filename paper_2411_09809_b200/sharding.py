@@ -58,10 +58,13 @@ def allreduce_partials(buf, group=None):
 
 
 def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, world: int,
-                     with_crossing: bool = True, records=None, out=None):
+                     with_crossing: bool = True, records=None, out=None,
+                     strategy: str = "dense"):
     """Compute this rank's partial (count, dev_sum, occlusions) on the current
     CUDA device into a device float64[3] tensor and allreduce it.  Returns the
-    tensor (summed over ranks); no host synchronisation."""
+    tensor (summed over ranks); no host synchronisation.  ``strategy`` as in
+    metrics (dense unit triangle or culled candidate list); every rank builds
+    the same plan, so the unit spaces agree."""
     import torch
 
     from . import metrics as M
@@ -71,11 +74,11 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
     else:
         out.zero_()
     if with_crossing and dg.num_edges >= 2:
-        rec = records if records is not None else M.CrossingRecords(dg)
+        rec = records if records is not None else M.CrossingRecords(dg, strategy)
         b, e = shard_range(rec.units, rank, world)
         rec.partial(ideal, b, e, out=out[0:2])
     if radius is not None and dg.num_vertices >= 2:
-        U = M.occlusion_units(dg.num_vertices)
-        b, e = shard_range(U, rank, world)
-        M.occlusion_partial(dg, M.occlusion_threshold(radius), b, e, out=out[2:3])
+        plan = M.OcclusionPlan(dg, radius, strategy)
+        b, e = shard_range(plan.units, rank, world)
+        plan.partial(b, e, out=out[2:3])
     return allreduce_partials(out)
