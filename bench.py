@@ -235,7 +235,7 @@ def main():
 
     def crossing_step():
         rec = M.CrossingRecords(dg)
-        b, e = sharding.shard_range(rec.units, rank, world)
+        b, e = rec.shard(rank, world)
         rec.partial(ideal, b, e, out=out[0:2])
         sharding.allreduce_partials(out[0:2])
 
@@ -256,7 +256,7 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             rec = M.CrossingRecords(dg)
-            b, e = sharding.shard_range(rec.units, rank, world)
+            b, e = rec.shard(rank, world)
             k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             k0.record(stream)
             rec.partial(ideal, b, e, out=out[0:2])

@@ -107,6 +107,14 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,
                       uint64_t unit_begin, uint64_t unit_end, double *d_out,
                       void *stream);
 
+/* Per-tile cost weights of prepared records for balanced sharding: d_w[t] =
+ * tile + beta * (run starts in tile t), t < ceil(m / glr_crossing_tile()).
+ * Unit (ti, tj) of the pair space costs about d_w[tj] (half on the
+ * diagonal), because a j-edge that starts a run of edges sharing its first
+ * endpoint recomputes the per-run terms. */
+int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
+                              double beta, double *d_w, void *stream);
+
 /* ---- culled variants (results identical) ---------- */
 
 /* Writes to d_edges_out the edge list reordered by the Morton code of each

@@ -58,6 +58,8 @@ SIGNATURES = {
     ),
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_take_launch_count": (_c.c_uint64, []),
+    "glr_crossing_tile_weights": (
+        _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_void_p, _c.c_void_p]),
     "glr_spatial_sort_edges": (
         _c.c_int,
         [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p],

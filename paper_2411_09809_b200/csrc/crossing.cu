@@ -725,6 +725,22 @@ __global__ void tile_pairs_kernel(const int4 *__restrict__ box, int64_t T,
   }
 }
 
+// Per j-tile cost weight for balanced sharding: a continuing j-edge of a run
+// costs 1, a run start 1 + beta (it also recomputes the (a,c)/(b,c) terms).
+__global__ void __launch_bounds__(kTile)
+tile_weight_kernel(const int *__restrict__ newc, double beta, double *__restrict__ w) {
+  __shared__ int red[kTile / 32];
+  int s = newc[(int64_t)blockIdx.x * kTile + threadIdx.x] != 0 ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < kTile / 32; ++i) t += red[i];
+    w[blockIdx.x] = (double)kTile + beta * (double)t;
+  }
+}
+
 int grid_for(uint64_t units) {
   uint64_t g = (uint64_t)sm_count() * kMinBlocks;
   if (units < g) g = units;
@@ -952,6 +968,20 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
 extern "C" {
 
 int glr_crossing_tile(void) { return glr::kTile; }
+
+int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m, double beta,
+                              double *d_w, void *stream) {
+  if (d_records == nullptr || d_w == nullptr || m < 0 || n < 0) {
+    glr::set_error("glr_crossing_tile_weights: invalid arguments");
+    return GLR_EARG;
+  }
+  const int64_t m_pad = glr::pad_edges(m < 1 ? 1 : m);
+  glr::RecView rv = glr::view(const_cast<void *>(d_records), n, m);
+  glr::tile_weight_kernel<<<(unsigned)(m_pad / glr::kTile), glr::kTile, 0,
+                            glr::as_stream(stream)>>>(rv.newc, beta, d_w);
+  GLR_LAUNCHED("tile_weight_kernel");
+  return GLR_OK;
+}
 
 int glr_crossing_candidates(const void *d_records, int64_t n, int64_t m, void *d_list,
                             uint64_t capacity, uint64_t *h_count, void *stream) {

@@ -237,6 +237,32 @@ class CrossingRecords:
     def fast_path(self) -> bool:
         return _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream()) == 1
 
+    def tile_weights(self, beta: float | None = None) -> np.ndarray:
+        """Per j-tile cost weights (glr_crossing_tile_weights), on the host."""
+        from .sharding import RUN_START_BETA
+
+        T = -(-max(self.m, 1) // _lib.lib().glr_crossing_tile())
+        w = torch.empty(T, dtype=torch.float64, device=self.buf.device)
+        rc = _lib.lib().glr_crossing_tile_weights(
+            _ptr(self.buf), self.n, self.m, RUN_START_BETA if beta is None else float(beta),
+            _ptr(w), _stream())
+        _lib.check(rc, "glr_crossing_tile_weights")
+        return w.cpu().numpy()
+
+    def shard(self, rank: int, world: int, balanced: bool = True) -> tuple[int, int]:
+        """This rank's contiguous unit range: equal estimated cost (balanced)
+        or equal unit counts."""
+        from . import sharding
+
+        if world == 1 or not balanced or self.m < 2:
+            return sharding.shard_range(self.units, rank, world)
+        w = self.tile_weights()
+        if not self.culled:
+            return sharding.triangle_range(w, rank, world)
+        lst = self.list.cpu().numpy()
+        unit_w = w[lst[:, 1]] * np.where(lst[:, 0] == lst[:, 1], 0.5, 1.0)
+        return sharding.weighted_range(unit_w, rank, world)
+
     def partial(self, ideal: float | None, unit_begin: int, unit_end: int,
                 out: torch.Tensor | None = None) -> torch.Tensor:
         """Device float64[2] = (count, dev_sum) over units [unit_begin, unit_end)."""

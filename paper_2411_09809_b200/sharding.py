@@ -75,10 +75,89 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
         out.zero_()
     if with_crossing and dg.num_edges >= 2:
         rec = records if records is not None else M.CrossingRecords(dg, strategy)
-        b, e = shard_range(rec.units, rank, world)
+        b, e = rec.shard(rank, world)
         rec.partial(ideal, b, e, out=out[0:2])
     if radius is not None and dg.num_vertices >= 2:
         plan = M.OcclusionPlan(dg, radius, strategy)
         b, e = shard_range(plan.units, rank, world)
         plan.partial(b, e, out=out[2:3])
     return allreduce_partials(out)
+
+
+# ---- cost-balanced splits ----------------------------------------------------
+# Units do not all cost the same: with run reuse (csrc/crossing.cu) a j-tile
+# full of run starts costs more than one inside a hub's run.  Measured on C5,
+# equal unit counts left the last of 8 ranks 17% slower than the first.  The
+# splits below cut the unit sequence at equal cumulative weight instead; every
+# rank computes the same cuts from the same weights, so the ranges still tile
+# the unit space exactly.
+
+# Extra cost of a run-start j-edge relative to a continuing one.  Calibrated
+# on C5 (fused E_c + E_ca, 8 ranges timed back to back on one B200): equal
+# unit counts 1.17 max/mean, beta 0.3 -> 1.047, beta 0.6 -> 1.014.
+RUN_START_BETA = 0.6
+
+
+def _cut(cum: "np.ndarray", frac: float) -> int:
+    """First index whose cumulative weight reaches frac of the total."""
+    import numpy as np
+
+    total = float(cum[-1]) if len(cum) else 0.0
+    return int(np.searchsorted(cum, frac * total, side="left"))
+
+
+def weighted_range(unit_weights, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous range of a 1-D unit sequence with per-unit weights."""
+    import numpy as np
+
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    w = np.asarray(unit_weights, dtype=np.float64)
+    U = len(w)
+    if U == 0:
+        return 0, 0
+    cum = np.cumsum(w)
+    b = 0 if rank == 0 else min(U, _cut(cum, rank / world) + 1)
+    e = U if rank == world - 1 else min(U, _cut(cum, (rank + 1) / world) + 1)
+    return b, max(b, e)
+
+
+def triangle_range(tile_w, rank: int, world: int) -> tuple[int, int]:
+    """Balanced contiguous range of the row-major upper-triangular unit space
+    (ti <= tj) where unit (ti, tj) weighs tile_w[tj] (half on the diagonal)."""
+    import numpy as np
+
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    w = np.asarray(tile_w, dtype=np.float64)
+    T = len(w)
+    U = T * (T + 1) // 2
+    suffix = np.cumsum(w[::-1])[::-1]                # sum_{tj >= ti} w[tj]
+    row = suffix - 0.5 * w                           # diagonal unit at half weight
+    row_cum = np.cumsum(row)
+    total = float(row_cum[-1])
+
+    def unit_at(frac: float) -> int:
+        if frac <= 0.0:
+            return 0
+        if frac >= 1.0:
+            return U
+        target = frac * total
+        ti = int(np.searchsorted(row_cum, target, side="left"))
+        if ti >= T:
+            return U
+        before = float(row_cum[ti - 1]) if ti > 0 else 0.0
+        within = np.cumsum(np.concatenate(([0.5 * w[ti]], w[ti + 1:])))
+        tj_off = int(np.searchsorted(within, target - before, side="left"))
+        start = ti * T - ti * (ti - 1) // 2
+        return min(U, start + tj_off + 1)
+
+    return unit_at(rank / world), unit_at((rank + 1) / world)
+
+
+def triangle_plan(tile_w, world: int) -> list[tuple[int, int]]:
+    plan = [triangle_range(tile_w, r, world) for r in range(world)]
+    T = len(tile_w)
+    assert plan[0][0] == 0 and plan[-1][1] == T * (T + 1) // 2
+    assert all(a[1] == b[0] for a, b in zip(plan, plan[1:]))
+    return plan

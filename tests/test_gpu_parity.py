@@ -209,3 +209,22 @@ def test_device_graph_input(gpu):
     dg = G.DeviceGraph(torch.from_numpy(g.xy).cuda(), torch.from_numpy(g.edges).cuda())
     assert G.edge_crossing(dg) == 4194903
     assert G.node_occlusion(dg, 1.0) == 9588
+
+
+def test_balanced_shards_sum_to_whole(gpu):
+    """Cost-balanced unit ranges (CrossingRecords.shard) tile the unit space
+    and their partials add up exactly, dense and culled."""
+    from paper_2411_09809_b200 import metrics as M
+
+    g = graph_from(cases.lattice_stress)
+    dg = M.DeviceGraph.from_graph(g)
+    for strategy in ("dense", "culled"):
+        rec = M.CrossingRecords(dg, strategy)
+        full = rec.partial(IDEAL, 0, rec.units).tolist()
+        for world in (2, 5, 8):
+            ranges = [rec.shard(r, world) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == rec.units
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            parts = [rec.partial(IDEAL, b, e).tolist() for b, e in ranges]
+            assert sum(p[0] for p in parts) == full[0] == 4194903
+            assert strict_close(sum(p[1] for p in parts), full[1])

@@ -89,3 +89,22 @@ def test_gloo_world2_partials_sum_to_oracle():
         assert rc == c == 4194903
         assert abs(rd - d) <= 1e-9 * abs(d)
         assert ro == occ == 9588
+
+
+def test_balanced_triangle_and_weighted_ranges():
+    rng = np.random.default_rng(0)
+    for T in (1, 2, 7, 60):
+        w = rng.uniform(0.5, 2.0, T)
+        for world in (1, 2, 3, 8):
+            plan = sharding.triangle_plan(w, world)
+            # per-rank weight is balanced within one unit's weight
+            U = T * (T + 1) // 2
+            unit_w = np.array([w[tj] * (0.5 if ti == tj else 1.0)
+                               for ti in range(T) for tj in range(ti, T)])
+            assert len(unit_w) == U
+            loads = [unit_w[b:e].sum() for b, e in plan]
+            assert max(loads) - min(loads) <= 2.0 * unit_w.max() + 1e-9
+        lst_w = rng.uniform(0.5, 2.0, 50)
+        cuts = [sharding.weighted_range(lst_w, r, 4) for r in range(4)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == 50
+        assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
