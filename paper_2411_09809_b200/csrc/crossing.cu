@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                    const double *__restrict__ theta, const int2 *__restrict__ ids,
                    const int *__restrict__ newc, const int2 *__restrict__ ulist, uint64_t T,
-                   uint64_t ubeg, uint64_t uend, double kappa,
+                   uint64_t ubeg, uint64_t uend, uint64_t chunk, double kappa,
                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   // ulist == nullptr: units are the implicit upper triangle of tile pairs;
   // otherwise unit u is the explicit tile pair ulist[u] (culled candidates).
@@ -482,15 +482,21 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   __shared__ unsigned long long red_u[kThreads / 32];
   __shared__ double red_d[kThreads / 32];
 
-  const uint64_t span = uend - ubeg;
-  const uint64_t b = ubeg + span * blockIdx.x / gridDim.x;
-  const uint64_t e = ubeg + span * (blockIdx.x + 1) / gridDim.x;
+  // Chunks of `chunk` consecutive units are dealt round-robin to the CTAs:
+  // unit cost varies along the triangle (run structure of the j-tile), and
+  // interleaving gives every CTA the same mix (a contiguous split left the
+  // slowest CTA ~15% behind).  Consecutive units inside a chunk mostly share
+  // ti, so the i-edges stay in registers.
+  const uint64_t nchunks = (uend - ubeg + chunk - 1) / chunk;
 
   unsigned long long total = 0;
   double dsum = 0.0, dcomp = 0.0;  // Kahan over per-unit partials
   IRegs<IDS> R;
   uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
-  if (b < e && ulist == nullptr) tri_unit_coords(b, T, &ti, &tj);
+  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  const uint64_t b = ubeg + ch * chunk;
+  const uint64_t e = b + chunk < uend ? b + chunk : uend;
+  if (ulist == nullptr) tri_unit_coords(b, T, &ti, &tj);
   for (uint64_t u = b; u < e; ++u) {
     if (ulist != nullptr) {
       const int2 p = ulist[u];
@@ -550,6 +556,7 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
     }
     if (++tj == T) { ++ti; tj = ti; }
   }
+  }  // chunks
   unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
   double bd = block_sum<kThreads>(dsum, red_d);
   if (threadIdx.x == 0) {
@@ -896,22 +903,26 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   double *cd = reinterpret_cast<double *>(ac + agrid);
   double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
+  // chunk: at least 8 chunks per CTA for balance, at most 32 units per chunk
+  uint64_t chunk = (uend - ubeg) / ((uint64_t)grid * 8);
+  if (chunk > 32) chunk = 32;
+  if (chunk < 1) chunk = 1;
   if (with_angle) {
     cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, kappa, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
     cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, kappa, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, kappa, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                  d_list, U, T, ubeg, uend, kappa, ac, ad);
     GLR_LAUNCHED("adj_kernel<angle>");
   } else {
     cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, 0.0, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast>");
     cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, 0.0, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, 0.0, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                   d_list, U, T, ubeg, uend, 0.0, ac, ad);
