@@ -235,8 +235,7 @@ def main():
 
     def crossing_step():
         rec = M.CrossingRecords(dg)
-        b, e = rec.shard(rank, world)
-        rec.partial(ideal, b, e, out=out[0:2])
+        rec.partial_interleaved(ideal, rank, world, out=out[0:2])
         sharding.allreduce_partials(out[0:2])
 
     def occlusion_step():
@@ -256,10 +255,9 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             rec = M.CrossingRecords(dg)
-            b, e = rec.shard(rank, world)
             k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             k0.record(stream)
-            rec.partial(ideal, b, e, out=out[0:2])
+            rec.partial_interleaved(ideal, rank, world, out=out[0:2])
             k1.record(stream)
             sharding.allreduce_partials(out[0:2])
             kern_ms.append((k0, k1))

@@ -73,8 +73,14 @@ int glr_occlusion_count(const double *d_xy, int64_t n, double thr,
 /* Edges per tile of the crossing unit space. */
 int glr_crossing_tile(void);
 
-/* Number of edge tile-pair units for m edges (same enumeration as
- * glr_occlusion_units with T = ceil(m / glr_crossing_tile())). */
+/* j-tiles per band of the crossing unit order.  Crossing units are the same
+ * tile pairs (ti <= tj) as for occlusion, T = ceil(m / glr_crossing_tile()),
+ * but ordered by (band of tj, ti, tj) with bands of glr_crossing_band()
+ * consecutive j-tiles (within a band: rows ti below the band first, then the
+ * band's own triangle), so concurrently running CTAs share j-tiles in L2. */
+int glr_crossing_band(void);
+
+/* Number of edge tile-pair units for m edges: T(T+1)/2. */
 uint64_t glr_crossing_units(int64_t m);
 
 /* Bytes of the record buffer glr_crossing_prepare fills for n vertices and
@@ -106,6 +112,18 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges,
                       int64_t m, int with_angle, double ideal,
                       uint64_t unit_begin, uint64_t unit_end, double *d_out,
                       void *stream);
+
+/* Interleaved sharding of the whole unit space (dense triangle when d_list is
+ * NULL, else the candidate list of length list_len): units are cut into
+ * chunks (size derived from the unit count and `world` only) and this call
+ * takes the chunks whose index is rank (mod world).  Every rank sees the same
+ * mix of unit costs, and the partials of ranks 0..world-1 sum exactly to the
+ * whole (the adjacency correction follows the same chunk ownership). */
+int glr_crossing_pairs_interleaved(const void *d_records, int64_t n, int64_t m,
+                                   int with_angle, double ideal,
+                                   const void *d_list, uint64_t list_len,
+                                   int rank, int world, double *d_out,
+                                   void *stream);
 
 /* Per-tile cost weights of prepared records for balanced sharding: d_w[t] =
  * tile + beta * (run starts in tile t), t < ceil(m / glr_crossing_tile()).

@@ -272,12 +272,33 @@ def _tri_coords(u: int, T: int):
     return ti, ti + u
 
 
-def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int):
+def _band_coords(u: int, T: int, W: int):
+    """(ti, tj) of unit u in the banded order of the crossing pass: bands of W
+    consecutive j-tiles; inside band [b0, e): rows ti < b0 (each over the
+    band's w tiles), then the band's own triangle."""
+    b0 = 0
+    while True:
+        e = min(T, b0 + W)
+        w = e - b0
+        count = b0 * w + w * (w + 1) // 2
+        if u < count:
+            break
+        u -= count
+        b0 = e
+    if u < b0 * w:
+        return u // w, b0 + u % w
+    a, c = _tri_coords(u - b0 * w, w)
+    return b0 + a, b0 + c
+
+
+def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int, band=None):
     """(count, dev_sum) restricted to pairs whose tile pair (i//tile, j//tile)
-    has a unit index in [ubeg, uend).  Summing over a partition of
-    [0, T(T+1)/2) gives crossing_scan()."""
+    has a unit index in [ubeg, uend) -- in the banded unit order with band
+    width `band` tiles (None: one band, i.e. row-major).  Summing over a
+    partition of [0, T(T+1)/2) gives crossing_scan()."""
     m = len(edges)
     T = max(1, -(-m // tile))
+    W = T if band is None else int(band)
     e0, e1 = edges[:, 0], edges[:, 1]
     ax, ay, bx, by = xy[e0, 0], xy[e0, 1], xy[e1, 0], xy[e1, 1]
     xmin, xmax = np.minimum(ax, bx), np.maximum(ax, bx)
@@ -285,7 +306,7 @@ def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int):
     theta = axis_angles(ax, ay, bx, by) if ideal is not None else None
     total, dev = 0, 0.0
     for u in range(ubeg, uend):
-        ti, tj = _tri_coords(u, T)
+        ti, tj = _band_coords(u, T, W)
         I = np.arange(ti * tile, min(m, (ti + 1) * tile))[:, None]
         J = np.arange(tj * tile, min(m, (tj + 1) * tile))[None, :]
         if I.size == 0 or J.size == 0:

@@ -32,6 +32,7 @@ SIGNATURES = {
         [_c.c_void_p, _c.c_int64, _c.c_double, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_void_p],
     ),
     "glr_crossing_tile": (_c.c_int, []),
+    "glr_crossing_band": (_c.c_int, []),
     "glr_crossing_units": (_c.c_uint64, [_c.c_int64]),
     "glr_crossing_records_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int64]),
     "glr_crossing_prepare": (
@@ -58,6 +59,11 @@ SIGNATURES = {
     ),
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_take_launch_count": (_c.c_uint64, []),
+    "glr_crossing_pairs_interleaved": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_double, _c.c_void_p, _c.c_uint64,
+         _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p],
+    ),
     "glr_crossing_tile_weights": (
         _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_double, _c.c_void_p, _c.c_void_p]),
     "glr_spatial_sort_edges": (

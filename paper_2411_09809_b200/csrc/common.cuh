@@ -95,6 +95,62 @@ __host__ __device__ inline void tri_unit_coords(uint64_t u, uint64_t T, uint64_t
   *tj = (uint64_t)t + (u - tri_row_start((uint64_t)t, T));
 }
 
+// Banded enumeration of the same unit set, used by the crossing pass so that
+// CTAs running at the same time share j-tiles in L2: units are ordered by
+// (band of tj, ti, tj) with bands of W consecutive j-tiles.  Within band b
+// (tj in [bW, e), w = e - bW): first the full rows ti < bW (w units each),
+// then the triangle ti, tj in [bW, e).  W >= T gives the row-major order.
+__host__ __device__ inline uint64_t band_units_before(uint64_t b, uint64_t W) {
+  // all bands before b are full: unit count of band k = k*W*W + W(W+1)/2
+  return W * W * (b * (b - 1) / 2) + b * (W * (W + 1) / 2);
+}
+
+__host__ __device__ inline void band_unit_coords(uint64_t u, uint64_t T, uint64_t W,
+                                                 uint64_t *ti, uint64_t *tj) {
+  const uint64_t nb = (T + W - 1) / W;
+  uint64_t lo = 0, hi = nb - 1;  // last band whose prefix <= u
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi + 1) >> 1;
+    if (band_units_before(mid, W) <= u) lo = mid; else hi = mid - 1;
+  }
+  const uint64_t b = lo, b0 = b * W, e = (b0 + W < T) ? b0 + W : T, w = e - b0;
+  const uint64_t local = u - band_units_before(b, W);
+  if (local < b0 * w) {
+    *ti = local / w;
+    *tj = b0 + local % w;
+  } else {
+    uint64_t a, c;
+    tri_unit_coords(local - b0 * w, w, &a, &c);
+    *ti = b0 + a;
+    *tj = b0 + c;
+  }
+}
+
+// inverse of band_unit_coords
+__host__ __device__ inline uint64_t band_unit_index(uint64_t ti, uint64_t tj, uint64_t T,
+                                                    uint64_t W) {
+  const uint64_t b = tj / W, b0 = b * W, e = (b0 + W < T) ? b0 + W : T, w = e - b0;
+  const uint64_t base = band_units_before(b, W);
+  if (ti < b0) return base + ti * w + (tj - b0);
+  return base + b0 * w + tri_row_start(ti - b0, w) + (tj - ti);
+}
+
+// next unit in banded order
+__host__ __device__ inline void band_advance(uint64_t T, uint64_t W, uint64_t *ti,
+                                             uint64_t *tj) {
+  const uint64_t b0 = (*tj / W) * W, e = (b0 + W < T) ? b0 + W : T;
+  if (++*tj < e) return;
+  ++*ti;
+  if (*ti < b0) {
+    *tj = b0;
+  } else if (*ti < e) {
+    *tj = *ti;
+  } else {  // next band
+    *ti = 0;
+    *tj = e;
+  }
+}
+
 // Block-wide sum of a double (deterministic: fixed shuffle tree + fixed
 // warp order).  All threads must call; result valid in thread 0.
 template <int NT>

@@ -67,6 +67,13 @@ constexpr int kTile = kThreads * kK;
 constexpr int kMinBlocks = GLR_XMINB;   // CTAs per SM
 constexpr int kUnroll = GLR_XUNROLL;    // j-loop unroll of the off-diagonal tiles
 constexpr int kAdjTile = 128;           // incidence-list tile of adj_kernel
+// j-tiles per band of the unit order (common.cuh band_unit_coords): 2048
+// tiles x 256 edges x ~76 B of records/theta/flags = 40 MB, so the j-tiles
+// the CTAs are sweeping at any moment stay in the 126 MB L2.
+#ifndef GLR_XBAND
+#define GLR_XBAND 2048
+#endif
+constexpr int kBandTiles = GLR_XBAND;
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
@@ -468,7 +475,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                    const double *__restrict__ theta, const int2 *__restrict__ ids,
                    const int *__restrict__ newc, const int2 *__restrict__ ulist, uint64_t T,
-                   uint64_t ubeg, uint64_t uend, uint64_t chunk, double kappa,
+                   uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk,
+                   unsigned srank, unsigned sworld, double kappa,
                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   // ulist == nullptr: units are the implicit upper triangle of tile pairs;
   // otherwise unit u is the explicit tile pair ulist[u] (culled candidates).
@@ -487,16 +495,19 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   // interleaving gives every CTA the same mix (a contiguous split left the
   // slowest CTA ~15% behind).  Consecutive units inside a chunk mostly share
   // ti, so the i-edges stay in registers.
+  // Interleaved sharding: this call owns the chunks whose index is
+  // srank (mod sworld) -- every rank sees the same mix of unit costs.
   const uint64_t nchunks = (uend - ubeg + chunk - 1) / chunk;
 
   unsigned long long total = 0;
   double dsum = 0.0, dcomp = 0.0;  // Kahan over per-unit partials
   IRegs<IDS> R;
   uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
-  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+  for (uint64_t ch = srank + (uint64_t)sworld * blockIdx.x; ch < nchunks;
+       ch += (uint64_t)sworld * gridDim.x) {
   const uint64_t b = ubeg + ch * chunk;
   const uint64_t e = b + chunk < uend ? b + chunk : uend;
-  if (ulist == nullptr) tri_unit_coords(b, T, &ti, &tj);
+  if (ulist == nullptr) band_unit_coords(b, T, W, &ti, &tj);
   for (uint64_t u = b; u < e; ++u) {
     if (ulist != nullptr) {
       const int2 p = ulist[u];
@@ -554,7 +565,7 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
       dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
       dsum = t;
     }
-    if (++tj == T) { ++ti; tj = ti; }
+    if (ulist == nullptr) band_advance(T, W, &ti, &tj);
   }
   }  // chunks
   unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
@@ -574,30 +585,16 @@ __global__ void __launch_bounds__(kAdjTile)
 adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
            const int *__restrict__ inc, const int *__restrict__ offs,
            const long long *__restrict__ wofs, const int2 *__restrict__ ulist, uint64_t ulen,
-           uint64_t T, uint64_t ubeg, uint64_t uend, double kappa,
+           uint64_t T, uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk,
+           unsigned srank, unsigned sworld, double kappa,
            unsigned long long *__restrict__ part_cnt, double *__restrict__ part_dev) {
-  // Units are tile pairs in row-major (lexicographic) order, both for the
-  // implicit triangle and for a culled candidate list (sorted, and containing
-  // every tile pair whose tile bboxes overlap -- hence every adjacent pair's).
-  // A range [ubeg, uend) is therefore the key interval [key(ubeg), key(uend))
-  // with key(ti, tj) = ti*T + tj.
-  uint64_t key_lo, key_hi;
-  {
-    uint64_t a, c;
-    if (ulist == nullptr) {
-      tri_unit_coords(ubeg, T, &a, &c);
-      key_lo = a * T + c;
-      if (uend >= ulen) {
-        key_hi = T * T;
-      } else {
-        tri_unit_coords(uend, T, &a, &c);
-        key_hi = a * T + c;
-      }
-    } else {
-      key_lo = (uint64_t)ulist[ubeg].x * T + (uint64_t)ulist[ubeg].y;
-      key_hi = uend >= ulen ? T * T : (uint64_t)ulist[uend].x * T + (uint64_t)ulist[uend].y;
-    }
-  }
+  // Each adjacent pair belongs to the unit of its tile pair (tl, th): for the
+  // implicit space its index is band_unit_index(tl, th); a culled candidate
+  // list is sorted row-major and contains every tile pair whose tile bboxes
+  // overlap (hence every adjacent pair's), so its index is found by binary
+  // search on key(ti, tj) = ti*T + tj.  The pair is removed here iff the
+  // pair kernel evaluated that unit: u in [ubeg, uend) and its chunk is one
+  // of this call's (interleaved sharding, see cross_pairs_kernel).
   __shared__ int s_e[kAdjTile];
   __shared__ double s_t[kAdjTile];
   __shared__ long long s_v;
@@ -611,10 +608,10 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
     return;
   }
   const long long n = hdr->n;
-  const long long W = wofs[n];
+  const long long nwork = wofs[n];
   unsigned long long cnt = 0;
   double dsum = 0.0, dcomp = 0.0;
-  for (long long w = blockIdx.x; w < W; w += gridDim.x) {
+  for (long long w = blockIdx.x; w < nwork; w += gridDim.x) {
     if (threadIdx.x == 0) {  // vertex owning work item w: last v with wofs[v] <= w
       long long lo = 0, hi = n;
       while (lo < hi) {
@@ -646,8 +643,22 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
       for (int qq = (ti == tj) ? (int)threadIdx.x + 1 : 0; qq < qn; ++qq) {
         const int e2 = s_e[qq];
         const uint64_t lo = (uint64_t)min(e1, e2) / kTile, hi = (uint64_t)max(e1, e2) / kTile;
-        const uint64_t key = lo * T + hi;
-        if (key >= key_lo && key < key_hi) {
+        uint64_t unit;
+        if (ulist == nullptr) {
+          unit = band_unit_index(lo, hi, T, W);
+        } else {
+          const uint64_t key = lo * T + hi;
+          uint64_t a = 0, z = ulen;
+          while (a < z) {
+            const uint64_t mid = (a + z) >> 1;
+            const uint64_t k = (uint64_t)ulist[mid].x * T + (uint64_t)ulist[mid].y;
+            if (k < key) a = mid + 1; else z = mid;
+          }
+          unit = a;
+        }
+        const bool in = unit >= ubeg && unit < uend &&
+                        ((unit - ubeg) / chunk) % sworld == srank;
+        if (in) {
           ++cnt;
           if (ANGLE) s = __dadd_rn(s, angle_dev(t1, s_t[qq], kappa));
         }
@@ -872,8 +883,9 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
 
 int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                    const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
-                   double *d_out, cudaStream_t st) {
-  if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0) {
+                   int srank, int sworld, double *d_out, cudaStream_t st) {
+  if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0 || sworld < 1 || srank < 0 ||
+      srank >= sworld) {
     set_error("glr_crossing_pairs: invalid arguments");
     return GLR_EARG;
   }
@@ -894,7 +906,8 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     return GLR_OK;
   }
   RecView rv = view(const_cast<void *>(d_records), n, m);
-  const int grid = grid_for(uend - ubeg);
+  const uint64_t span = uend - ubeg;
+  const int grid = grid_for((span + sworld - 1) / sworld);
   const int agrid = sm_count() * 8;
   Scratch scr((size_t)(grid + agrid) * (sizeof(unsigned long long) + sizeof(double)), st);
   GLR_CUDA(scr.err);
@@ -903,29 +916,38 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   double *cd = reinterpret_cast<double *>(ac + agrid);
   double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
-  // chunk: at least 8 chunks per CTA for balance, at most 32 units per chunk
-  uint64_t chunk = (uend - ubeg) / ((uint64_t)grid * 8);
+  // chunk: >= 8 chunks per CTA of every rank, <= 32 units per chunk; a
+  // function of the whole range and the rank count only, so all ranks agree
+  uint64_t chunk = span / ((uint64_t)grid_for(span) * 8 * (uint64_t)sworld);
   if (chunk > 32) chunk = 32;
   if (chunk < 1) chunk = 1;
+  const uint64_t W = (uint64_t)kBandTiles;
+  const unsigned r = (unsigned)srank, g = (unsigned)sworld;
   if (with_angle) {
     cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, kappa, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
+        cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
     cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, kappa, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
+        cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
-                                                 d_list, U, T, ubeg, uend, kappa, ac, ad);
+                                                 d_list, U, T, W, ubeg, uend, chunk, r, g, kappa,
+                                                 ac, ad);
     GLR_LAUNCHED("adj_kernel<angle>");
   } else {
     cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, 0.0, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+        cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast>");
     cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, ubeg, uend, chunk, 0.0, cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+        cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
-                                                  d_list, U, T, ubeg, uend, 0.0, ac, ad);
+                                                  d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
+                                                  ac, ad);
     GLR_LAUNCHED("adj_kernel");
   }
   cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, ac, ad, agrid, d_out);
@@ -980,6 +1002,8 @@ extern "C" {
 
 int glr_crossing_tile(void) { return glr::kTile; }
 
+int glr_crossing_band(void) { return glr::kBandTiles; }
+
 int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m, double beta,
                               double *d_w, void *stream) {
   if (d_records == nullptr || d_w == nullptr || m < 0 || n < 0) {
@@ -992,6 +1016,15 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m, doubl
                             glr::as_stream(stream)>>>(rv.newc, beta, d_w);
   GLR_LAUNCHED("tile_weight_kernel");
   return GLR_OK;
+}
+
+int glr_crossing_pairs_interleaved(const void *d_records, int64_t n, int64_t m, int with_angle,
+                                   double ideal, const void *d_list, uint64_t list_len, int rank,
+                                   int world, double *d_out, void *stream) {
+  const uint64_t U = d_list != nullptr ? list_len : glr_crossing_units(m);
+  return glr::crossing_pairs(d_records, n, m, with_angle, ideal,
+                             reinterpret_cast<const int2 *>(d_list), list_len, 0, U, rank, world,
+                             d_out, glr::as_stream(stream));
 }
 
 int glr_crossing_candidates(const void *d_records, int64_t n, int64_t m, void *d_list,
@@ -1018,7 +1051,7 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m, int wit
   }
   return glr::crossing_pairs(d_records, n, m, with_angle, ideal,
                              reinterpret_cast<const int2 *>(d_list), list_len, unit_begin,
-                             unit_end, d_out, glr::as_stream(stream));
+                             unit_end, 0, 1, d_out, glr::as_stream(stream));
 }
 
 uint64_t glr_crossing_units(int64_t m) {
@@ -1036,7 +1069,7 @@ int glr_crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, 
 int glr_crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                        uint64_t unit_begin, uint64_t unit_end, double *d_out, void *stream) {
   return glr::crossing_pairs(d_records, n, m, with_angle, ideal, nullptr, 0, unit_begin,
-                             unit_end, d_out, glr::as_stream(stream));
+                             unit_end, 0, 1, d_out, glr::as_stream(stream));
 }
 
 int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
@@ -1048,7 +1081,7 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
   int rc = glr::crossing_prepare(d_xy, n, d_edges, m, rec.ptr, st);
   if (rc != GLR_OK) return rc;
   return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, nullptr, 0, unit_begin, unit_end,
-                             d_out, st);
+                             0, 1, d_out, st);
 }
 
 int glr_crossing_fast_path(const void *d_records, void *stream) {

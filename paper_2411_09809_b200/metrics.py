@@ -237,6 +237,23 @@ class CrossingRecords:
     def fast_path(self) -> bool:
         return _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream()) == 1
 
+    def partial_interleaved(self, ideal: float | None, rank: int, world: int,
+                            out: torch.Tensor | None = None) -> torch.Tensor:
+        """Device float64[2]: this rank's share of the whole unit space under
+        interleaved chunk ownership (glr_crossing_pairs_interleaved); the
+        ranks' partials sum exactly to the full (count, dev_sum)."""
+        if out is None:
+            out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
+        if self.culled and len(self.list) == 0:
+            return out.zero_()
+        rc = _lib.lib().glr_crossing_pairs_interleaved(
+            _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
+            0.0 if ideal is None else float(ideal),
+            _ptr(self.list) if self.culled else None, len(self.list) if self.culled else 0,
+            int(rank), int(world), _ptr(out), _stream())
+        _lib.check(rc, "glr_crossing_pairs_interleaved")
+        return out
+
     def tile_weights(self, beta: float | None = None) -> np.ndarray:
         """Per j-tile cost weights (glr_crossing_tile_weights), on the host."""
         from .sharding import RUN_START_BETA
@@ -258,7 +275,7 @@ class CrossingRecords:
             return sharding.shard_range(self.units, rank, world)
         w = self.tile_weights()
         if not self.culled:
-            return sharding.triangle_range(w, rank, world)
+            return sharding.triangle_range(w, rank, world, _lib.lib().glr_crossing_band())
         lst = self.list.cpu().numpy()
         unit_w = w[lst[:, 1]] * np.where(lst[:, 0] == lst[:, 1], 0.5, 1.0)
         return sharding.weighted_range(unit_w, rank, world)

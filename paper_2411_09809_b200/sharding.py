@@ -75,8 +75,7 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
         out.zero_()
     if with_crossing and dg.num_edges >= 2:
         rec = records if records is not None else M.CrossingRecords(dg, strategy)
-        b, e = rec.shard(rank, world)
-        rec.partial(ideal, b, e, out=out[0:2])
+        rec.partial_interleaved(ideal, rank, world, out=out[0:2])
     if radius is not None and dg.num_vertices >= 2:
         plan = M.OcclusionPlan(dg, radius, strategy)
         b, e = shard_range(plan.units, rank, world)
@@ -122,9 +121,32 @@ def weighted_range(unit_weights, rank: int, world: int) -> tuple[int, int]:
     return b, max(b, e)
 
 
-def triangle_range(tile_w, rank: int, world: int) -> tuple[int, int]:
-    """Balanced contiguous range of the row-major upper-triangular unit space
-    (ti <= tj) where unit (ti, tj) weighs tile_w[tj] (half on the diagonal)."""
+def _band_unit_weights(w, band: int):
+    """Per-band pieces of the banded unit order (see glr_crossing_band):
+    for each band [b0, e): (b0, e, base unit, weight of one full row over the
+    band, cumulative weights of the band's triangle rows)."""
+    import numpy as np
+
+    T = len(w)
+    out = []
+    base = 0
+    for b0 in range(0, T, band):
+        e = min(T, b0 + band)
+        wb = w[b0:e]
+        full_row = float(wb.sum())
+        suffix = np.cumsum(wb[::-1])[::-1]
+        tri_rows = suffix - 0.5 * wb          # row ti in [b0, e): half diagonal + rest
+        out.append((b0, e, base, full_row, np.cumsum(tri_rows)))
+        wdt = e - b0
+        base += b0 * wdt + wdt * (wdt + 1) // 2
+    return out
+
+
+def triangle_range(tile_w, rank: int, world: int, band: int | None = None) -> tuple[int, int]:
+    """Balanced contiguous range of the upper-triangular unit space (ti <= tj)
+    in the crossing pass's banded order (band width `band` j-tiles; None = one
+    band = row-major), where unit (ti, tj) weighs tile_w[tj] (half on the
+    diagonal)."""
     import numpy as np
 
     if world < 1 or not 0 <= rank < world:
@@ -132,10 +154,12 @@ def triangle_range(tile_w, rank: int, world: int) -> tuple[int, int]:
     w = np.asarray(tile_w, dtype=np.float64)
     T = len(w)
     U = T * (T + 1) // 2
-    suffix = np.cumsum(w[::-1])[::-1]                # sum_{tj >= ti} w[tj]
-    row = suffix - 0.5 * w                           # diagonal unit at half weight
-    row_cum = np.cumsum(row)
-    total = float(row_cum[-1])
+    W = T if band is None else max(1, int(band))
+    bands = _band_unit_weights(w, W)
+    band_tot = np.array([b0 * full + (tri[-1] if len(tri) else 0.0)
+                         for (b0, e, base, full, tri) in bands])
+    band_cum = np.cumsum(band_tot)
+    total = float(band_cum[-1]) if len(band_cum) else 0.0
 
     def unit_at(frac: float) -> int:
         if frac <= 0.0:
@@ -143,20 +167,32 @@ def triangle_range(tile_w, rank: int, world: int) -> tuple[int, int]:
         if frac >= 1.0:
             return U
         target = frac * total
-        ti = int(np.searchsorted(row_cum, target, side="left"))
-        if ti >= T:
+        k = int(np.searchsorted(band_cum, target, side="left"))
+        if k >= len(bands):
             return U
-        before = float(row_cum[ti - 1]) if ti > 0 else 0.0
-        within = np.cumsum(np.concatenate(([0.5 * w[ti]], w[ti + 1:])))
-        tj_off = int(np.searchsorted(within, target - before, side="left"))
-        start = ti * T - ti * (ti - 1) // 2
-        return min(U, start + tj_off + 1)
+        b0, e, base, full, tri = bands[k]
+        t = target - (float(band_cum[k - 1]) if k else 0.0)
+        wdt = e - b0
+        wb = w[b0:e]
+        if b0 > 0 and t <= b0 * full:           # in the full rows below the band
+            ti = min(b0 - 1, int(t // full)) if full > 0 else 0
+            rem = t - ti * full
+            tj_off = int(np.searchsorted(np.cumsum(wb), rem, side="left"))
+            return min(U, base + ti * wdt + min(tj_off, wdt - 1) + 1)
+        t -= b0 * full
+        r = int(np.searchsorted(tri, t, side="left"))
+        r = min(r, wdt - 1)
+        before = float(tri[r - 1]) if r else 0.0
+        within = np.cumsum(np.concatenate(([0.5 * wb[r]], wb[r + 1:])))
+        off = int(np.searchsorted(within, t - before, side="left"))
+        off = min(off, wdt - r - 1)
+        return min(U, base + b0 * wdt + r * wdt - r * (r - 1) // 2 + off + 1)
 
     return unit_at(rank / world), unit_at((rank + 1) / world)
 
 
-def triangle_plan(tile_w, world: int) -> list[tuple[int, int]]:
-    plan = [triangle_range(tile_w, r, world) for r in range(world)]
+def triangle_plan(tile_w, world: int, band: int | None = None) -> list[tuple[int, int]]:
+    plan = [triangle_range(tile_w, r, world, band) for r in range(world)]
     T = len(tile_w)
     assert plan[0][0] == 0 and plan[-1][1] == T * (T + 1) // 2
     assert all(a[1] == b[0] for a, b in zip(plan, plan[1:]))

@@ -84,7 +84,8 @@ def test_config5_occlusion_and_tile_samples(gpu, golden_configs):
     rng = np.random.default_rng(2024)
     for u in rng.integers(0, rec.units, 24).tolist():
         gc, gd = rec.partial(IDEAL, u, u + 1).tolist()
-        oc, od = O.crossing_scan_units(g.xy, g.edges, IDEAL, tile, u, u + 1)
+        oc, od = O.crossing_scan_units(g.xy, g.edges, IDEAL, tile, u, u + 1,
+                                       band=M._lib.lib().glr_crossing_band())
         assert gc == oc
         assert strict_close(gd, od, floor=1e-9)
     for seed in range(3):

@@ -170,7 +170,8 @@ def test_unit_range_partials_sum_to_whole(gpu):
         assert strict_close(sum(p[1] for p in parts), full[1])
         for r, p in enumerate(parts):
             b, e = sharding.shard_range(rec.units, r, world)
-            oc, od = O.crossing_scan_units(g.xy, g.edges, IDEAL, tile, b, e)
+            oc, od = O.crossing_scan_units(g.xy, g.edges, IDEAL, tile, b, e,
+                                           band=M._lib.lib().glr_crossing_band())
             assert p[0] == oc
             assert strict_close(p[1], od, floor=1e-9)
     n = g.num_vertices
@@ -228,3 +229,86 @@ def test_balanced_shards_sum_to_whole(gpu):
             parts = [rec.partial(IDEAL, b, e).tolist() for b, e in ranges]
             assert sum(p[0] for p in parts) == full[0] == 4194903
             assert strict_close(sum(p[1] for p in parts), full[1])
+
+
+@pytest.mark.parametrize("m", [2, 3, 255, 256, 257, 511, 512, 513, 1023, 1025])
+def test_tile_boundaries_dense_and_culled(gpu, m):
+    """Edge counts around the 256-edge tile (padding, diagonal tiles, ragged
+    last tile) on a degenerate-heavy integer lattice, against the oracle."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import metrics as M
+    from paper_2411_09809_b200.model import LayoutGraph
+
+    rng = np.random.default_rng(m)
+    n = max(4, m // 2)
+    xy = rng.integers(0, 12, (n, 2)).astype(np.float64)
+    pairs = rng.integers(0, n, (3 * m, 2))
+    pairs = pairs[np.any(xy[pairs[:, 0]] != xy[pairs[:, 1]], axis=1)]
+    g = LayoutGraph(np.arange(n), xy, pairs)
+    e = g.edges[:m]
+    g = LayoutGraph(np.arange(n), xy, e)
+    want_c, want_d = O.crossing_scan(g.xy, g.edges, IDEAL)
+    want_nc = O.node_occlusion(g.xy, 0.7)
+    for strategy in ("dense", "culled"):
+        c, d = M._crossing_scan(g, IDEAL, strategy=strategy)
+        assert c == want_c, strategy
+        assert strict_close(d, want_d), strategy
+        assert M.node_occlusion(g, 0.7, strategy=strategy) == want_nc, strategy
+
+
+def test_vertex_tile_boundaries(gpu):
+    """Vertex counts around the 1024-vertex occlusion tile."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import metrics as M
+    from paper_2411_09809_b200.model import LayoutGraph
+
+    for n in (2, 1023, 1024, 1025, 2049):
+        xy = np.random.default_rng(n).integers(0, 40, (n, 2)).astype(np.float64)
+        g = LayoutGraph(np.arange(n), xy, [])
+        want = O.node_occlusion(g.xy, 1.0)
+        for strategy in ("dense", "culled"):
+            assert M.node_occlusion(g, 1.0, strategy=strategy) == want, (n, strategy)
+
+
+def test_random_degenerate_graphs(gpu):
+    """Many small graphs on tiny integer grids (collinear, overlapping,
+    coincident and touching segments everywhere) against the oracle."""
+    from oracle import glare_oracle as O
+    import paper_2411_09809_b200 as G
+
+    rng = np.random.default_rng(123)
+    for trial in range(40):
+        n = int(rng.integers(3, 60))
+        side = int(rng.integers(2, 8))
+        xy = rng.integers(0, side, (n, 2)).astype(np.float64)
+        if trial % 3 == 0:
+            xy = xy * 0.1 - 0.3  # non-integer, negative, still degenerate
+        pairs = rng.integers(0, n, (int(rng.integers(1, 150)), 2))
+        pairs = pairs[np.any(xy[pairs[:, 0]] != xy[pairs[:, 1]], axis=1)]
+        if len(pairs) == 0:
+            continue
+        g = G.LayoutGraph(np.arange(n), xy, pairs)
+        c, d = G._crossing_scan(g, IDEAL)
+        oc, od = O.crossing_scan(g.xy, g.edges, IDEAL)
+        assert c == oc and strict_close(d, od), trial
+        r = float(rng.uniform(0.05, 1.0))
+        assert G.node_occlusion(g, r) == O.node_occlusion(g.xy, r), trial
+        assert strict_close(G.minimum_angle(g), O.minimum_angle(g.xy, g.edges)), trial
+        if g.num_edges > 1:
+            assert strict_close(G.edge_length_variation(g),
+                                O.edge_length_variation(g.xy, g.edges)), trial
+
+
+def test_interleaved_shards_sum_to_whole(gpu):
+    """Interleaved chunk ownership (the multi-GPU default): ranks' partials
+    sum exactly to the whole, dense and culled, and match the oracle."""
+    from paper_2411_09809_b200 import metrics as M
+
+    g = graph_from(cases.lattice_stress)
+    dg = M.DeviceGraph.from_graph(g)
+    for strategy in ("dense", "culled"):
+        rec = M.CrossingRecords(dg, strategy)
+        for world in (1, 2, 3, 8):
+            parts = [rec.partial_interleaved(IDEAL, r, world).tolist() for r in range(world)]
+            assert sum(p[0] for p in parts) == 4194903, (strategy, world)
+            assert strict_close(sum(p[1] for p in parts), 1475177.8703388437)

@@ -121,6 +121,18 @@ def test_unit_range_partials_compose():
     parts = [O.crossing_scan_units(g.xy, g.edges, IDEAL, tile, a, b) for a, b in zip(cuts, cuts[1:])]
     assert sum(p[0] for p in parts) == full[0]
     assert rel_close(sum(p[1] for p in parts), full[1])
+    # banded unit order (the crossing kernels' order) is a permutation of the
+    # triangle: every tile pair once, for any band width
+    for band in (1, 2, 3, 5, T):
+        seen = [O._band_coords(u, T, band) for u in range(U)]
+        assert sorted(seen) == [(a, b) for a in range(T) for b in range(a, T)]
+    small = 96
+    Ts = -(-g.num_edges // small)
+    Us = Ts * (Ts + 1) // 2
+    cuts = [0, 7, Us // 3, Us - 5, Us]
+    parts = [O.crossing_scan_units(g.xy, g.edges, IDEAL, small, a, b, band=4)
+             for a, b in zip(cuts, cuts[1:])]
+    assert sum(p[0] for p in parts) == full[0]
     tile_v = 1024
     Tv = -(-g.num_vertices // tile_v)
     Uv = Tv * (Tv + 1) // 2

@@ -95,15 +95,18 @@ def test_balanced_triangle_and_weighted_ranges():
     rng = np.random.default_rng(0)
     for T in (1, 2, 7, 60):
         w = rng.uniform(0.5, 2.0, T)
-        for world in (1, 2, 3, 8):
-            plan = sharding.triangle_plan(w, world)
-            # per-rank weight is balanced within one unit's weight
+        from oracle.glare_oracle import _band_coords
+
+        for band in (None, 1, 3, 16):
+            W = T if band is None else band
             U = T * (T + 1) // 2
-            unit_w = np.array([w[tj] * (0.5 if ti == tj else 1.0)
-                               for ti in range(T) for tj in range(ti, T)])
-            assert len(unit_w) == U
-            loads = [unit_w[b:e].sum() for b, e in plan]
-            assert max(loads) - min(loads) <= 2.0 * unit_w.max() + 1e-9
+            order = [_band_coords(u, T, W) for u in range(U)]
+            unit_w = np.array([w[tj] * (0.5 if ti == tj else 1.0) for ti, tj in order])
+            for world in (1, 2, 3, 8):
+                plan = sharding.triangle_plan(w, world, band)
+                # per-rank weight is balanced within one unit's weight
+                loads = [unit_w[b:e].sum() for b, e in plan]
+                assert max(loads) - min(loads) <= 2.0 * unit_w.max() + 1e-9, (T, band, world)
         lst_w = rng.uniform(0.5, 2.0, 50)
         cuts = [sharding.weighted_range(lst_w, r, 4) for r in range(4)]
         assert cuts[0][0] == 0 and cuts[-1][1] == 50
