@@ -74,6 +74,10 @@ constexpr int kAdjTile = 128;           // incidence-list tile of adj_kernel
 #define GLR_XBAND 2048
 #endif
 constexpr int kBandTiles = GLR_XBAND;
+#ifndef GLR_XCHUNK
+#define GLR_XCHUNK 256
+#endif
+constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bound)
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
@@ -916,10 +920,12 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   double *cd = reinterpret_cast<double *>(ac + agrid);
   double *ad = cd + grid;
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
-  // chunk: >= 8 chunks per CTA of every rank, <= 32 units per chunk; a
-  // function of the whole range and the rank count only, so all ranks agree
+  // chunk: >= 8 chunks per CTA of every rank, <= kMaxChunk units per chunk
+  // (each chunk reloads its i-tile, so longer chunks mean less L2/DRAM
+  // traffic); a function of the whole range and the rank count only, so all
+  // ranks agree
   uint64_t chunk = span / ((uint64_t)grid_for(span) * 8 * (uint64_t)sworld);
-  if (chunk > 32) chunk = 32;
+  if (chunk > (uint64_t)kMaxChunk) chunk = (uint64_t)kMaxChunk;
   if (chunk < 1) chunk = 1;
   const uint64_t W = (uint64_t)kBandTiles;
   const unsigned r = (unsigned)srank, g = (unsigned)sworld;
