@@ -4,13 +4,14 @@ BASELINE.json config 5 -- the strong-scaling configuration -- at N B200s.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 is launched by torchrun (one process per GPU, NCCL): every rank builds
-the same seeded synthetic C5 graph, takes its contiguous share of the
-upper-triangular tile-pair unit space, and the partials are combined with one
-allreduce; scaling is strong (fixed total work).
+the same seeded synthetic C5 graph, owns every world-th chunk of the
+upper-triangular tile-pair unit space (crossing; contiguous ranges for
+occlusion), and the partials are combined with one allreduce (SURVEY.md
+8(e)); scaling is strong (fixed total work).
 
 Step = one fused E_c + E_ca pass (glr_crossing_pairs with the angle sum) over
-the whole C5 edge set, inputs resident in HBM (records 320 MB > 126 MB L2, so
-no L2 flush is needed).  `value` = m(m-1)/2 algorithmic edge-pair tests per
+the whole C5 edge set, inputs resident in HBM (records ~390 MB > 126 MB L2,
+so no L2 flush is needed).  `value` = m(m-1)/2 algorithmic edge-pair tests per
 second over the K timed steps (max over ranks).  `e2e` = the same metric
 through the public API with host (pinned) inputs: H2D of xy+edges, prologue,
 pair pass, allreduce, D2H of the result.  `occlusion` = node-pair tests/s of
@@ -42,6 +43,10 @@ CONFIG = 5
 FP64_PER_PAIR_EC = 18      # DADD/DMUL of the bit-exact predicate
 FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
 FP64_PER_PAIR_NC = 5
+# Bytes the pair kernel must read at least once per launch: EdgeRec 64 B +
+# theta 8 B + ids 8 B + run-start flag 4 B per edge.
+REC_BYTES_PER_EDGE = 84
+C5_DRAM_BYTES_PER_LAUNCH = 227_204_840_192 + 191_279_104   # profiles/r01_dram_c5.txt
 CPU_SAMPLE_EDGES = 120_000
 CPU_SAMPLE_SEED = 99
 
@@ -178,7 +183,7 @@ def _config_desc(g, p, world):
             "edge_pairs": int(g.num_edges) * (int(g.num_edges) - 1) // 2,
             "node_pairs": int(g.num_vertices) * (int(g.num_vertices) - 1) // 2,
             "ideal_deg": 70.0, "radius": p["radius"], "parallelism": f"units{world}",
-            "l2": "inputs (320 MB records) exceed the 126 MB L2; no flush needed"}
+            "l2": "inputs (~390 MB records) exceed the 126 MB L2; no flush needed"}
 
 
 def main():
@@ -379,7 +384,12 @@ def main():
                      "kernel": "cross_pairs_kernel<fast,angle>",
                      "kernel_ms": kernel_ms,
                      "fp64_per_pair": FP64_PER_PAIR_ECA,
-                     "traffic": None},
+                     # DRAM read+write bytes of one full-C5 launch from ncu
+                     # (profiles/r01_dram_c5.txt); per-rank share for N>1.
+                     # The kernel is FP64-bound: 227 GB over 10.6 s = 21 GB/s.
+                     "traffic": C5_DRAM_BYTES_PER_LAUNCH / world,
+                     "traffic_unit": "bytes/launch (dram__bytes_read+write, ncu)",
+                     "algorithmic_bytes": REC_BYTES_PER_EDGE * m},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 3 * 8},

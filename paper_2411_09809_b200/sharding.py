@@ -1,9 +1,15 @@
 """Multi-GPU sharding of the all-pairs passes.
 
 Both all-pairs passes enumerate an upper-triangular space of tile-pair units
-(``glr_*_units``).  Rank g of G takes the contiguous range
-[floor(gU/G), floor((g+1)U/G)); units have equal cost (diagonal ones half), so
-the static split is balanced to within one unit.  Inputs are replicated (each
+(``glr_*_units``).  Occlusion units have equal cost (diagonal ones half), so
+rank g of G takes the contiguous range [floor(gU/G), floor((g+1)U/G)).
+Crossing units do not (run reuse makes a j-tile's cost depend on its run
+structure), so ``sharded_evaluate`` uses interleaved ownership instead: the
+crossing kernel deals units to CTAs in chunks and rank g keeps the chunks
+whose index is g (mod G) (``glr_crossing_pairs_interleaved``), which balances
+to 1.4% over 8 ranks on C5 with no cost model.  The cost-weighted contiguous
+splits further down remain for callers that want contiguous ranges
+(``CrossingRecords.shard``).  Inputs are replicated (each
 rank holds xy/edges: 24 + 64 MB for C5), every rank computes its partial
 (count, dev_sum, occlusion count) on its own device with no data-path
 collective, and ONE allreduce(sum) of a float64[3] buffer combines them --
