@@ -198,9 +198,18 @@ int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges,
 
 /* ---- introspection (tests / bench) --------------------------------------- */
 
-/* 1 if the prepared records take the fast sign path, 0 for the general
- * exact-comparison path (synchronous: reads the records header). */
+/* Pair-kernel mode of the prepared records (synchronous: reads the records
+ * header): 0 = general exact-comparison path (any input), 1 = FP64 float-view
+ * sign path with adjacency correction, 2 = certified packed-FP32 filter with
+ * exact FP64 fallback (the default whenever every nonzero |coordinate| lies
+ * in [2^-160, 2^500]).  All modes give identical results; -1 on error. */
 int glr_crossing_fast_path(const void *d_records, void *stream);
+
+/* Overrides the pair-kernel mode (0, 1 or 2, see glr_crossing_fast_path) of
+ * prepared records, for cross-checking the modes against each other; modes
+ * 1 and 2 fall back to 0 when the input is outside the fast window.
+ * Stream-ordered. */
+int glr_crossing_set_mode(void *d_records, int mode, void *stream);
 
 /* Number of kernel launches issued by this thread since the last call
  * (counter is reset by the call). */

@@ -91,8 +91,8 @@ struct __align__(16) EdgeRec {
 static_assert(sizeof(EdgeRec) == 64, "EdgeRec must be 64 bytes");
 
 struct __align__(16) RecHeader {
-  int fast;  // 1: fast sign path admissible
-  int pad0;
+  int fast;        // pair-kernel mode: kModeGeneral / kModeSign / kModeFilter
+  int admissible;  // 1: every nonzero |coordinate| in [2^-160, 2^500]
   long long n;
   long long m;
   long long m_pad;
@@ -102,11 +102,51 @@ struct __align__(16) RecHeader {
 };
 static_assert(sizeof(RecHeader) == 256, "RecHeader must be 256 bytes");
 
+// Pair-kernel modes (RecHeader::fast).  General: doubles compared directly,
+// ids tested per pair (any input).  Sign: float view of the FP64 cross
+// products + adjacency correction (fast window only).  Filter: certified
+// packed-FP32 filter with exact FP64 fallback (fast window only, default).
+constexpr int kModeGeneral = 0;
+constexpr int kModeSign = 1;
+constexpr int kModeFilter = 2;
+#ifdef GLR_XNOFILTER
+constexpr int kModeFastDefault = kModeSign;
+#else
+constexpr int kModeFastDefault = kModeFilter;
+#endif
+
+// Filter record of an edge (32 B): endpoint coordinates translated to the
+// lower-left corner of the edges' bounding box and scaled by a power of two
+// into [0, 1/2], rounded to FP32; the FP32 direction b - a scaled by a
+// per-edge power of two 2^k (sabx, and -saby pre-negated) such that a
+// product of two of its cross products exceeding 1 in magnitude certifies
+// both factors' signs; theta.  This is
+// the shared-memory form of a j-edge (two broadcast LDS.128).
+struct __align__(16) FRec {
+  float ax, ay, bx, by;
+  float sabx, nsaby;
+  double theta;
+};
+static_assert(sizeof(FRec) == 32, "FRec must be 32 bytes");
+
+// In HBM the filter records of a tile are stored field-major and paired the
+// way the kernel packs its i-edges: v[f][g][p] = (field f of tile slot
+// 2g*kThreads + p, of slot (2g+1)*kThreads + p), so each packed i-register
+// pair is one 64-bit load (f = ax, ay, bx, by, sabx, nsaby).
+constexpr int kFGroups = GLR_XK / 2;
+struct __align__(16) FTile {
+  float2 v[6][kFGroups][kThreads];
+  double theta[kTile];
+};
+static_assert(sizeof(FTile) == (size_t)kTile * sizeof(FRec), "FTile must be 32 B per edge");
+
 // Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
-// inc[2m] (incident edge ids grouped by vertex) | offs[n+1] | wofs[n+1].
+// newc[m_pad] | frec[m_pad] | inc[2m] (incident edge ids grouped by vertex) |
+// offs[n+1] | wofs[n+1].
 struct RecView {
   RecHeader *hdr;
   EdgeRec *rec;
+  FTile *ftile;
   double *theta;
   int2 *ids;
   int *newc;  // 1 if edge e starts a run of edges sharing endpoint a (or a tile)
@@ -119,7 +159,7 @@ inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; 
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t rec, theta, ids, newc, inc, offs, wofs, total;
+  size_t rec, theta, ids, newc, frec, inc, offs, wofs, total;
 };
 
 inline Layout layout(int64_t n, int64_t m) {
@@ -130,7 +170,8 @@ inline Layout layout(int64_t n, int64_t m) {
   L.theta = L.rec + al256((size_t)mp * sizeof(EdgeRec));
   L.ids = L.theta + al256((size_t)mp * sizeof(double));
   L.newc = L.ids + al256((size_t)mp * sizeof(int2));
-  L.inc = L.newc + al256((size_t)mp * sizeof(int));
+  L.frec = L.newc + al256((size_t)mp * sizeof(int));
+  L.inc = L.frec + al256((size_t)mp * sizeof(FRec));
   L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
   L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
   L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
@@ -146,6 +187,7 @@ inline RecView view(void *base, int64_t n, int64_t m) {
   v.theta = reinterpret_cast<double *>(p + L.theta);
   v.ids = reinterpret_cast<int2 *>(p + L.ids);
   v.newc = reinterpret_cast<int *>(p + L.newc);
+  v.ftile = reinterpret_cast<FTile *>(p + L.frec);
   v.inc = reinterpret_cast<int *>(p + L.inc);
   v.offs = reinterpret_cast<int *>(p + L.offs);
   v.wofs = reinterpret_cast<long long *>(p + L.wofs);
@@ -274,7 +316,64 @@ __global__ void header_kernel(RecHeader *hdr, int64_t n, int64_t m, int64_t m_pa
   hdr->m_pad = m_pad;
   hdr->maxabs_bits = mx;
   hdr->minabs_bits = mn;
-  hdr->fast = (dmx <= kMaxAbsFast && dmn >= kMinAbsFast) ? 1 : 0;
+  const int ok = (dmx <= kMaxAbsFast && dmn >= kMinAbsFast) ? 1 : 0;
+  hdr->admissible = ok;
+  hdr->fast = ok ? kModeFastDefault : kModeGeneral;
+}
+
+// Filter records (FRec).  x0/y0 = smallest endpoint coordinate, W = largest
+// extent rounded up, s = 2^-(ilogb(W)+2) so that (x - x0) * s lies in
+// [0, 1/2] after the (monotone) roundings.  Per edge: L = |abx| + |aby| of
+// the FP32 direction, tau = 2^-22 * L * (1 + 2^-18) >= E * C * (1 + u) with
+// E = 2^-21 the cross-product error bound and C = L/2 (1 + 2^-20) the
+// cross-product magnitude bound, and the direction is scaled by
+// 2^k, 2k <= -ilogb(tau) - 1, so 2^2k <= 1/tau.  Degenerate FP32 directions
+// (L == 0) get a zero direction: their products are 0, never certain.
+__global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *sx,
+                            const double *sy) {
+  const double x0 = sx[0], y0 = sy[0];
+  const double W = fmax(__dsub_ru(sx[2 * m - 1], x0), __dsub_ru(sy[2 * m - 1], y0));
+  const double s = (W > 0.0 && W <= 0x1p1000) ? ldexp(1.0, -(ilogb(W) + 2)) : 1.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m_pad;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    FRec f;
+    if (e < m) {
+      const EdgeRec r = rv.rec[e];
+      f.ax = __double2float_rn(__dmul_rn(__dsub_rn(r.ax, x0), s));
+      f.ay = __double2float_rn(__dmul_rn(__dsub_rn(r.ay, y0), s));
+      f.bx = __double2float_rn(__dmul_rn(__dsub_rn(r.bx, x0), s));
+      f.by = __double2float_rn(__dmul_rn(__dsub_rn(r.by, y0), s));
+      const float abx = __fsub_rn(f.bx, f.ax), aby = __fsub_rn(f.by, f.ay);
+      const double L = fabs((double)abx) + fabs((double)aby);
+      if (L > 0.0) {
+        const double tau = L * 0x1p-22 * (1.0 + 0x1p-18);
+        const int k = (-ilogb(tau) - 1) / 2;  // tau < 2^-21, so the numerator is > 0
+        f.sabx = scalbnf(abx, k);
+        f.nsaby = -scalbnf(aby, k);
+      } else {
+        f.sabx = 0.0f;
+        f.nsaby = 0.0f;
+      }
+      f.theta = rv.theta[e];
+    } else {
+      f.ax = f.ay = f.bx = f.by = f.sabx = f.nsaby = 0.0f;
+      f.theta = 0.0;
+    }
+    FTile &t = rv.ftile[e / kTile];
+    const int slot = (int)(e % kTile);
+    const int g = slot / (2 * kThreads), h = (slot / kThreads) & 1, q = slot % kThreads;
+    const float vals[6] = {f.ax, f.ay, f.bx, f.by, f.sabx, f.nsaby};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      float *pair = reinterpret_cast<float *>(&t.v[k][g][q]);
+      pair[h] = vals[k];
+    }
+    t.theta[slot] = f.theta;
+  }
+}
+
+__global__ void set_mode_kernel(RecHeader *hdr, int mode) {
+  hdr->fast = (mode != kModeGeneral && hdr->admissible) ? mode : kModeGeneral;
 }
 
 // ------------------------------------------------------------ pair kernels --
@@ -474,6 +573,188 @@ __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const Edge
   }
 }
 
+// ------------------------------------------------ certified FP32 filter --
+//
+// Packed-FP32 (FFMA2/FMUL2/FADD2) evaluation of the four cross products of
+// two i-edges against one j-edge per instruction.  With the FRec scaling,
+// c1^ = 2^ki c1~, c2^ = 2^ki c2~ (ki from edge i), c3^, c4^ with kj, where
+// |c~ - c_exact| <= E = 2^-21 for every c (error analysis in DESIGN.md,
+// including the FP64 rounding of the reference's own c), and |c~| <= C.
+// P12 = fl(c1^ c2^) > 1 in magnitude therefore implies |c1~|, |c2~| > E, so
+// sign(c1_fp64) = sign(c1~) != 0 (same for c2), and likewise P34.  With
+// M = max(P12, P34):
+//   M < -1  : both pairs strictly straddle in exact arithmetic, so the
+//             segments cross properly -> bboxes overlap, no shared vertex
+//             (a shared vertex makes one exact c zero): the reference counts
+//             the pair;
+//   M > 1   : one pair certainly does not straddle: not counted;
+//   |M| <= 1: uncertain -> exact FP64 evaluation (exact_pair) of the
+//             reference predicate for that pair.
+// The fast window (hdr->admissible) guarantees the reference's FP64
+// products c1*c2 never underflow, so its test equals the sign test.
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_bcast(float a) { return f2_pack(a, a); }
+__device__ __forceinline__ float f2_lo(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float f2_hi(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+constexpr int kGroups = kK / 2;  // packed i-edge pairs per thread
+static_assert(kK % 2 == 0, "the filter packs i-edges in pairs");
+
+struct FIRegs {
+  uint64_t ax[kGroups], ay[kGroups], bx[kGroups], by[kGroups], sabx[kGroups], nsaby[kGroups];
+  double th[kK];
+};
+
+// i-edge k of group g is tile slot threadIdx.x + (2g + h) * kThreads, h = 0/1
+// in the low/high half of the packed registers (one 64-bit load each).
+template <bool ANGLE>
+__device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint64_t ti) {
+  const FTile &t = ftile[ti];
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][g][threadIdx.x]);
+    constexpr int kField = kFGroups * kThreads;  // uint64 stride between fields
+    R.ax[g] = v[0 * kField];
+    R.ay[g] = v[1 * kField];
+    R.bx[g] = v[2 * kField];
+    R.by[g] = v[3 * kField];
+    R.sabx[g] = v[4 * kField];
+    R.nsaby[g] = v[5 * kField];
+    R.th[2 * g] = ANGLE ? t.theta[threadIdx.x + (2 * g) * kThreads] : 0.0;
+    R.th[2 * g + 1] = ANGLE ? t.theta[threadIdx.x + (2 * g + 1) * kThreads] : 0.0;
+  }
+}
+
+// Exact reference predicate for one pair (general semantics: doubles
+// compared directly, ids tested), used for the filter's uncertain pairs.
+// Returns -1 for no hit, else the pair's angle deviation (0 without ANGLE).
+template <bool ANGLE>
+__device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
+                                             const int2 *__restrict__ ids,
+                                             const double *__restrict__ theta, int64_t ei,
+                                             int64_t ej, double kappa) {
+  const EdgeRec a = rec[ei], c = rec[ej];
+  const int2 ia = ids[ei], ic = ids[ej];
+  bool ok = (c.rxmax >= a.rxmin) & (a.rxmax >= c.rxmin) & (c.rymax >= a.rymin) &
+            (a.rymax >= c.rymin);
+  ok &= (ia.x != ic.x) & (ia.x != ic.y) & (ia.y != ic.x) & (ia.y != ic.y);
+  const double dcx = __dsub_rn(c.ax, a.ax);
+  const double dcy = __dsub_rn(c.ay, a.ay);
+  const double ddx = __dsub_rn(c.bx, a.ax);
+  const double ddy = __dsub_rn(c.by, a.ay);
+  const double ebx = __dsub_rn(a.bx, c.ax);
+  const double eby = __dsub_rn(a.by, c.ay);
+  const double c1 = __dsub_rn(__dmul_rn(a.abx, dcy), __dmul_rn(a.aby, dcx));
+  const double c2 = __dsub_rn(__dmul_rn(a.abx, ddy), __dmul_rn(a.aby, ddx));
+  const double c3 = __dsub_rn(__dmul_rn(c.aby, dcx), __dmul_rn(c.abx, dcy));
+  const double c4 = __dsub_rn(__dmul_rn(c.abx, eby), __dmul_rn(c.aby, ebx));
+  const bool s_cd = ((c1 <= 0.0) & (c2 >= 0.0)) | ((c1 >= 0.0) & (c2 <= 0.0));
+  const bool s_ab = ((c3 <= 0.0) & (c4 >= 0.0)) | ((c3 >= 0.0) & (c4 <= 0.0));
+  if (!(ok & s_cd & s_ab)) return -1.0;
+  return ANGLE ? angle_dev(theta[ei], theta[ej], kappa) : 0.0;
+}
+
+// One j-edge (from shared memory) against the thread's K i-edges.
+template <bool ANGLE, bool DIAG>
+__device__ __forceinline__ void filter_row(const FIRegs &R, const float4 *sj4, int jj,
+                                           unsigned (&cnt)[kK], double (&dev)[kK],
+                                           double kappa, const EdgeRec *__restrict__ rec,
+                                           const int2 *__restrict__ ids,
+                                           const double *__restrict__ theta, int64_t ibase,
+                                           int64_t j) {
+  const float4 q0 = sj4[2 * jj];      // cx cy dx dy
+  const float4 q1 = sj4[2 * jj + 1];  // scdx -scdy theta
+  const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
+  const uint64_t DX = f2_bcast(q0.z), DY = f2_bcast(q0.w);
+  const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y);
+  const double thj = ANGLE ? __hiloint2double(__float_as_int(q1.w), __float_as_int(q1.z)) : 0.0;
+  bool unc[kK];
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    const uint64_t t1 = f2_sub(CY, R.ay[g]), t2 = f2_sub(CX, R.ax[g]);  // c - a
+    const uint64_t t3 = f2_sub(DY, R.ay[g]), t4 = f2_sub(DX, R.ax[g]);  // d - a
+    const uint64_t t5 = f2_sub(CY, R.by[g]), t6 = f2_sub(CX, R.bx[g]);  // c - b
+    // c1 = ab x (c - a), c2 = ab x (d - a); c3' = -c3 = cd x (c - a) with
+    // c - a = -(a - c), c4' = -c4 = cd x (c - b): P34 = c3' c4' = c3 c4
+    const uint64_t c1 = f2_fma(R.sabx[g], t1, f2_mul(R.nsaby[g], t2));
+    const uint64_t c2 = f2_fma(R.sabx[g], t3, f2_mul(R.nsaby[g], t4));
+    const uint64_t c3 = f2_fma(SCDX, t1, f2_mul(NSCDY, t2));
+    const uint64_t c4 = f2_fma(SCDX, t5, f2_mul(NSCDY, t6));
+    const uint64_t p12 = f2_mul(c1, c2), p34 = f2_mul(c3, c4);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * g + h;
+      float M = fmaxf(h ? f2_hi(p12) : f2_lo(p12), h ? f2_hi(p34) : f2_lo(p34));
+      if (DIAG && !(jj > (int)threadIdx.x + k * kThreads)) M = 2.0f;  // masked: certain miss
+      unc[k] = fabsf(M) <= 1.0f;
+      // @(M < -1) cnt += 1 (and dev += t): predicated adds, no selects
+      if (ANGLE) {
+        // dev += hit ? t : 0 as fma(t, {0.0 | 1.0}, dev): one DFMA and one SEL
+        // (exact: fma(t, 1, dev) == dev + t, fma(t, 0, dev) == dev)
+        const double t = angle_dev(R.th[k], thj, kappa);
+        int hw;
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.f32 p, %2, 0fBF800000;\n\t"
+            "@p add.u32 %0, %0, 1;\n\t"
+            "selp.b32 %1, 1072693248, 0, p;\n\t}"
+            : "+r"(cnt[k]), "=r"(hw)
+            : "f"(M));
+        dev[k] = __fma_rn(t, __hiloint2double(hw, 0), dev[k]);
+      } else {
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.f32 p, %1, 0fBF800000;\n\t"
+            "@p add.u32 %0, %0, 1;\n\t}"
+            : "+r"(cnt[k])
+            : "f"(M));
+      }
+    }
+  }
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < kK; ++k) any |= unc[k];
+  if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      if (unc[k]) {
+        const double t =
+            exact_pair<ANGLE>(rec, ids, theta, ibase + threadIdx.x + k * kThreads, j, kappa);
+        if (t >= 0.0) {
+          cnt[k] += 1u;
+          if (ANGLE) dev[k] = __dadd_rn(dev[k], t);
+        }
+      }
+    }
+  }
+}
+
 template <bool FAST, bool ANGLE>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
@@ -571,6 +852,99 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
     }
     if (ulist == nullptr) band_advance(T, W, &ti, &tj);
   }
+  }  // chunks
+  unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
+  double bd = block_sum<kThreads>(dsum, red_d);
+  if (threadIdx.x == 0) {
+    cta_cnt[blockIdx.x] = bc;
+    cta_dev[blockIdx.x] = bd;
+  }
+}
+
+// Filter-mode pair kernel (hdr->fast == kModeFilter): same unit space,
+// chunking and reductions as cross_pairs_kernel; the j-tile's FRecs are
+// staged in shared memory (8 KB) and read as two broadcast LDS.128 per
+// j-edge.  Shared-vertex pairs are never certain (an exact c is 0), so they
+// reach exact_pair, which tests ids: no adjacency correction in this mode.
+template <bool ANGLE>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
+                    const FTile *__restrict__ ftile, const double *__restrict__ theta,
+                    const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
+                    uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk, unsigned srank,
+                    unsigned sworld, double kappa, unsigned long long *__restrict__ cta_cnt,
+                    double *__restrict__ cta_dev) {
+  if (hdr->fast != kModeFilter) return;
+  __shared__ __align__(16) float4 sj4[2 * kTile];
+  __shared__ unsigned long long red_u[kThreads / 32];
+  __shared__ double red_d[kThreads / 32];
+  const uint64_t nchunks = (uend - ubeg + chunk - 1) / chunk;
+  unsigned long long total = 0;
+  double dsum = 0.0, dcomp = 0.0;
+  FIRegs R;
+  uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
+  for (uint64_t ch = srank + (uint64_t)sworld * blockIdx.x; ch < nchunks;
+       ch += (uint64_t)sworld * gridDim.x) {
+    const uint64_t b = ubeg + ch * chunk;
+    const uint64_t e = b + chunk < uend ? b + chunk : uend;
+    if (ulist == nullptr) band_unit_coords(b, T, W, &ti, &tj);
+    for (uint64_t u = b; u < e; ++u) {
+      if (ulist != nullptr) {
+        const int2 p = ulist[u];
+        ti = (uint64_t)p.x;
+        tj = (uint64_t)p.y;
+      }
+      if (ti != cur_ti) {
+        load_fi<ANGLE>(R, ftile, ti);
+        cur_ti = ti;
+      }
+      __syncthreads();  // previous tile fully consumed
+      {  // unpack the j-tile into per-edge FRecs
+        const FTile &t = ftile[tj];
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) {
+          float2 v[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) v[k] = t.v[k][g][threadIdx.x];
+          const int s0 = (2 * g) * kThreads + threadIdx.x, s1 = s0 + kThreads;
+          const double th0 = t.theta[s0], th1 = t.theta[s1];
+          sj4[2 * s0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+          sj4[2 * s0 + 1] = make_float4(v[4].x, v[5].x, __int_as_float(__double2loint(th0)),
+                                        __int_as_float(__double2hiint(th0)));
+          sj4[2 * s1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+          sj4[2 * s1 + 1] = make_float4(v[4].y, v[5].y, __int_as_float(__double2loint(th1)),
+                                        __int_as_float(__double2hiint(th1)));
+        }
+      }
+      __syncthreads();
+      unsigned cnt[kK];
+      double dev[kK];
+#pragma unroll
+      for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+      const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
+      if (ti == tj) {
+        for (int jj = 0; jj < kTile; ++jj)
+          filter_row<ANGLE, true>(R, sj4, jj, cnt, dev, kappa, rec, ids, theta, ibase,
+                                  jbase + jj);
+      } else {
+#pragma unroll kUnroll
+        for (int jj = 0; jj < kTile; ++jj)
+          filter_row<ANGLE, false>(R, sj4, jj, cnt, dev, kappa, rec, ids, theta, ibase,
+                                   jbase + jj);
+      }
+      unsigned c = 0;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
+      total += c;
+      if (ANGLE) {
+        double y = __dsub_rn(s, dcomp);
+        double t = __dadd_rn(dsum, y);
+        dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
+        dsum = t;
+      }
+      if (ulist == nullptr) band_advance(T, W, &ti, &tj);
+    }
   }  // chunks
   unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
   double bd = block_sum<kThreads>(dsum, red_d);
@@ -859,6 +1233,8 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
     count_launch(4);
     rank_kernel<<<blocks_for(mm, nt, 16), nt, 0, st>>>(mm, rv, xs, ys, sx, sy);
     GLR_LAUNCHED("rank_kernel");
+    frec_kernel<<<blocks_for(m_pad, nt, 16), nt, 0, st>>>(mm, m_pad, rv, sx, sy);
+    GLR_LAUNCHED("frec_kernel");
     // incidence lists grouped by vertex; stable, so each list is ordered
     // (edges where the vertex is first, then where it is second, by edge id)
     tb = t_cub;
@@ -938,6 +1314,10 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
+    cross_filter_kernel<true><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.ftile, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
+        cc, cd);
+    GLR_LAUNCHED("cross_filter_kernel<angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                  d_list, U, T, W, ubeg, uend, chunk, r, g, kappa,
                                                  ac, ad);
@@ -951,6 +1331,10 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
+    cross_filter_kernel<false><<<grid, kThreads, 0, st>>>(
+        rv.hdr, rv.rec, rv.ftile, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+        cc, cd);
+    GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                   d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
                                                   ac, ad);
@@ -1088,6 +1472,17 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
   if (rc != GLR_OK) return rc;
   return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, nullptr, 0, unit_begin, unit_end,
                              0, 1, d_out, st);
+}
+
+int glr_crossing_set_mode(void *d_records, int mode, void *stream) {
+  if (d_records == nullptr || mode < glr::kModeGeneral || mode > glr::kModeFilter) {
+    glr::set_error("glr_crossing_set_mode: invalid arguments (mode %d)", mode);
+    return GLR_EARG;
+  }
+  glr::set_mode_kernel<<<1, 1, 0, glr::as_stream(stream)>>>(
+      reinterpret_cast<glr::RecHeader *>(d_records), mode);
+  GLR_LAUNCHED("set_mode_kernel");
+  return GLR_OK;
 }
 
 int glr_crossing_fast_path(const void *d_records, void *stream) {

@@ -234,8 +234,26 @@ class CrossingRecords:
     def units(self) -> int:
         return len(self.list) if self.culled else crossing_units(self.m)
 
+    #: pair-kernel modes (glr_crossing_fast_path / glr_crossing_set_mode)
+    MODE_GENERAL, MODE_SIGN, MODE_FILTER = 0, 1, 2
+
+    def mode(self) -> int:
+        """Pair-kernel mode of these records (synchronises the stream)."""
+        mode = _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream())
+        if mode < 0:
+            _lib.check(_lib.GLR_ECUDA, "glr_crossing_fast_path")
+        return mode
+
+    def set_mode(self, mode: int) -> "CrossingRecords":
+        """Force a pair-kernel mode (cross-checks); 1 and 2 degrade to 0
+        outside the fast window.  All modes give identical results."""
+        _lib.check(_lib.lib().glr_crossing_set_mode(_ptr(self.buf), int(mode), _stream()),
+                   "glr_crossing_set_mode")
+        return self
+
     def fast_path(self) -> bool:
-        return _lib.lib().glr_crossing_fast_path(_ptr(self.buf), _stream()) == 1
+        """True when the input lies in the fast window (modes 1/2)."""
+        return self.mode() != self.MODE_GENERAL
 
     def partial_interleaved(self, ideal: float | None, rank: int, world: int,
                             out: torch.Tensor | None = None) -> torch.Tensor:

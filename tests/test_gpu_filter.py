@@ -1,0 +1,191 @@
+"""GPU: the certified packed-FP32 crossing filter (pair-kernel mode 2, the
+default inside the fast window) against the general exact-comparison kernel
+(mode 0), the FP64 float-view sign kernel (mode 1) and the C oracle, on
+inputs built to defeat a filter: near-collinear triples, exact collinear
+lattice points, coordinates far from the origin, mixed scales, very short
+edges, hubs (shared vertices) and coincident vertices with distinct ids.
+
+Modes 0 and 2 accumulate every pair in the same order, so their (count,
+dev_sum) must agree bit for bit; mode 1 subtracts its adjacency correction
+afterwards, so its dev_sum is compared at 1e-12.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import strict_close
+
+pytestmark = pytest.mark.gpu
+
+IDEAL = 7.0 * math.pi / 18.0
+
+
+def _graph(xy, pairs):
+    from paper_2411_09809_b200.model import LayoutGraph
+
+    xy = np.asarray(xy, dtype=np.float64)
+    return LayoutGraph(np.arange(len(xy)), xy, np.asarray(pairs, dtype=np.int64))
+
+
+def _random_pairs(rng, n, m):
+    u = rng.integers(0, n, 3 * m)
+    v = rng.integers(0, n, 3 * m)
+    keep = u != v
+    p = np.stack([u[keep], v[keep]], 1)[:m]
+    return p
+
+
+def near_collinear(seed=1, lines=60, per_line=20):
+    """Points on random lines, perturbed by ~1e-9 of the extent: many cross
+    products within the filter's uncertainty band."""
+    rng = np.random.default_rng(seed)
+    pts = []
+    for _ in range(lines):
+        p0 = rng.uniform(0, 1, 2)
+        d = rng.normal(size=2)
+        d /= np.linalg.norm(d)
+        t = rng.uniform(-0.5, 0.5, per_line)
+        q = p0 + t[:, None] * d + rng.normal(scale=1e-9, size=(per_line, 2))
+        pts.append(q)
+    xy = np.concatenate(pts)
+    n = len(xy)
+    pairs = [(i, i + 1) for i in range(0, n - 1)] + [tuple(p) for p in _random_pairs(rng, n, n)]
+    return xy, pairs
+
+
+def exact_lattice(seed=2, side=6, m=1500):
+    """Integer lattice with many exactly collinear vertex/edge triples."""
+    rng = np.random.default_rng(seed)
+    gx, gy = np.meshgrid(np.arange(side), np.arange(side))
+    xy = np.stack([gx.ravel(), gy.ravel()], 1).astype(np.float64)
+    return xy, _random_pairs(rng, len(xy), m)
+
+
+def far_offset(seed=3, n=600, m=2000, offset=2.0 ** 40):
+    """Coordinates 2^40 + small integers/halves: the FP32 filter must work on
+    translated coordinates."""
+    rng = np.random.default_rng(seed)
+    xy = offset + rng.integers(0, 200, (n, 2)).astype(np.float64) * 0.5
+    xy = np.unique(xy, axis=0)
+    return xy, _random_pairs(rng, len(xy), m)
+
+
+def mixed_scales(seed=4, n=800, m=2500):
+    """A dense cluster of extent 1e-7 plus long edges spanning [0, 1]."""
+    rng = np.random.default_rng(seed)
+    cluster = 0.5 + rng.uniform(0, 1e-7, (n, 2))
+    far = rng.uniform(0, 1, (50, 2))
+    xy = np.concatenate([cluster, far])
+    pairs = _random_pairs(rng, n, m - 100)
+    pairs = np.concatenate([pairs, _random_pairs(rng, len(xy), 100)])
+    return xy, pairs
+
+
+def short_edges(seed=5, n=3000):
+    """Edges of length ~1e-6 in a unit square (C3-like, extreme)."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0, 1, (n, 2))
+    b = a + rng.normal(scale=1e-6, size=(n, 2))
+    c = a + rng.normal(scale=1e-6, size=(n, 2))
+    xy = np.concatenate([a, b, c])
+    pairs = [(i, n + i) for i in range(n)] + [(n + i, 2 * n + i) for i in range(n)]
+    return xy, pairs
+
+
+def hubs(seed=6, n=2000, m=4000):
+    """A few hubs holding most edges, some spokes exactly collinear."""
+    rng = np.random.default_rng(seed)
+    xy = rng.integers(0, 64, (n, 2)).astype(np.float64)
+    xy = np.unique(xy, axis=0)
+    n = len(xy)
+    hub = rng.integers(0, 5, m)
+    other = rng.integers(5, n, m)
+    return xy, np.stack([hub, other], 1)
+
+
+def coincident(seed=7, n=400, m=1500):
+    """Distinct vertex ids sharing coordinates."""
+    rng = np.random.default_rng(seed)
+    half = n // 2
+    base = rng.uniform(0, 1, (half, 2))
+    xy = np.concatenate([base, base])
+    p = _random_pairs(rng, len(xy), 2 * m)
+    p = p[(p[:, 0] % half) != (p[:, 1] % half)][:m]  # no zero-length edges
+    return xy, p
+
+
+def lattice_c5_like(seed=8, n=3000, m=6000):
+    rng = np.random.default_rng(seed)
+    xy = rng.integers(0, 2 ** 16, (n, 2)).astype(np.float64)
+    return xy, _random_pairs(rng, n, m)
+
+
+CASES = {f.__name__: f for f in (near_collinear, exact_lattice, far_offset, mixed_scales,
+                                  short_edges, hubs, coincident, lattice_c5_like)}
+
+
+def _run(dg, mode, ideal):
+    from paper_2411_09809_b200 import metrics as M
+
+    rec = M.CrossingRecords(dg)
+    got_mode = rec.set_mode(mode).mode()
+    out = rec.partial(ideal, 0, rec.units).tolist()
+    return got_mode, int(out[0]), out[1]
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_filter_modes_agree_with_oracle(gpu, name):
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import metrics as M
+
+    g = _graph(*CASES[name]())
+    dg = M.DeviceGraph.from_graph(g)
+    assert M.CrossingRecords(dg).mode() == M.CrossingRecords.MODE_FILTER
+    m2, c2, d2 = _run(dg, 2, IDEAL)
+    m1, c1, d1 = _run(dg, 1, IDEAL)
+    m0, c0, d0 = _run(dg, 0, IDEAL)
+    assert (m0, m1, m2) == (0, 1, 2)
+    assert c2 == c0 == c1
+    assert d2 == d0  # same accumulation order: bit-identical
+    assert abs(d1 - d0) <= 1e-12 * max(abs(d0), 1e-300)
+    cw, dw = S.crossing_scan(g.xy, g.edges, IDEAL)
+    assert c2 == cw
+    assert strict_close(d2, dw)
+    # count-only instantiation
+    _, c2n, _ = _run(dg, 2, None)
+    assert c2n == cw
+
+
+@pytest.mark.parametrize("name", ["near_collinear", "hubs", "exact_lattice"])
+def test_filter_unit_partials_and_shards(gpu, name):
+    from paper_2411_09809_b200 import metrics as M
+
+    g = _graph(*CASES[name]())
+    dg = M.DeviceGraph.from_graph(g)
+    rec = M.CrossingRecords(dg)
+    whole = rec.partial(IDEAL, 0, rec.units).tolist()
+    U = rec.units
+    cuts = [0, U // 3, U // 2, U]
+    parts = [rec.partial(IDEAL, a, b).tolist() for a, b in zip(cuts, cuts[1:])]
+    assert sum(int(p[0]) for p in parts) == int(whole[0])
+    assert strict_close(sum(p[1] for p in parts), whole[1])
+    shares = [rec.partial_interleaved(IDEAL, r, 3).tolist() for r in range(3)]
+    assert sum(int(p[0]) for p in shares) == int(whole[0])
+    assert strict_close(sum(p[1] for p in shares), whole[1])
+
+
+def test_set_mode_outside_fast_window_degrades(gpu):
+    from paper_2411_09809_b200 import metrics as M
+
+    rng = np.random.default_rng(9)
+    xy = rng.uniform(0, 1, (300, 2)) * 2.0 ** 600  # outside [2^-160, 2^500]
+    g = _graph(xy, _random_pairs(rng, 300, 600))
+    rec = M.CrossingRecords(M.DeviceGraph.from_graph(g))
+    assert rec.mode() == 0
+    assert rec.set_mode(2).mode() == 0
+    with pytest.raises(Exception):
+        rec.set_mode(3)
