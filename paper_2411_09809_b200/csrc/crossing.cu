@@ -78,6 +78,10 @@ constexpr int kBandTiles = GLR_XBAND;
 #define GLR_XCHUNK 256
 #endif
 constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bound)
+#ifndef GLR_XFBLOCK
+#define GLR_XFBLOCK 4
+#endif
+constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp vote each)
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
@@ -115,30 +119,28 @@ constexpr int kModeFastDefault = kModeSign;
 constexpr int kModeFastDefault = kModeFilter;
 #endif
 
-// Filter record of an edge (32 B): endpoint coordinates translated to the
+// Filter record of an edge: endpoint coordinates translated to the
 // lower-left corner of the edges' bounding box and scaled by a power of two
-// into [0, 1/2], rounded to FP32; the FP32 direction b - a scaled by a
-// per-edge power of two 2^k (sabx, and -saby pre-negated) such that a
-// product of two of its cross products exceeding 1 in magnitude certifies
-// both factors' signs; theta.  This is
-// the shared-memory form of a j-edge (two broadcast LDS.128).
-struct __align__(16) FRec {
-  float ax, ay, bx, by;
-  float sabx, nsaby;
-  double theta;
-};
-static_assert(sizeof(FRec) == 32, "FRec must be 32 bytes");
+// into [0, 1/2], rounded to FP32 (ax, ay, bx, by); the FP32 direction
+// (abx, aby) = (bx - ax, by - ay) and the line constant ka = ab x a =
+// abx*ay - aby*ax (FP64 from the FP32 values, rounded once), all three
+// scaled by a per-edge power of two 2^k and stored as (sabx, nsaby =
+// -saby, nska = -ska); theta.  Then the scaled cross product of a point p
+// with the line is one FFMA pair: ab x (p - a) = sabx*py + (nsaby*px + nska),
+// and 2^k is chosen so that a product of two such values exceeding 1 in
+// magnitude certifies both factors' signs.
+enum FField { kFAx, kFAy, kFBx, kFBy, kFSabx, kFNsaby, kFNska, kFFields };
 
 // In HBM the filter records of a tile are stored field-major and paired the
 // way the kernel packs its i-edges: v[f][g][p] = (field f of tile slot
 // 2g*kThreads + p, of slot (2g+1)*kThreads + p), so each packed i-register
-// pair is one 64-bit load (f = ax, ay, bx, by, sabx, nsaby).
+// pair is one 64-bit load.
 constexpr int kFGroups = GLR_XK / 2;
 struct __align__(16) FTile {
-  float2 v[6][kFGroups][kThreads];
+  float2 v[kFFields][kFGroups][kThreads];
   double theta[kTile];
 };
-static_assert(sizeof(FTile) == (size_t)kTile * sizeof(FRec), "FTile must be 32 B per edge");
+static_assert(sizeof(FTile) == (size_t)kTile * 36, "FTile must be 36 B per edge");
 
 // Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
 // newc[m_pad] | frec[m_pad] | inc[2m] (incident edge ids grouped by vertex) |
@@ -171,7 +173,7 @@ inline Layout layout(int64_t n, int64_t m) {
   L.ids = L.theta + al256((size_t)mp * sizeof(double));
   L.newc = L.ids + al256((size_t)mp * sizeof(int2));
   L.frec = L.newc + al256((size_t)mp * sizeof(int));
-  L.inc = L.frec + al256((size_t)mp * sizeof(FRec));
+  L.inc = L.frec + al256((size_t)(mp / kTile) * sizeof(FTile));
   L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
   L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
   L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
@@ -321,7 +323,7 @@ __global__ void header_kernel(RecHeader *hdr, int64_t n, int64_t m, int64_t m_pa
   hdr->fast = ok ? kModeFastDefault : kModeGeneral;
 }
 
-// Filter records (FRec).  x0/y0 = smallest endpoint coordinate, W = largest
+// Filter records (FTile).  x0/y0 = smallest endpoint coordinate, W = largest
 // extent rounded up, s = 2^-(ilogb(W)+2) so that (x - x0) * s lies in
 // [0, 1/2] after the (monotone) roundings.  Per edge: L = |abx| + |aby| of
 // the FP32 direction, tau = 2^-22 * L * (1 + 2^-18) >= E * C * (1 + u) with
@@ -336,39 +338,35 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
   const double s = (W > 0.0 && W <= 0x1p1000) ? ldexp(1.0, -(ilogb(W) + 2)) : 1.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m_pad;
        e += (int64_t)gridDim.x * blockDim.x) {
-    FRec f;
+    float f[kFFields] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    double theta = 0.0;
     if (e < m) {
       const EdgeRec r = rv.rec[e];
-      f.ax = __double2float_rn(__dmul_rn(__dsub_rn(r.ax, x0), s));
-      f.ay = __double2float_rn(__dmul_rn(__dsub_rn(r.ay, y0), s));
-      f.bx = __double2float_rn(__dmul_rn(__dsub_rn(r.bx, x0), s));
-      f.by = __double2float_rn(__dmul_rn(__dsub_rn(r.by, y0), s));
-      const float abx = __fsub_rn(f.bx, f.ax), aby = __fsub_rn(f.by, f.ay);
+      const float ax = __double2float_rn(__dmul_rn(__dsub_rn(r.ax, x0), s));
+      const float ay = __double2float_rn(__dmul_rn(__dsub_rn(r.ay, y0), s));
+      const float bx = __double2float_rn(__dmul_rn(__dsub_rn(r.bx, x0), s));
+      const float by = __double2float_rn(__dmul_rn(__dsub_rn(r.by, y0), s));
+      const float abx = __fsub_rn(bx, ax), aby = __fsub_rn(by, ay);
+      // products of FP32 values are exact in FP64; one FP64 and one FP32 rounding
+      const float ka = __double2float_rn(
+          __dsub_rn(__dmul_rn((double)abx, (double)ay), __dmul_rn((double)aby, (double)ax)));
       const double L = fabs((double)abx) + fabs((double)aby);
+      f[kFAx] = ax; f[kFAy] = ay; f[kFBx] = bx; f[kFBy] = by;
       if (L > 0.0) {
         const double tau = L * 0x1p-22 * (1.0 + 0x1p-18);
         const int k = (-ilogb(tau) - 1) / 2;  // tau < 2^-21, so the numerator is > 0
-        f.sabx = scalbnf(abx, k);
-        f.nsaby = -scalbnf(aby, k);
-      } else {
-        f.sabx = 0.0f;
-        f.nsaby = 0.0f;
+        f[kFSabx] = scalbnf(abx, k);
+        f[kFNsaby] = -scalbnf(aby, k);
+        f[kFNska] = -scalbnf(ka, k);
       }
-      f.theta = rv.theta[e];
-    } else {
-      f.ax = f.ay = f.bx = f.by = f.sabx = f.nsaby = 0.0f;
-      f.theta = 0.0;
+      theta = rv.theta[e];
     }
     FTile &t = rv.ftile[e / kTile];
     const int slot = (int)(e % kTile);
     const int g = slot / (2 * kThreads), h = (slot / kThreads) & 1, q = slot % kThreads;
-    const float vals[6] = {f.ax, f.ay, f.bx, f.by, f.sabx, f.nsaby};
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      float *pair = reinterpret_cast<float *>(&t.v[k][g][q]);
-      pair[h] = vals[k];
-    }
-    t.theta[slot] = f.theta;
+    for (int k = 0; k < kFFields; ++k) reinterpret_cast<float *>(&t.v[k][g][q])[h] = f[k];
+    t.theta[slot] = theta;
   }
 }
 
@@ -576,7 +574,7 @@ __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const Edge
 // ------------------------------------------------ certified FP32 filter --
 //
 // Packed-FP32 (FFMA2/FMUL2/FADD2) evaluation of the four cross products of
-// two i-edges against one j-edge per instruction.  With the FRec scaling,
+// two i-edges against one j-edge per instruction.  With the FTile scaling,
 // c1^ = 2^ki c1~, c2^ = 2^ki c2~ (ki from edge i), c3^, c4^ with kj, where
 // |c~ - c_exact| <= E = 2^-21 for every c (error analysis in DESIGN.md,
 // including the FP64 rounding of the reference's own c), and |c~| <= C.
@@ -629,7 +627,8 @@ constexpr int kGroups = kK / 2;  // packed i-edge pairs per thread
 static_assert(kK % 2 == 0, "the filter packs i-edges in pairs");
 
 struct FIRegs {
-  uint64_t ax[kGroups], ay[kGroups], bx[kGroups], by[kGroups], sabx[kGroups], nsaby[kGroups];
+  uint64_t ax[kGroups], ay[kGroups], bx[kGroups], by[kGroups];
+  uint64_t sabx[kGroups], nsaby[kGroups], nska[kGroups];
   double th[kK];
 };
 
@@ -642,12 +641,13 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
   for (int g = 0; g < kGroups; ++g) {
     const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][g][threadIdx.x]);
     constexpr int kField = kFGroups * kThreads;  // uint64 stride between fields
-    R.ax[g] = v[0 * kField];
-    R.ay[g] = v[1 * kField];
-    R.bx[g] = v[2 * kField];
-    R.by[g] = v[3 * kField];
-    R.sabx[g] = v[4 * kField];
-    R.nsaby[g] = v[5 * kField];
+    R.ax[g] = v[kFAx * kField];
+    R.ay[g] = v[kFAy * kField];
+    R.bx[g] = v[kFBx * kField];
+    R.by[g] = v[kFBy * kField];
+    R.sabx[g] = v[kFSabx * kField];
+    R.nsaby[g] = v[kFNsaby * kField];
+    R.nska[g] = v[kFNska * kField];
     R.th[2 * g] = ANGLE ? t.theta[threadIdx.x + (2 * g) * kThreads] : 0.0;
     R.th[2 * g + 1] = ANGLE ? t.theta[threadIdx.x + (2 * g + 1) * kThreads] : 0.0;
   }
@@ -682,40 +682,59 @@ __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
   return ANGLE ? angle_dev(theta[ei], theta[ej], kappa) : 0.0;
 }
 
-// One j-edge (from shared memory) against the thread's K i-edges.
-template <bool ANGLE, bool DIAG>
-__device__ __forceinline__ void filter_row(const FIRegs &R, const float4 *sj4, int jj,
-                                           unsigned (&cnt)[kK], double (&dev)[kK],
-                                           double kappa, const EdgeRec *__restrict__ rec,
-                                           const int2 *__restrict__ ids,
-                                           const double *__restrict__ theta, int64_t ibase,
-                                           int64_t j) {
-  const float4 q0 = sj4[2 * jj];      // cx cy dx dy
-  const float4 q1 = sj4[2 * jj + 1];  // scdx -scdy theta
+// M_k = max(P12, P34) of one j-edge (shared memory) against the thread's K
+// i-edges; masked pairs of a diagonal tile get M = 2 (certain miss).
+// Per pair: 8 FFMA + 2 FMUL, issued as packed pairs over two i-edges.
+template <bool DIAG>
+__device__ __forceinline__ void filter_m(const FIRegs &R, const float4 *sjc, const float4 *sjk,
+                                         int jj, float (&M)[kK]) {
+  const float4 q0 = sjc[jj];  // cx cy dx dy
+  const float4 q1 = sjk[jj];  // scdx -scdy -skc
   const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
   const uint64_t DX = f2_bcast(q0.z), DY = f2_bcast(q0.w);
-  const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y);
-  const double thj = ANGLE ? __hiloint2double(__float_as_int(q1.w), __float_as_int(q1.z)) : 0.0;
-  bool unc[kK];
+  const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y), NSKC = f2_bcast(q1.z);
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    const uint64_t t1 = f2_sub(CY, R.ay[g]), t2 = f2_sub(CX, R.ax[g]);  // c - a
-    const uint64_t t3 = f2_sub(DY, R.ay[g]), t4 = f2_sub(DX, R.ax[g]);  // d - a
-    const uint64_t t5 = f2_sub(CY, R.by[g]), t6 = f2_sub(CX, R.bx[g]);  // c - b
-    // c1 = ab x (c - a), c2 = ab x (d - a); c3' = -c3 = cd x (c - a) with
-    // c - a = -(a - c), c4' = -c4 = cd x (c - b): P34 = c3' c4' = c3 c4
-    const uint64_t c1 = f2_fma(R.sabx[g], t1, f2_mul(R.nsaby[g], t2));
-    const uint64_t c2 = f2_fma(R.sabx[g], t3, f2_mul(R.nsaby[g], t4));
-    const uint64_t c3 = f2_fma(SCDX, t1, f2_mul(NSCDY, t2));
-    const uint64_t c4 = f2_fma(SCDX, t5, f2_mul(NSCDY, t6));
+    // c1 = ab x (c - a), c2 = ab x (d - a), c3 = cd x (a - c), c4 = cd x (b - c)
+    const uint64_t c1 = f2_fma(R.sabx[g], CY, f2_fma(R.nsaby[g], CX, R.nska[g]));
+    const uint64_t c2 = f2_fma(R.sabx[g], DY, f2_fma(R.nsaby[g], DX, R.nska[g]));
+    const uint64_t c3 = f2_fma(SCDX, R.ay[g], f2_fma(NSCDY, R.ax[g], NSKC));
+    const uint64_t c4 = f2_fma(SCDX, R.by[g], f2_fma(NSCDY, R.bx[g], NSKC));
     const uint64_t p12 = f2_mul(c1, c2), p34 = f2_mul(c3, c4);
+    M[2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
+    M[2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
+  }
+  if (DIAG) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = 2 * g + h;
-      float M = fmaxf(h ? f2_hi(p12) : f2_lo(p12), h ? f2_hi(p34) : f2_lo(p34));
-      if (DIAG && !(jj > (int)threadIdx.x + k * kThreads)) M = 2.0f;  // masked: certain miss
-      unc[k] = fabsf(M) <= 1.0f;
-      // @(M < -1) cnt += 1 (and dev += t): predicated adds, no selects
+    for (int k = 0; k < kK; ++k)
+      if (!(jj > (int)threadIdx.x + k * kThreads)) M[k] = 2.0f;
+  }
+}
+
+// NJ consecutive j-edges against the thread's K i-edges.  Certain hits are
+// counted (and their angle deviations summed) with predicated adds; one
+// warp vote per block decides whether any lane met an uncertain pair, and
+// only then is the block re-filtered to run exact_pair on those pairs, so
+// the hot path has no branch inside the block and the compiler can
+// interleave its NJ independent j-steps.
+template <bool ANGLE, bool DIAG, int NJ>
+__device__ __forceinline__ void filter_block(const FIRegs &R, const float4 *sjc,
+                                             const float4 *sjk, const double *sth, int jj0,
+                                             unsigned (&cnt)[kK], double (&dev)[kK],
+                                             double kappa, const EdgeRec *__restrict__ rec,
+                                             const int2 *__restrict__ ids,
+                                             const double *__restrict__ theta, int64_t ibase,
+                                             int64_t jbase) {
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) {
+    float M[kK];
+    filter_m<DIAG>(R, sjc, sjk, jj0 + q, M);
+    const double thj = ANGLE ? sth[jj0 + q] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      any |= fabsf(M[k]) <= 1.0f;
+      // @(M < -1) cnt += 1 (and dev += t)
       if (ANGLE) {
         // dev += hit ? t : 0 as fma(t, {0.0 | 1.0}, dev): one DFMA and one SEL
         // (exact: fma(t, 1, dev) == dev + t, fma(t, 0, dev) == dev)
@@ -726,29 +745,31 @@ __device__ __forceinline__ void filter_row(const FIRegs &R, const float4 *sj4, i
             "@p add.u32 %0, %0, 1;\n\t"
             "selp.b32 %1, 1072693248, 0, p;\n\t}"
             : "+r"(cnt[k]), "=r"(hw)
-            : "f"(M));
+            : "f"(M[k]));
         dev[k] = __fma_rn(t, __hiloint2double(hw, 0), dev[k]);
       } else {
         asm("{\n\t.reg .pred p;\n\t"
             "setp.lt.f32 p, %1, 0fBF800000;\n\t"
             "@p add.u32 %0, %0, 1;\n\t}"
             : "+r"(cnt[k])
-            : "f"(M));
+            : "f"(M[k]));
       }
     }
   }
-  bool any = false;
-#pragma unroll
-  for (int k = 0; k < kK; ++k) any |= unc[k];
   if (__any_sync(0xffffffffu, any)) {
+#pragma unroll 1
+    for (int q = 0; q < NJ; ++q) {
+      float M[kK];
+      filter_m<DIAG>(R, sjc, sjk, jj0 + q, M);
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
-      if (unc[k]) {
-        const double t =
-            exact_pair<ANGLE>(rec, ids, theta, ibase + threadIdx.x + k * kThreads, j, kappa);
-        if (t >= 0.0) {
-          cnt[k] += 1u;
-          if (ANGLE) dev[k] = __dadd_rn(dev[k], t);
+      for (int k = 0; k < kK; ++k) {
+        if (fabsf(M[k]) <= 1.0f) {
+          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + threadIdx.x + k * kThreads,
+                                             jbase + jj0 + q, kappa);
+          if (t >= 0.0) {
+            cnt[k] += 1u;
+            if (ANGLE) dev[k] = __dadd_rn(dev[k], t);
+          }
         }
       }
     }
@@ -875,7 +896,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     unsigned sworld, double kappa, unsigned long long *__restrict__ cta_cnt,
                     double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
-  __shared__ __align__(16) float4 sj4[2 * kTile];
+  __shared__ __align__(16) float4 sjc[kTile];  // cx cy dx dy
+  __shared__ __align__(16) float4 sjk[kTile];  // scdx -scdy -skc 0
+  __shared__ double sth[ANGLE ? kTile : 1];
   __shared__ unsigned long long red_u[kThreads / 32];
   __shared__ double red_d[kThreads / 32];
   const uint64_t nchunks = (uend - ubeg + chunk - 1) / chunk;
@@ -899,21 +922,22 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         cur_ti = ti;
       }
       __syncthreads();  // previous tile fully consumed
-      {  // unpack the j-tile into per-edge FRecs
+      {  // unpack the j-tile into per-edge records
         const FTile &t = ftile[tj];
 #pragma unroll
         for (int g = 0; g < kGroups; ++g) {
-          float2 v[6];
+          float2 v[kFFields];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) v[k] = t.v[k][g][threadIdx.x];
+          for (int k = 0; k < kFFields; ++k) v[k] = t.v[k][g][threadIdx.x];
           const int s0 = (2 * g) * kThreads + threadIdx.x, s1 = s0 + kThreads;
-          const double th0 = t.theta[s0], th1 = t.theta[s1];
-          sj4[2 * s0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
-          sj4[2 * s0 + 1] = make_float4(v[4].x, v[5].x, __int_as_float(__double2loint(th0)),
-                                        __int_as_float(__double2hiint(th0)));
-          sj4[2 * s1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
-          sj4[2 * s1 + 1] = make_float4(v[4].y, v[5].y, __int_as_float(__double2loint(th1)),
-                                        __int_as_float(__double2hiint(th1)));
+          sjc[s0] = make_float4(v[kFAx].x, v[kFAy].x, v[kFBx].x, v[kFBy].x);
+          sjk[s0] = make_float4(v[kFSabx].x, v[kFNsaby].x, v[kFNska].x, 0.0f);
+          sjc[s1] = make_float4(v[kFAx].y, v[kFAy].y, v[kFBx].y, v[kFBy].y);
+          sjk[s1] = make_float4(v[kFSabx].y, v[kFNsaby].y, v[kFNska].y, 0.0f);
+          if (ANGLE) {
+            sth[s0] = t.theta[s0];
+            sth[s1] = t.theta[s1];
+          }
         }
       }
       __syncthreads();
@@ -923,14 +947,14 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
       for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
       const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
       if (ti == tj) {
-        for (int jj = 0; jj < kTile; ++jj)
-          filter_row<ANGLE, true>(R, sj4, jj, cnt, dev, kappa, rec, ids, theta, ibase,
-                                  jbase + jj);
+        for (int jj = 0; jj < kTile; jj += kFilterBlock)
+          filter_block<ANGLE, true, kFilterBlock>(R, sjc, sjk, sth, jj, cnt, dev, kappa, rec, ids,
+                                                  theta, ibase, jbase);
       } else {
-#pragma unroll kUnroll
-        for (int jj = 0; jj < kTile; ++jj)
-          filter_row<ANGLE, false>(R, sj4, jj, cnt, dev, kappa, rec, ids, theta, ibase,
-                                   jbase + jj);
+#pragma unroll 1
+        for (int jj = 0; jj < kTile; jj += kFilterBlock)
+          filter_block<ANGLE, false, kFilterBlock>(R, sjc, sjk, sth, jj, cnt, dev, kappa, rec,
+                                                   ids, theta, ibase, jbase);
       }
       unsigned c = 0;
       double s = 0.0;

@@ -5,9 +5,10 @@ inputs built to defeat a filter: near-collinear triples, exact collinear
 lattice points, coordinates far from the origin, mixed scales, very short
 edges, hubs (shared vertices) and coincident vertices with distinct ids.
 
-Modes 0 and 2 accumulate every pair in the same order, so their (count,
-dev_sum) must agree bit for bit; mode 1 subtracts its adjacency correction
-afterwards, so its dev_sum is compared at 1e-12.
+Counts must agree exactly; dev_sum differs between modes only in the order
+the per-thread sums absorb the terms (mode 2 adds a block's uncertain pairs
+after its certain ones, mode 1 subtracts its adjacency correction at the
+end), so it is compared at 1e-12.
 """
 
 from __future__ import annotations
@@ -150,7 +151,8 @@ def test_filter_modes_agree_with_oracle(gpu, name):
     m0, c0, d0 = _run(dg, 0, IDEAL)
     assert (m0, m1, m2) == (0, 1, 2)
     assert c2 == c0 == c1
-    assert d2 == d0  # same accumulation order: bit-identical
+    # modes differ only in the order uncertain pairs are accumulated
+    assert abs(d2 - d0) <= 1e-12 * max(abs(d0), 1e-300)
     assert abs(d1 - d0) <= 1e-12 * max(abs(d0), 1e-300)
     cw, dw = S.crossing_scan(g.xy, g.edges, IDEAL)
     assert c2 == cw
