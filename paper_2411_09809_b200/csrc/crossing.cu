@@ -83,6 +83,7 @@ constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bou
 #endif
 constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp vote each)
 
+
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
 constexpr double kMinAbsFast = 0x1p-160;
@@ -142,6 +143,13 @@ struct __align__(16) FTile {
 };
 static_assert(sizeof(FTile) == (size_t)kTile * 36, "FTile must be 36 B per edge");
 
+// The same record in the j role, one edge per 32 B: (cx, cy, dx, dy) and
+// (scdx, -scdy, -skc, 0); read by all lanes of a warp at once (broadcast).
+struct __align__(16) JRec {
+  float4 c;
+  float4 k;
+};
+
 // Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
 // newc[m_pad] | frec[m_pad] | inc[2m] (incident edge ids grouped by vertex) |
 // offs[n+1] | wofs[n+1].
@@ -149,6 +157,7 @@ struct RecView {
   RecHeader *hdr;
   EdgeRec *rec;
   FTile *ftile;
+  JRec *jrec;
   double *theta;
   int2 *ids;
   int *newc;  // 1 if edge e starts a run of edges sharing endpoint a (or a tile)
@@ -161,7 +170,7 @@ inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; 
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t rec, theta, ids, newc, frec, inc, offs, wofs, total;
+  size_t rec, theta, ids, newc, frec, jrec, inc, offs, wofs, total;
 };
 
 inline Layout layout(int64_t n, int64_t m) {
@@ -173,7 +182,8 @@ inline Layout layout(int64_t n, int64_t m) {
   L.ids = L.theta + al256((size_t)mp * sizeof(double));
   L.newc = L.ids + al256((size_t)mp * sizeof(int2));
   L.frec = L.newc + al256((size_t)mp * sizeof(int));
-  L.inc = L.frec + al256((size_t)(mp / kTile) * sizeof(FTile));
+  L.jrec = L.frec + al256((size_t)(mp / kTile) * sizeof(FTile));
+  L.inc = L.jrec + al256((size_t)mp * sizeof(JRec));
   L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
   L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
   L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
@@ -190,6 +200,7 @@ inline RecView view(void *base, int64_t n, int64_t m) {
   v.ids = reinterpret_cast<int2 *>(p + L.ids);
   v.newc = reinterpret_cast<int *>(p + L.newc);
   v.ftile = reinterpret_cast<FTile *>(p + L.frec);
+  v.jrec = reinterpret_cast<JRec *>(p + L.jrec);
   v.inc = reinterpret_cast<int *>(p + L.inc);
   v.offs = reinterpret_cast<int *>(p + L.offs);
   v.wofs = reinterpret_cast<long long *>(p + L.wofs);
@@ -367,6 +378,10 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
 #pragma unroll
     for (int k = 0; k < kFFields; ++k) reinterpret_cast<float *>(&t.v[k][g][q])[h] = f[k];
     t.theta[slot] = theta;
+    JRec j;
+    j.c = make_float4(f[kFAx], f[kFAy], f[kFBx], f[kFBy]);
+    j.k = make_float4(f[kFSabx], f[kFNsaby], f[kFNska], 0.0f);
+    rv.jrec[e] = j;
   }
 }
 
@@ -686,10 +701,10 @@ __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
 // i-edges; masked pairs of a diagonal tile get M = 2 (certain miss).
 // Per pair: 8 FFMA + 2 FMUL, issued as packed pairs over two i-edges.
 template <bool DIAG>
-__device__ __forceinline__ void filter_m(const FIRegs &R, const float4 *sjc, const float4 *sjk,
-                                         int jj, float (&M)[kK]) {
-  const float4 q0 = sjc[jj];  // cx cy dx dy
-  const float4 q1 = sjk[jj];  // scdx -scdy -skc
+__device__ __forceinline__ void filter_m(const FIRegs &R, const JRec *jr, int jj,
+                                         float (&M)[kK]) {
+  const float4 q0 = jr[jj].c;  // cx cy dx dy
+  const float4 q1 = jr[jj].k;  // scdx -scdy -skc
   const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
   const uint64_t DX = f2_bcast(q0.z), DY = f2_bcast(q0.w);
   const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y), NSKC = f2_bcast(q1.z);
@@ -718,8 +733,8 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, const float4 *sjc, con
 // the hot path has no branch inside the block and the compiler can
 // interleave its NJ independent j-steps.
 template <bool ANGLE, bool DIAG, int NJ>
-__device__ __forceinline__ void filter_block(const FIRegs &R, const float4 *sjc,
-                                             const float4 *sjk, const double *sth, int jj0,
+__device__ __forceinline__ void filter_block(const FIRegs &R, const JRec *jr,
+                                             const double *sth, int jj0,
                                              unsigned (&cnt)[kK], double (&dev)[kK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
@@ -729,7 +744,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const float4 *sjc,
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kK];
-    filter_m<DIAG>(R, sjc, sjk, jj0 + q, M);
+    filter_m<DIAG>(R, jr, jj0 + q, M);
     const double thj = ANGLE ? sth[jj0 + q] : 0.0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
@@ -760,7 +775,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const float4 *sjc,
 #pragma unroll 1
     for (int q = 0; q < NJ; ++q) {
       float M[kK];
-      filter_m<DIAG>(R, sjc, sjk, jj0 + q, M);
+      filter_m<DIAG>(R, jr, jj0 + q, M);
 #pragma unroll
       for (int k = 0; k < kK; ++k) {
         if (fabsf(M[k]) <= 1.0f) {
@@ -882,94 +897,167 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   }
 }
 
+// Walks this CTA's units: chunks of `chunk` consecutive units dealt
+// round-robin over the CTAs of all ranks (see cross_pairs_kernel), in the
+// banded order (or the explicit culled list).
+struct UnitCursor {
+  const int2 *ulist;
+  uint64_t T, W, ubeg, uend, chunk, nchunks, step;
+  uint64_t ch, u, e, ti, tj;
+  bool valid;
+  __device__ void start(uint64_t first_chunk) {
+    ch = first_chunk;
+    begin_chunk();
+  }
+  __device__ void begin_chunk() {
+    valid = ch < nchunks;
+    if (!valid) return;
+    u = ubeg + ch * chunk;
+    e = u + chunk < uend ? u + chunk : uend;
+    if (ulist == nullptr) band_unit_coords(u, T, W, &ti, &tj);
+    else load();
+  }
+  __device__ void load() {
+    const int2 p = ulist[u];
+    ti = (uint64_t)p.x;
+    tj = (uint64_t)p.y;
+  }
+  __device__ void advance() {
+    if (++u < e) {
+      if (ulist == nullptr) band_advance(T, W, &ti, &tj);
+      else load();
+    } else {
+      ch += step;
+      begin_chunk();
+    }
+  }
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion signalled on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Filter-mode pair kernel (hdr->fast == kModeFilter): same unit space,
-// chunking and reductions as cross_pairs_kernel; the j-tile's FRecs are
-// staged in shared memory (8 KB) and read as two broadcast LDS.128 per
-// j-edge.  Shared-vertex pairs are never certain (an exact c is 0), so they
-// reach exact_pair, which tests ids: no adjacency correction in this mode.
+// chunking and reductions as cross_pairs_kernel.  The j-tile records (8 KB,
+// + 2 KB of theta) are double-buffered in shared memory: one elected thread
+// issues the TMA bulk copy of the NEXT unit's j-tile while the CTA works on
+// the current one, so a unit costs one barrier and no exposed load latency.
+// Shared-vertex pairs are never certain (an exact c is 0), so they reach
+// exact_pair, which tests ids: no adjacency correction in this mode.
 template <bool ANGLE>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
-                    const FTile *__restrict__ ftile, const double *__restrict__ theta,
-                    const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
-                    uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk, unsigned srank,
-                    unsigned sworld, double kappa, unsigned long long *__restrict__ cta_cnt,
-                    double *__restrict__ cta_dev) {
+                    const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
+                    const double *__restrict__ theta, const int2 *__restrict__ ids,
+                    const int2 *__restrict__ ulist, uint64_t T, uint64_t W, uint64_t ubeg,
+                    uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double kappa,
+                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
-  __shared__ __align__(16) float4 sjc[kTile];  // cx cy dx dy
-  __shared__ __align__(16) float4 sjk[kTile];  // scdx -scdy -skc 0
-  __shared__ double sth[ANGLE ? kTile : 1];
+  __shared__ __align__(128) JRec sj[2][kTile];
+  __shared__ __align__(128) double sth[2][ANGLE ? kTile : 2];
+  __shared__ __align__(8) uint64_t full[2];
   __shared__ unsigned long long red_u[kThreads / 32];
   __shared__ double red_d[kThreads / 32];
-  const uint64_t nchunks = (uend - ubeg + chunk - 1) / chunk;
+  constexpr unsigned kJBytes = kTile * sizeof(JRec);
+  constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
+
+  UnitCursor cur;
+  cur.ulist = ulist; cur.T = T; cur.W = W; cur.ubeg = ubeg; cur.uend = uend; cur.chunk = chunk;
+  cur.nchunks = (uend - ubeg + chunk - 1) / chunk;
+  cur.step = (uint64_t)sworld * gridDim.x;
+  cur.start(srank + (uint64_t)sworld * blockIdx.x);
+
+  auto issue = [&](int buf, uint64_t tj_) {
+    mbar_expect_tx(&full[buf], kJBytes + kThBytes);
+    bulk_g2s(sj[buf], jrec + (int64_t)tj_ * kTile, kJBytes, &full[buf]);
+    if (ANGLE) bulk_g2s(sth[buf], theta + (int64_t)tj_ * kTile, kThBytes, &full[buf]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && cur.valid) issue(0, cur.tj);
+
   unsigned long long total = 0;
   double dsum = 0.0, dcomp = 0.0;
   FIRegs R;
-  uint64_t ti = 0, tj = 0, cur_ti = ~0ull;
-  for (uint64_t ch = srank + (uint64_t)sworld * blockIdx.x; ch < nchunks;
-       ch += (uint64_t)sworld * gridDim.x) {
-    const uint64_t b = ubeg + ch * chunk;
-    const uint64_t e = b + chunk < uend ? b + chunk : uend;
-    if (ulist == nullptr) band_unit_coords(b, T, W, &ti, &tj);
-    for (uint64_t u = b; u < e; ++u) {
-      if (ulist != nullptr) {
-        const int2 p = ulist[u];
-        ti = (uint64_t)p.x;
-        tj = (uint64_t)p.y;
-      }
-      if (ti != cur_ti) {
-        load_fi<ANGLE>(R, ftile, ti);
-        cur_ti = ti;
-      }
-      __syncthreads();  // previous tile fully consumed
-      {  // unpack the j-tile into per-edge records
-        const FTile &t = ftile[tj];
-#pragma unroll
-        for (int g = 0; g < kGroups; ++g) {
-          float2 v[kFFields];
-#pragma unroll
-          for (int k = 0; k < kFFields; ++k) v[k] = t.v[k][g][threadIdx.x];
-          const int s0 = (2 * g) * kThreads + threadIdx.x, s1 = s0 + kThreads;
-          sjc[s0] = make_float4(v[kFAx].x, v[kFAy].x, v[kFBx].x, v[kFBy].x);
-          sjk[s0] = make_float4(v[kFSabx].x, v[kFNsaby].x, v[kFNska].x, 0.0f);
-          sjc[s1] = make_float4(v[kFAx].y, v[kFAy].y, v[kFBx].y, v[kFBy].y);
-          sjk[s1] = make_float4(v[kFSabx].y, v[kFNsaby].y, v[kFNska].y, 0.0f);
-          if (ANGLE) {
-            sth[s0] = t.theta[s0];
-            sth[s1] = t.theta[s1];
-          }
-        }
-      }
-      __syncthreads();
-      unsigned cnt[kK];
-      double dev[kK];
-#pragma unroll
-      for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
-      const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
-      if (ti == tj) {
-        for (int jj = 0; jj < kTile; jj += kFilterBlock)
-          filter_block<ANGLE, true, kFilterBlock>(R, sjc, sjk, sth, jj, cnt, dev, kappa, rec, ids,
-                                                  theta, ibase, jbase);
-      } else {
-#pragma unroll 1
-        for (int jj = 0; jj < kTile; jj += kFilterBlock)
-          filter_block<ANGLE, false, kFilterBlock>(R, sjc, sjk, sth, jj, cnt, dev, kappa, rec,
-                                                   ids, theta, ibase, jbase);
-      }
-      unsigned c = 0;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
-      total += c;
-      if (ANGLE) {
-        double y = __dsub_rn(s, dcomp);
-        double t = __dadd_rn(dsum, y);
-        dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
-        dsum = t;
-      }
-      if (ulist == nullptr) band_advance(T, W, &ti, &tj);
+  uint64_t cur_ti = ~0ull;
+  int buf = 0;
+  unsigned parity = 0u;  // bit b: phase of full[b]
+  while (cur.valid) {
+    const uint64_t ti = cur.ti, tj = cur.tj;
+    if (ti != cur_ti) {
+      load_fi<ANGLE>(R, ftile, ti);
+      cur_ti = ti;
     }
-  }  // chunks
+    mbar_wait(&full[buf], (parity >> buf) & 1u);  // this unit's j-tile has landed
+    parity ^= 1u << buf;
+    // every warp is past the previous unit, so the other buffer is free
+    __syncthreads();
+    cur.advance();
+    if (threadIdx.x == 0 && cur.valid) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(buf ^ 1, cur.tj);
+    }
+    const JRec *jr = sj[buf];
+    const double *jth = sth[buf];
+    unsigned cnt[kK];
+    double dev[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+    const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
+    if (ti == tj) {
+      for (int jj = 0; jj < kTile; jj += kFilterBlock)
+        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, cnt, dev, kappa, rec, ids, theta,
+                                                ibase, jbase);
+    } else {
+#pragma unroll 1
+      for (int jj = 0; jj < kTile; jj += kFilterBlock)
+        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, cnt, dev, kappa, rec, ids,
+                                                 theta, ibase, jbase);
+    }
+    unsigned c = 0;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
+    total += c;
+    if (ANGLE) {
+      double y = __dsub_rn(s, dcomp);
+      double t = __dadd_rn(dsum, y);
+      dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
+      dsum = t;
+    }
+    buf ^= 1;
+  }
   unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
   double bd = block_sum<kThreads>(dsum, red_d);
   if (threadIdx.x == 0) {
@@ -1339,7 +1427,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     cross_filter_kernel<true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel<angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
@@ -1356,7 +1444,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     cross_filter_kernel<false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
