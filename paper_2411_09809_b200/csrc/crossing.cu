@@ -82,6 +82,16 @@ constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bou
 #define GLR_XFBLOCK 4
 #endif
 constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp vote each)
+// CTAs per SM of the filter kernel (5 -> <= 102 registers, 6 -> <= 85):
+// tools/variant_bench.py on a C5-shaped graph, profiles/r01_variants_filter.txt
+#ifndef GLR_XFMINB_A
+#define GLR_XFMINB_A 5
+#endif
+#ifndef GLR_XFMINB_C
+#define GLR_XFMINB_C 6
+#endif
+constexpr int kFilterMinBlocksAngle = GLR_XFMINB_A;
+constexpr int kFilterMinBlocksCount = GLR_XFMINB_C;
 
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
@@ -972,7 +982,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 // Shared-vertex pairs are never certain (an exact c is 0), so they reach
 // exact_pair, which tests ids: no adjacency correction in this mode.
 template <bool ANGLE>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+__global__ void __launch_bounds__(kThreads,
+                                  ANGLE ? kFilterMinBlocksAngle : kFilterMinBlocksCount)
 cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                     const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
                     const double *__restrict__ theta, const int2 *__restrict__ ids,
@@ -1249,8 +1260,8 @@ tile_weight_kernel(const int *__restrict__ newc, double beta, double *__restrict
   }
 }
 
-int grid_for(uint64_t units) {
-  uint64_t g = (uint64_t)sm_count() * kMinBlocks;
+int grid_for(uint64_t units, int per_sm = kMinBlocks) {
+  uint64_t g = (uint64_t)sm_count() * per_sm;
   if (units < g) g = units;
   return (int)(g < 1 ? 1 : g);
 }
@@ -1400,13 +1411,19 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   RecView rv = view(const_cast<void *>(d_records), n, m);
   const uint64_t span = uend - ubeg;
   const int grid = grid_for((span + sworld - 1) / sworld);
+  const int fgrid = grid_for((span + sworld - 1) / sworld,
+                             with_angle ? kFilterMinBlocksAngle : kFilterMinBlocksCount);
+  const int cgrid = grid > fgrid ? grid : fgrid;  // CTA partial slots
   const int agrid = sm_count() * 8;
-  Scratch scr((size_t)(grid + agrid) * (sizeof(unsigned long long) + sizeof(double)), st);
+  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)), st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
-  unsigned long long *ac = cc + grid;
+  unsigned long long *ac = cc + cgrid;
   double *cd = reinterpret_cast<double *>(ac + agrid);
-  double *ad = cd + grid;
+  double *ad = cd + cgrid;
+  // only the kernel of the records' mode writes its CTA slots
+  GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)cgrid * sizeof(unsigned long long), st));
+  GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)cgrid * sizeof(double), st));
   const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
   // chunk: >= 8 chunks per CTA of every rank, <= kMaxChunk units per chunk
   // (each chunk reloads its i-tile, so longer chunks mean less L2/DRAM
@@ -1426,7 +1443,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
-    cross_filter_kernel<true><<<grid, kThreads, 0, st>>>(
+    cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel<angle>");
@@ -1443,7 +1460,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
-    cross_filter_kernel<false><<<grid, kThreads, 0, st>>>(
+    cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel");
@@ -1452,7 +1469,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
                                                   ac, ad);
     GLR_LAUNCHED("adj_kernel");
   }
-  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, grid, ac, ad, agrid, d_out);
+  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, cgrid, ac, ad, agrid, d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
   return GLR_OK;
 }
