@@ -91,6 +91,10 @@ constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp
 #define GLR_XFMINB_C 6
 #endif
 constexpr int kFilterMinBlocksAngle = GLR_XFMINB_A;
+#ifndef GLR_XFSTAGES
+#define GLR_XFSTAGES 4
+#endif
+constexpr int kStages = GLR_XFSTAGES;  // j-tile ring depth of the filter kernel
 constexpr int kFilterMinBlocksCount = GLR_XFMINB_C;
 
 
@@ -976,9 +980,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 
 // Filter-mode pair kernel (hdr->fast == kModeFilter): same unit space,
 // chunking and reductions as cross_pairs_kernel.  The j-tile records (8 KB,
-// + 2 KB of theta) are double-buffered in shared memory: one elected thread
-// issues the TMA bulk copy of the NEXT unit's j-tile while the CTA works on
-// the current one, so a unit costs one barrier and no exposed load latency.
+// + 2 KB of theta) of the CTA's next kStages units sit in a ring of shared
+// memory stages filled by TMA bulk copies.  Warps do not synchronise with
+// each other: each waits only for its unit's stage to land (mbarrier), and
+// the LAST warp to finish with a stage refills it with the unit kStages
+// ahead, so warps may drift up to kStages - 1 units apart (a CTA barrier per
+// unit cost ~19% of the time: warps that meet uncertain pairs run longer).
 // Shared-vertex pairs are never certain (an exact c is 0), so they reach
 // exact_pair, which tests ids: no adjacency correction in this mode.
 template <bool ANGLE>
@@ -991,56 +998,58 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double kappa,
                     unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
-  __shared__ __align__(128) JRec sj[2][kTile];
-  __shared__ __align__(128) double sth[2][ANGLE ? kTile : 2];
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ unsigned long long red_u[kThreads / 32];
-  __shared__ double red_d[kThreads / 32];
+  constexpr int kWarps = kThreads / 32;
+  __shared__ __align__(128) JRec sj[kStages][kTile];
+  __shared__ __align__(128) double sth[kStages][ANGLE ? kTile : 2];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ unsigned done[kStages];  // warps finished with the stage, cumulative
+  __shared__ unsigned long long red_u[kWarps];
+  __shared__ double red_d[kWarps];
   constexpr unsigned kJBytes = kTile * sizeof(JRec);
   constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
+  const unsigned lane = threadIdx.x & 31;
 
   UnitCursor cur;
   cur.ulist = ulist; cur.T = T; cur.W = W; cur.ubeg = ubeg; cur.uend = uend; cur.chunk = chunk;
   cur.nchunks = (uend - ubeg + chunk - 1) / chunk;
   cur.step = (uint64_t)sworld * gridDim.x;
   cur.start(srank + (uint64_t)sworld * blockIdx.x);
+  UnitCursor ahead = cur;  // the unit kStages after cur (refill target)
 
-  auto issue = [&](int buf, uint64_t tj_) {
-    mbar_expect_tx(&full[buf], kJBytes + kThBytes);
-    bulk_g2s(sj[buf], jrec + (int64_t)tj_ * kTile, kJBytes, &full[buf]);
-    if (ANGLE) bulk_g2s(sth[buf], theta + (int64_t)tj_ * kTile, kThBytes, &full[buf]);
+  auto issue = [&](int st, uint64_t tj_) {
+    mbar_expect_tx(&full[st], kJBytes + kThBytes);
+    bulk_g2s(sj[st], jrec + (int64_t)tj_ * kTile, kJBytes, &full[st]);
+    if (ANGLE) bulk_g2s(sth[st], theta + (int64_t)tj_ * kTile, kThBytes, &full[st]);
   };
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      done[st] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0 && cur.valid) issue(0, cur.tj);
+  for (int st = 0; st < kStages; ++st) {
+    if (threadIdx.x == 0 && ahead.valid) issue(st, ahead.tj);
+    ahead.advance();
+  }
 
   unsigned long long total = 0;
   double dsum = 0.0, dcomp = 0.0;
   FIRegs R;
   uint64_t cur_ti = ~0ull;
-  int buf = 0;
-  unsigned parity = 0u;  // bit b: phase of full[b]
+  int stage = 0;
+  unsigned parity = 0u;  // bit st: phase of full[st] this warp waits for
   while (cur.valid) {
     const uint64_t ti = cur.ti, tj = cur.tj;
     if (ti != cur_ti) {
       load_fi<ANGLE>(R, ftile, ti);
       cur_ti = ti;
     }
-    mbar_wait(&full[buf], (parity >> buf) & 1u);  // this unit's j-tile has landed
-    parity ^= 1u << buf;
-    // every warp is past the previous unit, so the other buffer is free
-    __syncthreads();
-    cur.advance();
-    if (threadIdx.x == 0 && cur.valid) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(buf ^ 1, cur.tj);
-    }
-    const JRec *jr = sj[buf];
-    const double *jth = sth[buf];
+    mbar_wait(&full[stage], (parity >> stage) & 1u);  // this unit's j-tile has landed
+    parity ^= 1u << stage;
+    const JRec *jr = sj[stage];
+    const double *jth = sth[stage];
     unsigned cnt[kK];
     double dev[kK];
 #pragma unroll
@@ -1056,6 +1065,20 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, cnt, dev, kappa, rec, ids,
                                                  theta, ibase, jbase);
     }
+    // release the stage; the last of the CTA's warps refills it
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const unsigned old = atomicAdd(&done[stage], 1u);
+      if ((old + 1) % kWarps == 0 && ahead.valid) {
+        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(stage, ahead.tj);
+      }
+    }
+    ahead.advance();
+    cur.advance();
+    stage = stage + 1 == kStages ? 0 : stage + 1;
     unsigned c = 0;
     double s = 0.0;
 #pragma unroll
@@ -1067,7 +1090,6 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
       dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
       dsum = t;
     }
-    buf ^= 1;
   }
   unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
   double bd = block_sum<kThreads>(dsum, red_d);
