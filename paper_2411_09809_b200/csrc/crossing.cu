@@ -350,12 +350,15 @@ __global__ void header_kernel(RecHeader *hdr, int64_t n, int64_t m, int64_t m_pa
 
 // Filter records (FTile).  x0/y0 = smallest endpoint coordinate, W = largest
 // extent rounded up, s = 2^-(ilogb(W)+2) so that (x - x0) * s lies in
-// [0, 1/2] after the (monotone) roundings.  Per edge: L = |abx| + |aby| of
-// the FP32 direction, tau = 2^-22 * L * (1 + 2^-18) >= E * C * (1 + u) with
-// E = 2^-21 the cross-product error bound and C = L/2 (1 + 2^-20) the
-// cross-product magnitude bound, and the direction is scaled by
-// 2^k, 2k <= -ilogb(tau) - 1, so 2^2k <= 1/tau.  Degenerate FP32 directions
-// (L == 0) get a zero direction: their products are 0, never certain.
+// [0, 1/2] after the (monotone) roundings.  Per edge, with L = |abx| + |aby|
+// of the FP32 direction: every cross product c of a point with the edge's
+// line, evaluated in FP32 from these records, is within E = 2^-23 (1 + 3L)
+// of the exact one (2x the bound derived in DESIGN.md, which also covers the
+// reference's own FP64 rounding) and |c| <= C = L/2 (1 + 2^-20) + E.  The
+// direction and line constant are scaled by sigma <= 1/sqrt(E C (1 + 2^-20))
+// (FP32, rounded down; the scaling rounding is part of E), so a product of
+// two scaled cross products above 1 in magnitude certifies both signs.
+// Degenerate FP32 directions (L == 0) get zeros: products 0, never certain.
 __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *sx,
                             const double *sy) {
   const double x0 = sx[0], y0 = sy[0];
@@ -372,17 +375,22 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
       const float bx = __double2float_rn(__dmul_rn(__dsub_rn(r.bx, x0), s));
       const float by = __double2float_rn(__dmul_rn(__dsub_rn(r.by, y0), s));
       const float abx = __fsub_rn(bx, ax), aby = __fsub_rn(by, ay);
-      // products of FP32 values are exact in FP64; one FP64 and one FP32 rounding
-      const float ka = __double2float_rn(
-          __dsub_rn(__dmul_rn((double)abx, (double)ay), __dmul_rn((double)aby, (double)ax)));
+      // ka = ab x a: products of FP32 values are exact in FP64, one rounding
+      const double ka = __dsub_rn(__dmul_rn((double)abx, (double)ay),
+                                  __dmul_rn((double)aby, (double)ax));
       const double L = fabs((double)abx) + fabs((double)aby);
       f[kFAx] = ax; f[kFAy] = ay; f[kFBx] = bx; f[kFBy] = by;
       if (L > 0.0) {
-        const double tau = L * 0x1p-22 * (1.0 + 0x1p-18);
-        const int k = (-ilogb(tau) - 1) / 2;  // tau < 2^-21, so the numerator is > 0
-        f[kFSabx] = scalbnf(abx, k);
-        f[kFNsaby] = -scalbnf(aby, k);
-        f[kFNska] = -scalbnf(ka, k);
+        // E: error bound of a scaled cross product (relative to the scale),
+        // C: its magnitude bound; scale sigma <= 1/sqrt(E C (1+u)) so that
+        // |product of two| > 1 certifies both signs
+        const double E = 0x1p-23 * (1.0 + 3.0 * L);
+        const double C = 0.5 * L * (1.0 + 0x1p-20) + E;
+        const double tau = E * C * (1.0 + 0x1p-20);
+        const float sig = __double2float_rd((1.0 / sqrt(tau)) * (1.0 - 0x1p-40));
+        f[kFSabx] = __double2float_rn((double)abx * (double)sig);
+        f[kFNsaby] = -__double2float_rn((double)aby * (double)sig);
+        f[kFNska] = -__double2float_rn(ka * (double)sig);
       }
       theta = rv.theta[e];
     }
