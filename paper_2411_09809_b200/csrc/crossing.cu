@@ -722,11 +722,30 @@ __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
 // M_k = max(P12, P34) of one j-edge (shared memory) against the thread's K
 // i-edges; masked pairs of a diagonal tile get M = 2 (certain miss).
 // Per pair: 8 FFMA + 2 FMUL, issued as packed pairs over two i-edges.
+// Shared-memory loads by 32-bit shared address (the stage base is computed
+// once per unit, so the block loop carries no generic-to-shared conversions).
+// volatile: never hoisted above the stage's mbarrier wait.
+#ifndef GLR_LDS_ASM
+#define GLR_LDS_ASM asm volatile
+#endif
+__device__ __forceinline__ float4 lds_f4(unsigned addr) {
+  float4 v;
+  GLR_LDS_ASM("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  GLR_LDS_ASM("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 template <bool DIAG>
-__device__ __forceinline__ void filter_m(const FIRegs &R, const JRec *jr, int jj,
+__device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj,
                                          float (&M)[kK]) {
-  const float4 q0 = jr[jj].c;  // cx cy dx dy
-  const float4 q1 = jr[jj].k;  // scdx -scdy -skc
+  const float4 q0 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec));       // cx cy dx dy
+  const float4 q1 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec) + 16);  // scdx -scdy -skc
   const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
   const uint64_t DX = f2_bcast(q0.z), DY = f2_bcast(q0.w);
   const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y), NSKC = f2_bcast(q1.z);
@@ -755,8 +774,8 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, const JRec *jr, int jj
 // the hot path has no branch inside the block and the compiler can
 // interleave its NJ independent j-steps.
 template <bool ANGLE, bool DIAG, int NJ>
-__device__ __forceinline__ void filter_block(const FIRegs &R, const JRec *jr,
-                                             const double *sth, int jj0,
+__device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
+                                             unsigned thaddr, int jj0,
                                              unsigned (&cnt)[kK], double (&dev)[kK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
@@ -766,8 +785,8 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const JRec *jr,
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kK];
-    filter_m<DIAG>(R, jr, jj0 + q, M);
-    const double thj = ANGLE ? sth[jj0 + q] : 0.0;
+    filter_m<DIAG>(R, jaddr, jj0 + q, M);
+    const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
       any |= fabsf(M[k]) <= 1.0f;
@@ -797,7 +816,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const JRec *jr,
 #pragma unroll 1
     for (int q = 0; q < NJ; ++q) {
       float M[kK];
-      filter_m<DIAG>(R, jr, jj0 + q, M);
+      filter_m<DIAG>(R, jaddr, jj0 + q, M);
 #pragma unroll
       for (int k = 0; k < kK; ++k) {
         if (fabsf(M[k]) <= 1.0f) {
@@ -929,11 +948,15 @@ struct UnitCursor {
   bool valid;
   __device__ void start(uint64_t first_chunk) {
     ch = first_chunk;
+    u = e = ti = tj = 0;  // defined even when this CTA owns no unit
     begin_chunk();
   }
   __device__ void begin_chunk() {
     valid = ch < nchunks;
-    if (!valid) return;
+    if (!valid) {
+      u = e = 0;
+      return;
+    }
     u = ubeg + ch * chunk;
     e = u + chunk < uend ? u + chunk : uend;
     if (ulist == nullptr) band_unit_coords(u, T, W, &ti, &tj);
@@ -968,6 +991,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+#ifdef GLR_XWATCHDOG
+  for (long long spin = 0;; ++spin) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin == 2000000) {
+      printf("mbar_wait stuck: block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x,
+             bar, parity);
+      __trap();
+    }
+  }
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
@@ -975,6 +1016,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // TMA bulk copy global -> shared, completion signalled on `bar`.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
@@ -1056,8 +1098,8 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     }
     mbar_wait(&full[stage], (parity >> stage) & 1u);  // this unit's j-tile has landed
     parity ^= 1u << stage;
-    const JRec *jr = sj[stage];
-    const double *jth = sth[stage];
+    const unsigned jr = smem_u32(sj[stage]);
+    const unsigned jth = smem_u32(sth[stage]);
     unsigned cnt[kK];
     double dev[kK];
 #pragma unroll
