@@ -40,12 +40,19 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 CONFIG = 5
-FP64_PER_PAIR_EC = 18      # DADD/DMUL of the bit-exact predicate
+FP64_PER_PAIR_EC = 18      # DADD/DMUL of the reference predicate
 FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
 FP64_PER_PAIR_NC = 5
-# Bytes the pair kernel must read at least once per launch: EdgeRec 64 B +
-# theta 8 B + ids 8 B + run-start flag 4 B per edge.
-REC_BYTES_PER_EDGE = 84
+# The default pair kernel (certified FP32 filter) per pair:
+# 8 FFMA + 2 FMUL on the FP32 FMA pipe (issued as packed pairs) and, fused
+# with E_ca, 3 DADD + 1 DFMA on the FP64 pipe.
+FMA_PER_PAIR = 10
+FP64_PER_PAIR_FILTER_ECA = 4
+FMA_LANES_PER_CLK_SM = 128   # measured 124 (FFMA2/FMUL2/FADD2, profiles/r01_packed.txt)
+FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
+# Bytes the pair kernel must read at least once per launch: i-role filter
+# record 36 B + j-role record 32 B + theta 8 B per edge.
+REC_BYTES_PER_EDGE = 76
 C5_DRAM_BYTES_PER_LAUNCH = 227_204_840_192 + 191_279_104   # profiles/r01_dram_c5.txt
 CPU_SAMPLE_EDGES = 120_000
 CPU_SAMPLE_SEED = 99
@@ -328,14 +335,19 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # FP64 roofline of the dominant kernel (cross_pairs_kernel<fast, angle>)
+    # Roofline of the dominant kernel (cross_filter_kernel<angle>): its
+    # algorithm loads the FP32 FMA pipe most (10 lane-ops per pair against
+    # 128 lanes/clk/SM, vs 4 FP64 lane-ops against 64), so that pipe bounds it.
     clk = clocks.summary()
-    fast = M.CrossingRecords(dg).fast_path()
+    recs = M.CrossingRecords(dg)
+    fast, mode = recs.fast_path(), recs.mode()
     pairs_per_launch = P_E / world
-    achieved = FP64_PER_PAIR_ECA * pairs_per_launch / (kernel_ms * 1e-3) / 1e12
-    peak_max = 64 * 148 * 1965e6 / 1e12
+    pair_rate = pairs_per_launch / (kernel_ms * 1e-3)
     sm_mhz = clk.get("sm_mhz") or 1965.0
-    peak_run = 64 * 148 * sm_mhz * 1e6 / 1e12
+    peak_run = FMA_LANES_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
+    peak_max = FMA_LANES_PER_CLK_SM * 148 * 1965e6 / 1e12
+    achieved = FMA_PER_PAIR * pair_rate / 1e12
+    fp64_peak_run = FP64_LANES_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
     cpu = None
     if not args.no_cpu_baseline:
         from oracle import sweep as S
@@ -362,7 +374,7 @@ def main():
         "config": _config_desc(g, p, world),
         "result": {"edge_crossing": int(count), "dev_sum": dev_sum,
                    "edge_crossing_angle": 1.0 - (dev_sum / ideal) / count if count else 1.0,
-                   "node_occlusion": int(occ_count), "fast_sign_path": fast},
+                   "node_occlusion": int(occ_count), "fast_window": fast},
         "occlusion": {"metric": "node-pair occlusion tests/s", "value": P_V / (occ_ms * 1e-3),
                       "unit": "pairs/s", "ms_per_step": occ_ms, "strategy": "dense",
                       "fp64_tflops": FP64_PER_PAIR_NC * P_V / world / (occ_ms * 1e-3) / 1e12,
@@ -373,20 +385,30 @@ def main():
                                  "dense_units": M.occlusion_units(n),
                                  "note": "effective rate: same count, Morton order + "
                                          "candidate tile pairs (incl. plan build)"}},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_run,
-                     "unit": "TFLOP/s (FP64 DADD/DMUL instr, 1 per lane)",
+        "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": peak_run,
+                     "unit": "T lane-op/s (FP32 FFMA/FMUL on the FMA pipe)",
                      "frac": achieved / peak_run,
                      "frac_at_max_clock": achieved / peak_max, "peak_at_max_clock": peak_max,
-                     "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x median SM clock "
-                                    "under load (microbenchmarked DADD/DMUL: 61.7 "
-                                    "lanes/clk/SM, profiles/r01_pipes.txt); "
-                                    "MEASURED_PEAKS.json has no FP64 entry",
-                     "kernel": "cross_pairs_kernel<fast,angle>",
+                     "peak_source": "128 FP32 lanes/clk/SM x 148 SMs x median SM clock under "
+                                    "load (microbenchmarked FFMA2/FMUL2/FADD2: 124 "
+                                    "lanes/clk/SM, profiles/r01_packed.txt)",
+                     "kernel": "cross_filter_kernel<angle>" if mode == 2 else
+                               "cross_pairs_kernel<mode %d>" % mode,
+                     "pair_kernel_mode": mode,
                      "kernel_ms": kernel_ms,
-                     "fp64_per_pair": FP64_PER_PAIR_ECA,
+                     "ops_per_pair": {"fp32_fma_pipe": FMA_PER_PAIR,
+                                      "fp64_pipe": FP64_PER_PAIR_FILTER_ECA},
+                     "fp64_pipe_frac": FP64_PER_PAIR_FILTER_ECA * pair_rate / 1e12 / fp64_peak_run,
+                     # the reference formulation (22 FP64
+                     # instructions per pair) at this pair rate, against the
+                     # FP64 peak: > 1 because the filter retires most pairs
+                     # without FP64 arithmetic
+                     "fp64_equivalent": {"fp64_per_pair": FP64_PER_PAIR_ECA,
+                                         "tflops": FP64_PER_PAIR_ECA * pair_rate / 1e12,
+                                         "vs_fp64_peak": FP64_PER_PAIR_ECA * pair_rate / 1e12
+                                         / fp64_peak_run},
                      # DRAM read+write bytes of one full-C5 launch from ncu
                      # (profiles/r01_dram_c5.txt); per-rank share for N>1.
-                     # The kernel is FP64-bound: 227 GB over 10.6 s = 21 GB/s.
                      "traffic": C5_DRAM_BYTES_PER_LAUNCH / world,
                      "traffic_unit": "bytes/launch (dram__bytes_read+write, ncu)",
                      "algorithmic_bytes": REC_BYTES_PER_EDGE * m},

@@ -978,6 +978,11 @@ struct UnitCursor {
   }
 };
 
+#ifdef GLR_XWAITSTAT
+// stage-wait cycles (first kStages units / later), counts, compute cycles
+__device__ unsigned long long g_wait_stats[5];
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -1090,13 +1095,30 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   uint64_t cur_ti = ~0ull;
   int stage = 0;
   unsigned parity = 0u;  // bit st: phase of full[st] this warp waits for
+#ifdef GLR_XWAITSTAT
+  long long unit_t0 = 0;
+  int nunit = 0;
+#endif
   while (cur.valid) {
     const uint64_t ti = cur.ti, tj = cur.tj;
     if (ti != cur_ti) {
       load_fi<ANGLE>(R, ftile, ti);
       cur_ti = ti;
     }
+#ifdef GLR_XWAITSTAT
+    const long long w0 = clock64();
+#endif
     mbar_wait(&full[stage], (parity >> stage) & 1u);  // this unit's j-tile has landed
+#ifdef GLR_XWAITSTAT
+    if ((threadIdx.x & 31) == 0) {
+      const long long w1 = clock64();
+      atomicAdd(&g_wait_stats[nunit < kStages ? 0 : 1], (unsigned long long)(w1 - w0));
+      atomicAdd(&g_wait_stats[nunit < kStages ? 2 : 3], 1ull);
+      if (nunit > 0) atomicAdd(&g_wait_stats[4], (unsigned long long)(w0 - unit_t0));
+      unit_t0 = w1;
+    }
+    ++nunit;
+#endif
     parity ^= 1u << stage;
     const unsigned jr = smem_u32(sj[stage]);
     const unsigned jth = smem_u32(sth[stage]);
@@ -1674,6 +1696,17 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
   return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, nullptr, 0, unit_begin, unit_end,
                              0, 1, d_out, st);
 }
+
+#ifdef GLR_XWAITSTAT
+int glr_debug_wait_stats(unsigned long long *h_out, int reset) {
+  cudaMemcpyFromSymbol(h_out, glr::g_wait_stats, sizeof(unsigned long long) * 5);
+  if (reset) {
+    unsigned long long z[5] = {0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(glr::g_wait_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 int glr_crossing_set_mode(void *d_records, int mode, void *stream) {
   if (d_records == nullptr || mode < glr::kModeGeneral || mode > glr::kModeFilter) {
