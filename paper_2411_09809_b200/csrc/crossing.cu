@@ -669,14 +669,16 @@ struct FIRegs {
   double th[kK];
 };
 
-// i-edge k of group g is tile slot threadIdx.x + (2g + h) * kThreads, h = 0/1
-// in the low/high half of the packed registers (one 64-bit load each).
+// i-edge k of group g is tile slot islot + (2g + h) * kThreads, h = 0/1 in
+// the low/high half of the packed registers (one 64-bit load each); islot
+// in [0, kThreads) is the thread's slot within its i-tile slice.
 template <bool ANGLE>
-__device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint64_t ti) {
+__device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint64_t ti,
+                               int islot) {
   const FTile &t = ftile[ti];
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][g][threadIdx.x]);
+    const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][g][islot]);
     constexpr int kField = kFGroups * kThreads;  // uint64 stride between fields
     R.ax[g] = v[kFAx * kField];
     R.ay[g] = v[kFAy * kField];
@@ -685,8 +687,8 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
     R.sabx[g] = v[kFSabx * kField];
     R.nsaby[g] = v[kFNsaby * kField];
     R.nska[g] = v[kFNska * kField];
-    R.th[2 * g] = ANGLE ? t.theta[threadIdx.x + (2 * g) * kThreads] : 0.0;
-    R.th[2 * g + 1] = ANGLE ? t.theta[threadIdx.x + (2 * g + 1) * kThreads] : 0.0;
+    R.th[2 * g] = ANGLE ? t.theta[islot + (2 * g) * kThreads] : 0.0;
+    R.th[2 * g + 1] = ANGLE ? t.theta[islot + (2 * g + 1) * kThreads] : 0.0;
   }
 }
 
@@ -742,7 +744,7 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
 }
 
 template <bool DIAG>
-__device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj,
+__device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj, int islot,
                                          float (&M)[kK]) {
   const float4 q0 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec));       // cx cy dx dy
   const float4 q1 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec) + 16);  // scdx -scdy -skc
@@ -763,7 +765,7 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
   if (DIAG) {
 #pragma unroll
     for (int k = 0; k < kK; ++k)
-      if (!(jj > (int)threadIdx.x + k * kThreads)) M[k] = 2.0f;
+      if (!(jj > islot + k * kThreads)) M[k] = 2.0f;
   }
 }
 
@@ -775,7 +777,7 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 // interleave its NJ independent j-steps.
 template <bool ANGLE, bool DIAG, int NJ>
 __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
-                                             unsigned thaddr, int jj0,
+                                             unsigned thaddr, int jj0, int islot,
                                              unsigned (&cnt)[kK], double (&dev)[kK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
@@ -785,7 +787,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kK];
-    filter_m<DIAG>(R, jaddr, jj0 + q, M);
+    filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
@@ -816,11 +818,11 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
 #pragma unroll 1
     for (int q = 0; q < NJ; ++q) {
       float M[kK];
-      filter_m<DIAG>(R, jaddr, jj0 + q, M);
+      filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
 #pragma unroll
       for (int k = 0; k < kK; ++k) {
         if (fabsf(M[k]) <= 1.0f) {
-          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + threadIdx.x + k * kThreads,
+          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + islot + k * kThreads,
                                              jbase + jj0 + q, kappa);
           if (t >= 0.0) {
             cnt[k] += 1u;
@@ -938,51 +940,6 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
   }
 }
 
-// Walks this CTA's units: chunks of `chunk` consecutive units dealt
-// round-robin over the CTAs of all ranks (see cross_pairs_kernel), in the
-// banded order (or the explicit culled list).
-struct UnitCursor {
-  const int2 *ulist;
-  uint64_t T, W, ubeg, uend, chunk, nchunks, step;
-  uint64_t ch, u, e, ti, tj;
-  bool valid;
-  __device__ void start(uint64_t first_chunk) {
-    ch = first_chunk;
-    u = e = ti = tj = 0;  // defined even when this CTA owns no unit
-    begin_chunk();
-  }
-  __device__ void begin_chunk() {
-    valid = ch < nchunks;
-    if (!valid) {
-      u = e = 0;
-      return;
-    }
-    u = ubeg + ch * chunk;
-    e = u + chunk < uend ? u + chunk : uend;
-    if (ulist == nullptr) band_unit_coords(u, T, W, &ti, &tj);
-    else load();
-  }
-  __device__ void load() {
-    const int2 p = ulist[u];
-    ti = (uint64_t)p.x;
-    tj = (uint64_t)p.y;
-  }
-  __device__ void advance() {
-    if (++u < e) {
-      if (ulist == nullptr) band_advance(T, W, &ti, &tj);
-      else load();
-    } else {
-      ch += step;
-      begin_chunk();
-    }
-  }
-};
-
-#ifdef GLR_XWAITSTAT
-// stage-wait cycles (first kStages units / later), counts, compute cycles
-__device__ unsigned long long g_wait_stats[5];
-#endif
-
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -1033,16 +990,42 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       : "memory");
 }
 
-// Filter-mode pair kernel (hdr->fast == kModeFilter): same unit space,
-// chunking and reductions as cross_pairs_kernel.  The j-tile records (8 KB,
-// + 2 KB of theta) of the CTA's next kStages units sit in a ring of shared
-// memory stages filled by TMA bulk copies.  Warps do not synchronise with
-// each other: each waits only for its unit's stage to land (mbarrier), and
-// the LAST warp to finish with a stage refills it with the unit kStages
-// ahead, so warps may drift up to kStages - 1 units apart (a CTA barrier per
-// unit cost ~19% of the time: warps that meet uncertain pairs run longer).
+// Filter-mode pair kernel (hdr->fast == kModeFilter): same unit space and
+// chunk ownership as cross_pairs_kernel.  The j-tile records (8 KB, + 2 KB
+// of theta) of the CTA's next kStages units sit in a ring of shared-memory
+// stages filled by TMA bulk copies.  Work is handed out in SLICES: a unit's
+// i-tile is cut into kWarps slices of 32 lanes x K i-edges, and each warp
+// takes the CTA's next slice from a shared counter, so fast warps simply do
+// more slices -- warps never wait for each other (a per-unit CTA barrier,
+// or a ring where the slowest warp gates the refills, cost 10-19%: warps of
+// a CTA progress at persistently different rates).  The warp that finishes
+// a unit's last slice refills its stage with the unit kStages ahead.
+// Sums are made order-independent so results stay deterministic: counts are
+// integers, and each lane's per-slice angle sum is added as a 2^-50
+// fixed-point integer into a 128-bit accumulator.
 // Shared-vertex pairs are never certain (an exact c is 0), so they reach
 // exact_pair, which tests ids: no adjacency correction in this mode.
+struct CtaUnits {  // the CTA's units as a flat sequence (see cross_pairs_kernel)
+  const int2 *ulist;
+  uint64_t T, W, ubeg, uend, chunk, nchunks, step, ch0;
+  __device__ bool at(uint64_t uq, uint64_t *ti, uint64_t *tj) const {
+    const uint64_t ch = ch0 + (uq / chunk) * step;
+    if (ch >= nchunks) return false;
+    const uint64_t u = ubeg + ch * chunk + uq % chunk;
+    if (u >= uend) return false;
+    if (ulist != nullptr) {
+      const int2 p = ulist[u];
+      *ti = (uint64_t)p.x;
+      *tj = (uint64_t)p.y;
+    } else {
+      band_unit_coords(u, T, W, ti, tj);
+    }
+    return true;
+  }
+};
+
+constexpr double kDevScale = 0x1p50;  // fixed-point scale of the angle sums
+
 template <bool ANGLE>
 __global__ void __launch_bounds__(kThreads,
                                   ANGLE ? kFilterMinBlocksAngle : kFilterMinBlocksCount)
@@ -1057,19 +1040,18 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   __shared__ __align__(128) JRec sj[kStages][kTile];
   __shared__ __align__(128) double sth[kStages][ANGLE ? kTile : 2];
   __shared__ __align__(8) uint64_t full[kStages];
-  __shared__ unsigned done[kStages];  // warps finished with the stage, cumulative
-  __shared__ unsigned long long red_u[kWarps];
-  __shared__ double red_d[kWarps];
+  __shared__ unsigned done[kStages];  // slices finished with the stage, cumulative
+  __shared__ unsigned next_slice;
+  __shared__ unsigned long long acc_cnt, acc_lo, acc_hi;
   constexpr unsigned kJBytes = kTile * sizeof(JRec);
   constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
   const unsigned lane = threadIdx.x & 31;
 
-  UnitCursor cur;
-  cur.ulist = ulist; cur.T = T; cur.W = W; cur.ubeg = ubeg; cur.uend = uend; cur.chunk = chunk;
-  cur.nchunks = (uend - ubeg + chunk - 1) / chunk;
-  cur.step = (uint64_t)sworld * gridDim.x;
-  cur.start(srank + (uint64_t)sworld * blockIdx.x);
-  UnitCursor ahead = cur;  // the unit kStages after cur (refill target)
+  CtaUnits cu;
+  cu.ulist = ulist; cu.T = T; cu.W = W; cu.ubeg = ubeg; cu.uend = uend; cu.chunk = chunk;
+  cu.nchunks = (uend - ubeg + chunk - 1) / chunk;
+  cu.step = (uint64_t)sworld * gridDim.x;
+  cu.ch0 = srank + (uint64_t)sworld * blockIdx.x;
 
   auto issue = [&](int st, uint64_t tj_) {
     mbar_expect_tx(&full[st], kJBytes + kThBytes);
@@ -1081,45 +1063,41 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
       mbar_init(&full[st], 1);
       done[st] = 0;
     }
+    next_slice = 0;
+    acc_cnt = acc_lo = acc_hi = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int st = 0; st < kStages; ++st) {
+      uint64_t a, b;
+      if (cu.at((uint64_t)st, &a, &b)) issue(st, b);
+    }
   }
   __syncthreads();
-  for (int st = 0; st < kStages; ++st) {
-    if (threadIdx.x == 0 && ahead.valid) issue(st, ahead.tj);
-    ahead.advance();
-  }
 
-  unsigned long long total = 0;
-  double dsum = 0.0, dcomp = 0.0;
+  unsigned long long total = 0, dlo = 0, dhi = 0;
   FIRegs R;
   uint64_t cur_ti = ~0ull;
-  int stage = 0;
-  unsigned parity = 0u;  // bit st: phase of full[st] this warp waits for
-#ifdef GLR_XWAITSTAT
-  long long unit_t0 = 0;
-  int nunit = 0;
-#endif
-  while (cur.valid) {
-    const uint64_t ti = cur.ti, tj = cur.tj;
-    if (ti != cur_ti) {
-      load_fi<ANGLE>(R, ftile, ti);
+  int cur_slice = -1;
+  for (;;) {
+    unsigned q = 0;
+    if (lane == 0) q = atomicAdd(&next_slice, 1u);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    const uint64_t uq = q / kWarps;
+    const int slice = (int)(q % kWarps);
+    uint64_t ti, tj;
+    if (!cu.at(uq, &ti, &tj)) break;
+    const int islot = slice * 32 + (int)lane;
+    if (ti != cur_ti || slice != cur_slice) {
+      load_fi<ANGLE>(R, ftile, ti, islot);
       cur_ti = ti;
+      cur_slice = slice;
     }
-#ifdef GLR_XWAITSTAT
-    const long long w0 = clock64();
-#endif
-    mbar_wait(&full[stage], (parity >> stage) & 1u);  // this unit's j-tile has landed
-#ifdef GLR_XWAITSTAT
-    if ((threadIdx.x & 31) == 0) {
-      const long long w1 = clock64();
-      atomicAdd(&g_wait_stats[nunit < kStages ? 0 : 1], (unsigned long long)(w1 - w0));
-      atomicAdd(&g_wait_stats[nunit < kStages ? 2 : 3], 1ull);
-      if (nunit > 0) atomicAdd(&g_wait_stats[4], (unsigned long long)(w0 - unit_t0));
-      unit_t0 = w1;
+    const int stage = (int)(uq % kStages);
+    const unsigned use = (unsigned)(uq / kStages);
+    // the stage's previous unit must be fully released (its refill issued)
+    // before its mbarrier phase parity identifies this use unambiguously
+    while (*(volatile unsigned *)&done[stage] < use * kWarps) {
     }
-    ++nunit;
-#endif
-    parity ^= 1u << stage;
+    mbar_wait(&full[stage], use & 1u);  // this unit's j-tile has landed
     const unsigned jr = smem_u32(sj[stage]);
     const unsigned jth = smem_u32(sth[stage]);
     unsigned cnt[kK];
@@ -1129,45 +1107,51 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, cnt, dev, kappa, rec, ids, theta,
-                                                ibase, jbase);
+        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, islot, cnt, dev, kappa, rec, ids,
+                                                theta, ibase, jbase);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, cnt, dev, kappa, rec, ids,
-                                                 theta, ibase, jbase);
+        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, islot, cnt, dev, kappa, rec,
+                                                 ids, theta, ibase, jbase);
     }
-    // release the stage; the last of the CTA's warps refills it
+    // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
       const unsigned old = atomicAdd(&done[stage], 1u);
-      if ((old + 1) % kWarps == 0 && ahead.valid) {
-        __threadfence_block();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(stage, ahead.tj);
+      if (old + 1 == (use + 1) * kWarps) {
+        uint64_t a, b;
+        if (cu.at(uq + kStages, &a, &b)) {
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(stage, b);
+        }
       }
     }
-    ahead.advance();
-    cur.advance();
-    stage = stage + 1 == kStages ? 0 : stage + 1;
     unsigned c = 0;
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
     total += c;
-    if (ANGLE) {
-      double y = __dsub_rn(s, dcomp);
-      double t = __dadd_rn(dsum, y);
-      dcomp = __dsub_rn(__dsub_rn(t, dsum), y);
-      dsum = t;
+    if (ANGLE) {  // s <= 2 * kTile * pi/2 < 2^10: s * 2^50 < 2^60
+      const unsigned long long f = (unsigned long long)__double2ll_rn(s * kDevScale);
+      dlo += f;
+      dhi += dlo < f ? 1ull : 0ull;
     }
   }
-  unsigned long long bc = block_sum_u64<kThreads>(total, red_u);
-  double bd = block_sum<kThreads>(dsum, red_d);
+  // order-independent CTA reduction (integer atomics commute)
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_down_sync(0xffffffffu, total, o);
+  if (lane == 0) atomicAdd(&acc_cnt, total);
+  if (ANGLE) {
+    const unsigned long long old = atomicAdd(&acc_lo, dlo);
+    atomicAdd(&acc_hi, dhi + (old + dlo < old ? 1ull : 0ull));
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    cta_cnt[blockIdx.x] = bc;
-    cta_dev[blockIdx.x] = bd;
+    cta_cnt[blockIdx.x] = acc_cnt;
+    cta_dev[blockIdx.x] =
+        ANGLE ? ((double)acc_hi * 0x1p64 + (double)acc_lo) / kDevScale : 0.0;
   }
 }
 
@@ -1696,17 +1680,6 @@ int glr_crossing_scan(const double *d_xy, int64_t n, const int64_t *d_edges, int
   return glr::crossing_pairs(rec.ptr, n, m, with_angle, ideal, nullptr, 0, unit_begin, unit_end,
                              0, 1, d_out, st);
 }
-
-#ifdef GLR_XWAITSTAT
-int glr_debug_wait_stats(unsigned long long *h_out, int reset) {
-  cudaMemcpyFromSymbol(h_out, glr::g_wait_stats, sizeof(unsigned long long) * 5);
-  if (reset) {
-    unsigned long long z[5] = {0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(glr::g_wait_stats, z, sizeof(z));
-  }
-  return 0;
-}
-#endif
 
 int glr_crossing_set_mode(void *d_records, int mode, void *stream) {
   if (d_records == nullptr || mode < glr::kModeGeneral || mode > glr::kModeFilter) {
