@@ -53,7 +53,7 @@ FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
 # Bytes the pair kernel must read at least once per launch: i-role filter
 # record 36 B + j-role record 32 B + theta 8 B per edge.
 REC_BYTES_PER_EDGE = 76
-C5_DRAM_BYTES_PER_LAUNCH = 227_204_840_192 + 191_279_104   # profiles/r01_dram_c5.txt
+C5_DRAM_BYTES_PER_LAUNCH = 289_670_264_576 + 339_670_528   # profiles/r01_dram_c5_filter.txt
 CPU_SAMPLE_EDGES = 120_000
 CPU_SAMPLE_SEED = 99
 
@@ -408,7 +408,7 @@ def main():
                                          "vs_fp64_peak": FP64_PER_PAIR_ECA * pair_rate / 1e12
                                          / fp64_peak_run},
                      # DRAM read+write bytes of one full-C5 launch from ncu
-                     # (profiles/r01_dram_c5.txt); per-rank share for N>1.
+                     # (profiles/r01_dram_c5_filter.txt); per-rank share for N>1.
                      "traffic": C5_DRAM_BYTES_PER_LAUNCH / world,
                      "traffic_unit": "bytes/launch (dram__bytes_read+write, ncu)",
                      "algorithmic_bytes": REC_BYTES_PER_EDGE * m},
