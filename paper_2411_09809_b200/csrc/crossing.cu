@@ -164,6 +164,14 @@ struct __align__(16) JRec {
   float4 k;
 };
 
+// Per tile: box of its edges' scaled FP32 endpoints and the largest L =
+// |abx| + |aby|; a unit's two boxes bound |p - a| for all its pairs, which
+// tightens the filter's certification threshold for spatially local units.
+struct __align__(16) TileBox {
+  float xlo, xhi, ylo, yhi;
+  float lmax, pad0, pad1, pad2;
+};
+
 // Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
 // newc[m_pad] | frec[m_pad] | inc[2m] (incident edge ids grouped by vertex) |
 // offs[n+1] | wofs[n+1].
@@ -172,6 +180,7 @@ struct RecView {
   EdgeRec *rec;
   FTile *ftile;
   JRec *jrec;
+  TileBox *tbox;
   double *theta;
   int2 *ids;
   int *newc;  // 1 if edge e starts a run of edges sharing endpoint a (or a tile)
@@ -184,7 +193,7 @@ inline int64_t pad_edges(int64_t m) { return ((m + kTile - 1) / kTile) * kTile; 
 inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t rec, theta, ids, newc, frec, jrec, inc, offs, wofs, total;
+  size_t rec, theta, ids, newc, frec, jrec, tbox, inc, offs, wofs, total;
 };
 
 inline Layout layout(int64_t n, int64_t m) {
@@ -197,7 +206,8 @@ inline Layout layout(int64_t n, int64_t m) {
   L.newc = L.ids + al256((size_t)mp * sizeof(int2));
   L.frec = L.newc + al256((size_t)mp * sizeof(int));
   L.jrec = L.frec + al256((size_t)(mp / kTile) * sizeof(FTile));
-  L.inc = L.jrec + al256((size_t)mp * sizeof(JRec));
+  L.tbox = L.jrec + al256((size_t)mp * sizeof(JRec));
+  L.inc = L.tbox + al256((size_t)(mp / kTile) * sizeof(TileBox));
   L.offs = L.inc + al256((size_t)(2 * (m < 0 ? 0 : m)) * sizeof(int));
   L.wofs = L.offs + al256((size_t)(nn + 1) * sizeof(int));
   L.total = L.wofs + al256((size_t)(nn + 1) * sizeof(long long));
@@ -215,6 +225,7 @@ inline RecView view(void *base, int64_t n, int64_t m) {
   v.newc = reinterpret_cast<int *>(p + L.newc);
   v.ftile = reinterpret_cast<FTile *>(p + L.frec);
   v.jrec = reinterpret_cast<JRec *>(p + L.jrec);
+  v.tbox = reinterpret_cast<TileBox *>(p + L.tbox);
   v.inc = reinterpret_cast<int *>(p + L.inc);
   v.offs = reinterpret_cast<int *>(p + L.offs);
   v.wofs = reinterpret_cast<long long *>(p + L.wofs);
@@ -405,6 +416,60 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
     j.k = make_float4(f[kFSabx], f[kFNsaby], f[kFNska], 0.0f);
     rv.jrec[e] = j;
   }
+}
+
+// One CTA (kTile threads) per tile: box of the real edges' scaled endpoints
+// and max L (pad edges are skipped; an all-pad tile gets an empty box).
+__global__ void __launch_bounds__(kTile) tile_fbox_kernel(int64_t m, RecView rv) {
+  __shared__ float red[5][kTile / 32];
+  const int64_t e = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  float xlo = INFINITY, xhi = -INFINITY, ylo = INFINITY, yhi = -INFINITY, l = 0.0f;
+  if (e < m) {
+    const JRec j = rv.jrec[e];
+    xlo = fminf(j.c.x, j.c.z); xhi = fmaxf(j.c.x, j.c.z);
+    ylo = fminf(j.c.y, j.c.w); yhi = fmaxf(j.c.y, j.c.w);
+    // L of the FP32 direction (exact float differences, rounded up)
+    l = __fadd_ru(fabsf(__fsub_rn(j.c.z, j.c.x)), fabsf(__fsub_rn(j.c.w, j.c.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    xlo = fminf(xlo, __shfl_down_sync(0xffffffffu, xlo, o));
+    xhi = fmaxf(xhi, __shfl_down_sync(0xffffffffu, xhi, o));
+    ylo = fminf(ylo, __shfl_down_sync(0xffffffffu, ylo, o));
+    yhi = fmaxf(yhi, __shfl_down_sync(0xffffffffu, yhi, o));
+    l = fmaxf(l, __shfl_down_sync(0xffffffffu, l, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = xlo; red[1][w] = xhi; red[2][w] = ylo; red[3][w] = yhi; red[4][w] = l;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kTile / 32; ++i) {
+      xlo = fminf(xlo, red[0][i]); xhi = fmaxf(xhi, red[1][i]);
+      ylo = fminf(ylo, red[2][i]); yhi = fmaxf(yhi, red[3][i]);
+      l = fmaxf(l, red[4][i]);
+    }
+    TileBox b;
+    b.xlo = xlo; b.xhi = xhi; b.ylo = ylo; b.yhi = yhi; b.lmax = l;
+    b.pad0 = b.pad1 = b.pad2 = 0.0f;
+    rv.tbox[blockIdx.x] = b;
+  }
+}
+
+// Certification threshold of a unit (tiles ti, tj).  With D = the larger
+// side of the union of the two tile boxes (so |p - a| <= D per axis for
+// every pair of the unit) and Lm = the larger tile lmax, the cross-product
+// error and magnitude bounds become E_u = 2^-23 (1.5 D + 3 L) and C_u = L D +
+// E_u, and a product above t = (1.5 D + 3 Lm)(3.5 D + 3 Lm)
+// (1 + 2^-18) >= sigma^2 E_u C_u (1 + 2^-20) certifies both signs; t is
+// capped at 1 (the unit-independent bound) and rounded up to FP32.
+__device__ inline float unit_threshold(const TileBox &a, const TileBox &b) {
+  const double D = fmax((double)fmaxf(a.xhi, b.xhi) - (double)fminf(a.xlo, b.xlo),
+                        (double)fmaxf(a.yhi, b.yhi) - (double)fminf(a.ylo, b.ylo));
+  const double Lm = (double)fmaxf(a.lmax, b.lmax);
+  if (!(D >= 0.0)) return 1.0f;  // an empty box (all-pad tile): keep the global bound
+  const double t = (1.5 * D + 3.0 * Lm) * (3.5 * D + 3.0 * Lm) * (1.0 + 0x1p-18);
+  return t >= 1.0 ? 1.0f : __double2float_ru(t);
 }
 
 __global__ void set_mode_kernel(RecHeader *hdr, int mode) {
@@ -777,7 +842,7 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 // interleave its NJ independent j-steps.
 template <bool ANGLE, bool DIAG, int NJ>
 __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
-                                             unsigned thaddr, int jj0, int islot,
+                                             unsigned thaddr, int jj0, int islot, float thr,
                                              unsigned (&cnt)[kK], double (&dev)[kK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
@@ -791,7 +856,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
-      any |= fabsf(M[k]) <= 1.0f;
+      any |= fabsf(M[k]) <= thr;
       // @(M < -1) cnt += 1 (and dev += t)
       if (ANGLE) {
         // dev += hit ? t : 0 as fma(t, {0.0 | 1.0}, dev): one DFMA and one SEL
@@ -799,18 +864,18 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
         const double t = angle_dev(R.th[k], thj, kappa);
         int hw;
         asm("{\n\t.reg .pred p;\n\t"
-            "setp.lt.f32 p, %2, 0fBF800000;\n\t"
+            "setp.lt.f32 p, %2, %3;\n\t"
             "@p add.u32 %0, %0, 1;\n\t"
             "selp.b32 %1, 1072693248, 0, p;\n\t}"
             : "+r"(cnt[k]), "=r"(hw)
-            : "f"(M[k]));
+            : "f"(M[k]), "f"(-thr));
         dev[k] = __fma_rn(t, __hiloint2double(hw, 0), dev[k]);
       } else {
         asm("{\n\t.reg .pred p;\n\t"
-            "setp.lt.f32 p, %1, 0fBF800000;\n\t"
+            "setp.lt.f32 p, %1, %2;\n\t"
             "@p add.u32 %0, %0, 1;\n\t}"
             : "+r"(cnt[k])
-            : "f"(M[k]));
+            : "f"(M[k]), "f"(-thr));
       }
     }
   }
@@ -821,7 +886,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
       filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
 #pragma unroll
       for (int k = 0; k < kK; ++k) {
-        if (fabsf(M[k]) <= 1.0f) {
+        if (fabsf(M[k]) <= thr) {
           const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + islot + k * kThreads,
                                              jbase + jj0 + q, kappa);
           if (t >= 0.0) {
@@ -1031,8 +1096,9 @@ __global__ void __launch_bounds__(kThreads,
                                   ANGLE ? kFilterMinBlocksAngle : kFilterMinBlocksCount)
 cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                     const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
-                    const double *__restrict__ theta, const int2 *__restrict__ ids,
-                    const int2 *__restrict__ ulist, uint64_t T, uint64_t W, uint64_t ubeg,
+                    const TileBox *__restrict__ tbox, const double *__restrict__ theta,
+                    const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
+                    uint64_t W, uint64_t ubeg,
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double kappa,
                     unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
@@ -1105,15 +1171,16 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
 #pragma unroll
     for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
+    const float thr = unit_threshold(tbox[ti], tbox[tj]);
     if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, islot, cnt, dev, kappa, rec, ids,
-                                                theta, ibase, jbase);
+        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, islot, thr, cnt, dev, kappa, rec,
+                                                ids, theta, ibase, jbase);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, islot, cnt, dev, kappa, rec,
-                                                 ids, theta, ibase, jbase);
+        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, islot, thr, cnt, dev, kappa,
+                                                 rec, ids, theta, ibase, jbase);
     }
     // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
@@ -1436,6 +1503,8 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
     GLR_LAUNCHED("rank_kernel");
     frec_kernel<<<blocks_for(m_pad, nt, 16), nt, 0, st>>>(mm, m_pad, rv, sx, sy);
     GLR_LAUNCHED("frec_kernel");
+    tile_fbox_kernel<<<(unsigned)(m_pad / kTile), kTile, 0, st>>>(mm, rv);
+    GLR_LAUNCHED("tile_fbox_kernel");
     // incidence lists grouped by vertex; stable, so each list is ordered
     // (edges where the vertex is first, then where it is second, by edge id)
     tb = t_cub;
@@ -1522,7 +1591,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel<angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
@@ -1539,7 +1608,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
         cc, cd);
     GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,

@@ -162,6 +162,41 @@ def test_filter_modes_agree_with_oracle(gpu, name):
     assert c2n == cw
 
 
+def lattice_local(seed=10, side=120):
+    """Jittered unit lattice with nearest-neighbour edges (C4-like): after
+    the Morton sort the culled units are spatially local, so the per-unit
+    certification threshold drops far below 1."""
+    rng = np.random.default_rng(seed)
+    gx, gy = np.meshgrid(np.arange(side, dtype=np.float64), np.arange(side, dtype=np.float64))
+    xy = np.stack([gx.ravel(), gy.ravel()], 1) + rng.uniform(-1e-3, 1e-3, (side * side, 2))
+    idx = np.arange(side * side).reshape(side, side)
+    pairs = np.concatenate([np.stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()], 1),
+                            np.stack([idx[:-1, :].ravel(), idx[1:, :].ravel()], 1),
+                            np.stack([idx[:-1, :-1].ravel(), idx[1:, 1:].ravel()], 1),
+                            np.stack([idx[:-1, 1:].ravel(), idx[1:, :-1].ravel()], 1)])
+    return xy, pairs
+
+
+@pytest.mark.parametrize("name", sorted(CASES) + ["lattice_local"])
+def test_filter_culled_units_agree_with_oracle(gpu, name):
+    """Culled (Morton-ordered, spatially local) units use tightened per-unit
+    thresholds: mode 2 must still equal mode 0 and the oracle."""
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import metrics as M
+
+    builder = CASES.get(name) or lattice_local
+    g = _graph(*builder())
+    dg = M.DeviceGraph.from_graph(g)
+    res = {}
+    for mode in (2, 0):
+        rec = M.CrossingRecords(dg, "culled")
+        rec.set_mode(mode)
+        res[mode] = rec.partial(IDEAL, 0, rec.units).tolist()
+    cw, dw = S.crossing_scan(g.xy, g.edges, IDEAL)
+    assert int(res[2][0]) == int(res[0][0]) == cw
+    assert strict_close(res[2][1], dw) and strict_close(res[0][1], dw)
+
+
 @pytest.mark.parametrize("name", ["near_collinear", "hubs", "exact_lattice"])
 def test_filter_unit_partials_and_shards(gpu, name):
     from paper_2411_09809_b200 import metrics as M

@@ -4,6 +4,7 @@ effective pair-test rates.  Used for profiles/rNN_configs.txt.
     python tools/config_bench.py [configs...]
 """
 import json
+import os
 import sys
 import time
 
@@ -36,6 +37,8 @@ def run(k):
     for strat in ("auto", "dense") if k != 5 else ("auto",):
         def cross():
             rec = M.CrossingRecords(dg, strat)
+            if os.environ.get("GLR_BENCH_MODE"):  # force a pair-kernel mode (0/1/2)
+                rec.set_mode(int(os.environ["GLR_BENCH_MODE"]))
             return rec.partial(p["ideal"], 0, rec.units).tolist(), rec.culled, rec.units
 
         (out, sec) = timed(cross, reps=1 if (strat == "dense" and k >= 4) else 2)
