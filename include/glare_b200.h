@@ -196,6 +196,17 @@ int glr_edge_length_variation(const double *d_xy, int64_t n,
 int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges,
                       int64_t m, double *d_out, void *stream);
 
+/* ---- force-directed layout: graphio.py:151-197 --- */
+
+/* Runs `iterations` rounds of the reference's fr_layout on d_pos (n x 2
+ * float64, row-major): in = the seeded start layout, out = the final layout
+ * rescaled into [0, extent]^2.  d_ei/d_ej: the normalized edges as indices
+ * into the sorted vertex ids (m int64 each).  Bit-identical to the
+ * reference's numpy iteration (pairwise-summation order of the repulsion
+ * sums, np.add.at order of the spring pulls). */
+int glr_fr_layout(double *d_pos, int64_t n, const int64_t *d_ei, const int64_t *d_ej,
+                  int64_t m, int iterations, double extent, void *stream);
+
 /* ---- introspection (tests / bench) --------------------------------------- */
 
 /* Pair-kernel mode of the prepared records (synchronous: reads the records

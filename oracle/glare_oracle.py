@@ -341,3 +341,46 @@ def node_occlusion_units(xy, r, tile: int, ubeg: int, uend: int) -> int:
         dy = y[I] - y[J]
         total += int(np.count_nonzero((dx * dx + dy * dy < thr) & (J > I)))
     return total
+
+
+# ---- force-directed layout --------------------------
+
+def fr_layout_positions(n: int, ei: np.ndarray, ej: np.ndarray, iterations: int, seed: int,
+                        extent: float) -> np.ndarray:
+    """Final positions of the reference's fr_layout (graphio.py:151-197) for n
+    vertices and normalized index edges (ei, ej).
+
+    Restated row by row: each vertex's repulsion is the numpy sum over the
+    full row of (p_i - p_j) * k^2 / max(|p_i - p_j|^2, 1e-12), which numpy
+    reduces with its pairwise summation, so the row sums are bit-identical
+    to the reference's blocked evaluation; the spring pulls are scattered
+    with np.add.at in edge order (first -pull at ei, then +pull at ej).
+    """
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(0.0, extent, size=(n, 2))
+    k = extent / math.sqrt(n)
+    ksq = k * k
+    t = extent / 10.0
+    rows = max(1, 1_000_000 // n)
+    for _ in range(iterations):
+        disp = np.zeros((n, 2))
+        for s in range(0, n, rows):
+            e = min(n, s + rows)
+            dx = pos[s:e, 0][:, None] - pos[:, 0][None, :]
+            dy = pos[s:e, 1][:, None] - pos[:, 1][None, :]
+            d2 = np.maximum(dx * dx + dy * dy, 1e-12)
+            coef = ksq / d2
+            disp[s:e, 0] += (dx * coef).sum(axis=1)
+            disp[s:e, 1] += (dy * coef).sum(axis=1)
+        dxy = pos[ei] - pos[ej]
+        dist = np.sqrt(dxy[:, 0] * dxy[:, 0] + dxy[:, 1] * dxy[:, 1])
+        pull = dxy * (dist / k)[:, None]
+        np.add.at(disp, ei, -pull)
+        np.add.at(disp, ej, pull)
+        length = np.maximum(np.sqrt(disp[:, 0] * disp[:, 0] + disp[:, 1] * disp[:, 1]), 1e-12)
+        pos = pos + disp * (np.minimum(length, t) / length)[:, None]
+        t *= 0.95
+    lo = pos.min(axis=0)
+    span = pos.max(axis=0) - lo
+    span[span <= 0] = 1.0
+    return (pos - lo) / span * extent

@@ -5,6 +5,7 @@ The five metric functions keep the reference's signatures and outputs
 hand-written sm_100a kernels through the C ABI in include/glare_b200.h.
 """
 
+from .layout import fr_layout, generate_layout, random_layout
 from .metrics import (
     CrossingRecords,
     DeviceGraph,
@@ -30,6 +31,9 @@ from .model import (
 )
 
 __all__ = [
+    "fr_layout",
+    "generate_layout",
+    "random_layout",
     "CrossingRecords",
     "DeviceGraph",
     "GlareError",
