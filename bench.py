@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-layout", action="store_true", help="skip the fr_layout line item")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -312,6 +313,26 @@ def main():
     occ_culled_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / args.steps)
     assert out[2].item() == occ_count, (out[2].item(), occ_count)
 
+    # ---- fr_layout: repulsion pairs/s, rank 0 ----
+    layout = None
+    if rank == 0 and not args.no_layout:
+        from paper_2411_09809_b200 import fr_layout
+        from paper_2411_09809_b200.configs import random_graph
+
+        ln, lm, lit = 20000, 40000, 10
+        ledges = random_graph(ln, lm, seed=1)
+        fr_layout(ledges, iterations=1, seed=1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fr_layout(ledges, iterations=lit, seed=1)
+        torch.cuda.synchronize()
+        lay_s = (time.perf_counter() - t0) / lit
+        layout = {"metric": "fr_layout repulsion pair terms/s (bit-exact with the reference)",
+                  "value": ln * ln / lay_s, "unit": "pairs/s",
+                  "ms_per_iteration": lay_s * 1e3,
+                  "config": {"vertices": ln, "edges": lm, "iterations": lit,
+                             "graph": "random_graph(20000, 40000, seed=1)"}}
+
     # ---- end-to-end through the public API with pinned host inputs ----
     xy_h = torch.from_numpy(g.xy).pin_memory()
     ed_h = torch.from_numpy(g.edges).pin_memory()
@@ -385,6 +406,7 @@ def main():
                                  "dense_units": M.occlusion_units(n),
                                  "note": "effective rate: same count, Morton order + "
                                          "candidate tile pairs (incl. plan build)"}},
+        "layout": layout,
         "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": peak_run,
                      "unit": "T lane-op/s (FP32 FFMA/FMUL on the FMA pipe)",
                      "frac": achieved / peak_run,
