@@ -209,6 +209,13 @@ int glr_fr_layout(double *d_pos, int64_t n, const int64_t *d_ei, const int64_t *
 
 /* ---- introspection (tests / bench) --------------------------------------- */
 
+/* Self-test of the repulsion kernel's branch-free division against
+ * __ddiv_rn on `samples` pseudo-random positive operand pairs (2^-60..2^60,
+ * plus near-midpoint quotients); *h_mismatches receives the number of
+ * differing results (synchronous). */
+int glr_selftest_division(uint64_t samples, uint64_t seed, uint64_t *h_mismatches,
+                          void *stream);
+
 /* Pair-kernel mode of the prepared records (synchronous: reads the records
  * header): 0 = general exact-comparison path (any input), 1 = FP64 float-view
  * sign path with adjacency correction, 2 = certified packed-FP32 filter with

@@ -100,3 +100,20 @@ def test_gpu_generate_layout_and_metrics(gpu):
     assert g1.xy.min() >= 0.0 and g1.xy.max() <= 10.0
     rand = generate_layout(edges, kind="random", seed=8, extent=10.0)
     assert edge_crossing(g1) < edge_crossing(rand)  # test_graphio.py:169-177
+
+
+@pytest.mark.gpu
+def test_gpu_branch_free_division_matches_ddiv_rn(gpu):
+    """The repulsion kernel's branch-free division equals __ddiv_rn (IEEE
+    round-to-nearest) on 2^28 operand pairs incl. near-midpoint quotients."""
+    import ctypes
+
+    import torch
+
+    from paper_2411_09809_b200 import _lib
+
+    bad = ctypes.c_uint64(0)
+    rc = _lib.lib().glr_selftest_division(1 << 28, 20241019, ctypes.byref(bad),
+                                          torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "glr_selftest_division")
+    assert bad.value == 0
