@@ -196,6 +196,19 @@ int glr_edge_length_variation(const double *d_xy, int64_t n,
 int glr_minimum_angle(const double *d_xy, int64_t n, const int64_t *d_edges,
                       int64_t m, double *d_out, void *stream);
 
+/* ---- strip-sweep approximations: enhanced.py:133-300, sweep.py:60-402 ---- */
+
+/* One orientation of the reference's strip sweep.
+ * d_bounds: the nstrips + 1 strip boundaries along the sweep axis, built as
+ * build_strips does (enhanced.py:155-167); axis 0 = vertical strips (x is
+ * the sweep axis), 1 = horizontal.  d_out[0] = the strip crossings (order
+ * inversions, exact), d_out[1] = the deviation sum |ideal - a_c| over them
+ * when with_angle (else 0).  Synchronous (the segment count sizes the
+ * scratch).  GLR_EINVARIANT if the two counting routes disagree. */
+int glr_strip_crossings(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                        const double *d_bounds, int64_t nstrips, int axis, int with_angle,
+                        double ideal, double *d_out, void *stream);
+
 /* ---- force-directed layout: graphio.py:151-197 --- */
 
 /* Runs `iterations` rounds of the reference's fr_layout on d_pos (n x 2

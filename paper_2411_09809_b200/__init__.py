@@ -5,6 +5,12 @@ The five metric functions keep the reference's signatures and outputs
 hand-written sm_100a kernels through the C ABI in include/glare_b200.h.
 """
 
+from .enhanced import (
+    crossing_angle_stats,
+    edge_crossing_angle_enhanced,
+    edge_crossing_enhanced,
+    node_occlusion_grid,
+)
 from .layout import fr_layout, generate_layout, random_layout
 from .metrics import (
     CrossingRecords,
@@ -31,6 +37,10 @@ from .model import (
 )
 
 __all__ = [
+    "crossing_angle_stats",
+    "edge_crossing_angle_enhanced",
+    "edge_crossing_enhanced",
+    "node_occlusion_grid",
     "fr_layout",
     "generate_layout",
     "random_layout",

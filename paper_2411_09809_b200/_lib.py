@@ -59,6 +59,9 @@ SIGNATURES = {
     ),
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_crossing_set_mode": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p]),
+    "glr_strip_crossings": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64,
+                                       _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int,
+                                       _c.c_double, _c.c_void_p, _c.c_void_p]),
     "glr_selftest_division": (_c.c_int, [_c.c_uint64, _c.c_uint64,
                                          _c.POINTER(_c.c_uint64), _c.c_void_p]),
     "glr_fr_layout": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p,

@@ -4,7 +4,8 @@ against the reference's own outputs by tests/test_oracle_golden.py and
 tests/test_configs_golden.py).  The reference is too slow at these sizes
 (C4 crossing ~20-30 min, C5 days).
 
-    python tests/golden/make_golden_oracle.py
+    python tests/golden/make_golden_oracle.py               # C4 all, C5 occlusion
+    python tests/golden/make_golden_oracle.py --c5-crossing # C5 E_c/E_ca (hours)
 """
 import json
 import os
@@ -19,7 +20,24 @@ from oracle import sweep as S  # noqa: E402
 from paper_2411_09809_b200 import configs  # noqa: E402
 
 
+def c5_crossing():
+    """Full C5 E_c / dev_sum with the C oracle on all host cores (~2 h on 8
+    cores); stored beside the C5 occlusion golden."""
+    path = os.path.join(HERE, "golden.json")
+    g, p = configs.config5()
+    c, d = S.crossing_scan(g.xy, g.edges, p["ideal"])
+    doc = json.load(open(path))
+    assert doc["configs"]["C5"]["fingerprint"] == configs.fingerprint(g)
+    doc["configs"]["C5"].update({"ec": c, "dev": d,
+                                 "eca": 1.0 if c == 0 else 1 - (d / p["ideal"]) / c,
+                                 "source_ec": "pinned oracle: oracle/sweep_oracle.c, all host threads"})
+    json.dump(doc, open(path, "w"), indent=1, sort_keys=True)
+    print(doc["configs"]["C5"])
+
+
 def main():
+    if "--c5-crossing" in sys.argv:
+        return c5_crossing()
     path = os.path.join(HERE, "golden.json")
     doc = json.load(open(path))
     g, p = configs.config4()
