@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .metrics import DeviceGraph, _ptr, _stream, node_occlusion
-from .model import InputError, LayoutGraph, ParameterError, check_ideal_angle
+from .model import InputError, ParameterError, check_ideal_angle
 
 STRIP_ORIENTATIONS = ("vertical", "horizontal", "both")
 
