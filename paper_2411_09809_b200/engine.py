@@ -34,8 +34,9 @@ from .model import (
     SchemaError,
 )
 
-MODES = ("b200",)
+MODES = ("b200", "b200-enhanced")
 _DEFAULT_METRICS = ("nc", "ma", "ml", "ec", "eca")
+_ENHANCED_METRICS = ("nc", "ec", "eca")  # engine.py:33
 
 
 @dataclass
@@ -71,10 +72,12 @@ class ReadabilityReport:
             raise SchemaError(f"report contains a non-finite value: {exc}") from exc
 
 
-def _normalize_metrics(metrics) -> tuple:
-    """engine.py:36-55 for the b200 mode (all five metrics available)."""
+def _normalize_metrics(metrics, mode: str = "b200") -> tuple:
+    """engine.py:36-55: all five metrics in b200 mode; b200-enhanced (the
+    reference's "enhanced" mode on the GPU) supports nc, ec, eca."""
+    enhanced = mode == "b200-enhanced"
     if metrics is None:
-        return _DEFAULT_METRICS
+        return _ENHANCED_METRICS if enhanced else _DEFAULT_METRICS
     seen = []
     for key in metrics:
         if key not in METRIC_FIELDS:
@@ -83,6 +86,10 @@ def _normalize_metrics(metrics) -> tuple:
             seen.append(key)
     if not seen:
         raise ParameterError("no metrics requested")
+    if enhanced:
+        bad = [k for k in seen if k not in _ENHANCED_METRICS]
+        if bad:
+            raise ParameterError(f"enhanced mode supports only {_ENHANCED_METRICS}, not {bad}")
     return tuple(seen)
 
 
@@ -132,6 +139,26 @@ class _Evaluator:
                 self._scan = (int(c), float(d))
         return self._scan
 
+    def enhanced_entry(self, key: str):
+        """engine.py:119-137 (the reference's "enhanced" mode) on the GPU."""
+        from . import enhanced as E
+
+        g, p = self.g, self.p
+        if key == "nc":
+            return lambda: (E.node_occlusion_grid(self.dg() if g.num_vertices >= 2 else g,
+                                                  p.radius), [])
+        if key == "ec":
+            return lambda: (E.edge_crossing_enhanced(g, p.strip_fraction, p.orientation), [])
+
+        def eca():
+            count, dev = E.crossing_angle_stats(g, p.strip_fraction, p.ideal_angle,
+                                                p.orientation)
+            if count == 0:
+                return 1.0, [WARN_NO_CROSSINGS]
+            return 1.0 - (dev / p.ideal_angle) / count, []
+
+        return eca
+
     def entry(self, key: str):
         g, p = self.g, self.p
         if key == "nc":
@@ -174,18 +201,42 @@ def evaluate(g, mode: str = "b200", params: MetricParams | None = None, metrics=
     mode = _check_mode(mode)
     params = params if params is not None else MetricParams()
     params.validate()
-    keys = _normalize_metrics(metrics)
+    keys = _normalize_metrics(metrics, mode)
     ev = _Evaluator(g, params, rank, world)
     report = ReadabilityReport(mode=mode, params=_params_echo(params, world))
     for key in keys:
         name = METRIC_FIELDS[key]
-        fn = ev.entry(key)
+        fn = ev.enhanced_entry(key) if mode == "b200-enhanced" else ev.entry(key)
         t0 = time.perf_counter()
         value, warns = fn()
         report.elapsed[name] = time.perf_counter() - t0
         setattr(report, name, value)
         report.warnings.extend(warns)
     return report
+
+
+def compare(g, params: MetricParams | None = None, metrics=None) -> list:
+    """Strip-sweep (b200-enhanced) vs exact (b200) values with percentage
+    errors, as the reference's compare (engine.py:163-200)."""
+    keys = _normalize_metrics(metrics if metrics is not None else _ENHANCED_METRICS,
+                              "b200-enhanced")
+    params = params if params is not None else MetricParams()
+    params.validate()
+    exact = evaluate(g, "b200", params, metrics=keys)
+    approx = evaluate(g, "b200-enhanced", params, metrics=keys)
+    rows = []
+    for key in keys:
+        name = METRIC_FIELDS[key]
+        o, e = getattr(exact, name), getattr(approx, name)
+        if o != 0:
+            pct, flagged = abs(e - o) / abs(o) * 100.0, False
+        elif e == 0:
+            pct, flagged = 0.0, False
+        else:
+            pct, flagged = None, True
+        rows.append({"metric": key, "oracle": o, "enhanced": e, "pct_error": pct,
+                     "flagged": flagged})
+    return rows
 
 
 def _values_match(a, b) -> bool:

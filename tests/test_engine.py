@@ -81,3 +81,41 @@ def test_bench_invariant_across_shards(gpu):
     assert by["ec"] == {4194903} and by["nc"] == {9588}
     assert len(rows) == 12
     assert all(math.isfinite(r["seconds"]) for r in rows)
+
+
+def test_enhanced_mode_metric_validation():
+    from paper_2411_09809_b200 import ParameterError
+    from paper_2411_09809_b200.engine import _normalize_metrics, evaluate
+
+    assert _normalize_metrics(None, "b200-enhanced") == ("nc", "ec", "eca")
+    with pytest.raises(ParameterError):
+        _normalize_metrics(["ma"], "b200-enhanced")
+    with pytest.raises(ParameterError):
+        evaluate(None, mode="enhanced")
+
+
+@pytest.mark.gpu
+def test_gpu_enhanced_mode_report_and_compare(gpu):
+    import math
+
+    import strip_cases
+    from paper_2411_09809_b200 import (MetricParams, crossing_angle_stats,
+                                       edge_crossing_enhanced, node_occlusion)
+    from paper_2411_09809_b200.engine import compare, evaluate
+    from paper_2411_09809_b200.model import LayoutGraph
+
+    ids, xy, pairs = strip_cases.GRAPHS["rg_80_300"]
+    g = LayoutGraph(ids, xy, pairs)
+    p = MetricParams(radius=0.5, ideal_angle=math.radians(70), strip_fraction=0.1,
+                     orientation="both")
+    rep = evaluate(g, "b200-enhanced", p)
+    assert rep.mode == "b200-enhanced"
+    assert rep.edge_crossing == edge_crossing_enhanced(g, 0.1, "both")
+    c, d = crossing_angle_stats(g, 0.1, p.ideal_angle, "both")
+    assert rep.edge_crossing_angle == pytest.approx(1.0 - (d / p.ideal_angle) / c, rel=1e-12)
+    assert rep.node_occlusion == node_occlusion(g, 0.5)
+    assert rep.minimum_angle is None
+    rows = compare(g, p)
+    assert [r["metric"] for r in rows] == ["nc", "ec", "eca"]
+    ec_row = rows[1]
+    assert ec_row["enhanced"] <= ec_row["oracle"] and not ec_row["flagged"]
