@@ -384,3 +384,46 @@ def fr_layout_positions(n: int, ei: np.ndarray, ej: np.ndarray, iterations: int,
     span = pos.max(axis=0) - lo
     span[span <= 0] = 1.0
     return (pos - lo) / span * extent
+
+
+# ---- strip sweeps -----------------------------------
+
+def strip_crossings(xy: np.ndarray, edges: np.ndarray, fraction: float, orientation: str,
+                    ideal=None):
+    """(strip crossings, deviation sum) of one orientation of the reference's
+    strip sweep (metrics/enhanced.py:133-215 strips, sweep.py:60-108 count,
+    sweep.py:110-402 deviation), restated by pair enumeration per strip:
+    a pair is counted when its l- and r-orders strictly disagree (the sweep's
+    tie rule) and contributes |ideal - a_c|.  O(S^2) per strip: small inputs.
+    """
+    if orientation == "horizontal":
+        axis_c, ord_c = xy[:, 1], xy[:, 0]
+    else:
+        axis_c, ord_c = xy[:, 0], xy[:, 1]
+    lo, hi = float(axis_c.min()), float(axis_c.max())
+    nstrips = math.ceil(1.0 / fraction)
+    width = (hi - lo) / nstrips
+    bounds = lo + np.arange(nstrips + 1) * width
+    bounds[-1] = hi
+    x0, y0 = axis_c[edges[:, 0]], ord_c[edges[:, 0]]
+    x1, y1 = axis_c[edges[:, 1]], ord_c[edges[:, 1]]
+    swap = x1 < x0
+    sx0, sy0 = np.where(swap, x1, x0), np.where(swap, y1, y0)
+    sx1, sy1 = np.where(swap, x0, x1), np.where(swap, y0, y1)
+    kf = np.searchsorted(bounds, sx0, side="left")
+    kl = np.searchsorted(bounds, sx1, side="right") - 1
+    total, dev = 0, 0.0
+    for k in range(nstrips):
+        sel = np.flatnonzero((kf <= k) & (k < kl))
+        if len(sel) < 2:
+            continue
+        slope = (sy1[sel] - sy0[sel]) / (sx1[sel] - sx0[sel])
+        lv = sy0[sel] + slope * (bounds[k] - sx0[sel])
+        rv = sy0[sel] + slope * (bounds[k + 1] - sx0[sel])
+        i, j = np.triu_indices(len(sel), 1)
+        inv = ((lv[i] < lv[j]) & (rv[i] > rv[j])) | ((lv[i] > lv[j]) & (rv[i] < rv[j]))
+        total += int(np.count_nonzero(inv))
+        if ideal is not None and inv.any():
+            th = axis_angles(sx0[sel], sy0[sel], sx1[sel], sy1[sel])
+            dev += float(np.sum(np.abs(ideal - crossing_angles(th[i[inv]], th[j[inv]]))))
+    return total, dev

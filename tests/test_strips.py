@@ -108,3 +108,56 @@ def test_gpu_strip_properties(gpu):
     assert edge_crossing_angle_enhanced(g, 0.25, IDEAL) == pytest.approx(
         edge_crossing_angle(g, IDEAL))
     assert edge_crossing_angle_enhanced(_graph("on_boundary"), 0.5, IDEAL) == 1.0
+
+
+@pytest.mark.parametrize("name", sorted(strip_cases.GRAPHS))
+def test_oracle_strip_restatement_matches_reference(strip_golden, name):
+    from oracle.glare_oracle import strip_crossings
+
+    g = _graph(name)
+    ideal = strip_golden["ideal"]
+    for row in strip_golden["cases"][name]:
+        frac, orient = row["fraction"], row["orientation"]
+        if orient == "both":
+            v = strip_crossings(g.xy, g.edges, frac, "vertical", ideal)
+            h = strip_crossings(g.xy, g.edges, frac, "horizontal", ideal)
+            got = v if v[0] >= h[0] else h
+        else:
+            got = strip_crossings(g.xy, g.edges, frac, orient, ideal)
+        assert got[0] == row["count"]
+        assert strict_close(got[1], row["dev"])
+
+
+@pytest.mark.gpu
+def test_gpu_strips_random_against_oracle(gpu):
+    """Random layouts (continuous and integer-lattice coordinates), random
+    fractions, both single orientations: GPU == oracle restatement."""
+    from oracle.glare_oracle import strip_crossings
+    from paper_2411_09809_b200 import crossing_angle_stats
+    from paper_2411_09809_b200.configs import random_graph
+    from paper_2411_09809_b200.model import LayoutGraph
+
+    rng = np.random.default_rng(11)
+    for trial in range(24):
+        n = int(rng.integers(8, 400))
+        m = min(int(rng.integers(n, 6 * n)), n * (n - 1) // 2)
+        e = random_graph(n, m, seed=trial)
+        ids = np.unique(e)
+        if trial % 3 == 0:
+            xy = rng.integers(0, 9, (len(ids), 2)).astype(np.float64)
+            keep = np.any(xy[np.searchsorted(ids, e[:, 0])] != xy[np.searchsorted(ids, e[:, 1])], 1)
+            e = e[keep]
+            if len(e) < 2:
+                continue
+            ids2 = np.unique(e)
+            xy = xy[np.searchsorted(ids, ids2)]
+            ids = ids2
+        else:
+            xy = rng.uniform(-5, 5, (len(ids), 2))
+        g = LayoutGraph(ids, xy, e)
+        frac = float(rng.uniform(0.01, 0.6))
+        for orient in ("vertical", "horizontal"):
+            c, d = crossing_angle_stats(g, frac, IDEAL, orient)
+            wc, wd = strip_crossings(g.xy, g.edges, frac, orient, IDEAL)
+            assert c == wc, (trial, orient)
+            assert strict_close(d, wd), (trial, orient, d, wd)
