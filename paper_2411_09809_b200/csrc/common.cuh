@@ -45,13 +45,33 @@ inline int check_cuda(cudaError_t e, const char *what) {
     if (_rc != GLR_OK) return _rc;                          \
   } while (0)
 
+// Keep freed stream-ordered scratch in the device's default pool instead of
+// returning it to the driver at every synchronisation (release threshold 0
+// by default), so repeated calls do not re-map hundreds of MB each time.
+// Only cudaMallocAsync users (this library) draw from this pool; torch's
+// caching allocator is separate.
+inline void retain_scratch_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 // RAII stream-ordered scratch allocation (cudaMallocAsync / cudaFreeAsync).
 struct Scratch {
   void *ptr = nullptr;
   cudaStream_t stream = nullptr;
   cudaError_t err = cudaSuccess;
   Scratch(size_t bytes, cudaStream_t s) : stream(s) {
-    if (bytes) err = cudaMallocAsync(&ptr, bytes, s);
+    if (bytes) {
+      retain_scratch_pool();
+      err = cudaMallocAsync(&ptr, bytes, s);
+    }
   }
   ~Scratch() {
     if (ptr) cudaFreeAsync(ptr, stream);
