@@ -849,6 +849,9 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
                                              const double *__restrict__ theta, int64_t ibase,
                                              int64_t jbase) {
   bool any = false;
+  double hf[kK];
+#pragma unroll
+  for (int k = 0; k < kK; ++k) hf[k] = 0.0;
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kK];
@@ -862,14 +865,17 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
         // dev += hit ? t : 0 as fma(t, {0.0 | 1.0}, dev): one DFMA and one SEL
         // (exact: fma(t, 1, dev) == dev + t, fma(t, 0, dev) == dev)
         const double t = angle_dev(R.th[k], thj, kappa);
-        int hw;
-        asm("{\n\t.reg .pred p;\n\t"
+        // hf[k] = {lo: 0 (carried), hi: hit ? 0x3ff00000 : 0}: only the high
+        // word is rewritten, so no zeroing MOV per pair
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
             "setp.lt.f32 p, %2, %3;\n\t"
             "@p add.u32 %0, %0, 1;\n\t"
-            "selp.b32 %1, 1072693248, 0, p;\n\t}"
-            : "+r"(cnt[k]), "=r"(hw)
+            "mov.b64 {lo, hi}, %1;\n\t"
+            "selp.b32 hi, 1072693248, 0, p;\n\t"
+            "mov.b64 %1, {lo, hi};\n\t}"
+            : "+r"(cnt[k]), "+d"(hf[k])
             : "f"(M[k]), "f"(-thr));
-        dev[k] = __fma_rn(t, __hiloint2double(hw, 0), dev[k]);
+        dev[k] = __fma_rn(t, hf[k], dev[k]);
       } else {
         asm("{\n\t.reg .pred p;\n\t"
             "setp.lt.f32 p, %1, %2;\n\t"
