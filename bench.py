@@ -10,7 +10,7 @@ occlusion), and the partials are combined with one allreduce (SURVEY.md
 8(e)); scaling is strong (fixed total work).
 
 Step = one fused E_c + E_ca pass (glr_crossing_pairs with the angle sum) over
-the whole C5 edge set, inputs resident in HBM (records ~390 MB > 126 MB L2,
+the whole C5 edge set, inputs resident in HBM (records ~660 MB > 126 MB L2,
 so no L2 flush is needed).  `value` = m(m-1)/2 algorithmic edge-pair tests per
 second over the K timed steps (max over ranks).  `e2e` = the same metric
 through the public API with host (pinned) inputs: H2D of xy+edges, prologue,
@@ -190,7 +190,7 @@ def _config_desc(g, p, world):
             "edge_pairs": int(g.num_edges) * (int(g.num_edges) - 1) // 2,
             "node_pairs": int(g.num_vertices) * (int(g.num_vertices) - 1) // 2,
             "ideal_deg": 70.0, "radius": p["radius"], "parallelism": f"units{world}",
-            "l2": "inputs (~390 MB records) exceed the 126 MB L2; no flush needed"}
+            "l2": "inputs (~660 MB records) exceed the 126 MB L2; no flush needed"}
 
 
 def main():
