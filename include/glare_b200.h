@@ -222,6 +222,11 @@ int glr_fr_layout(double *d_pos, int64_t n, const int64_t *d_ei, const int64_t *
 
 /* ---- introspection (tests / bench) --------------------------------------- */
 
+/* Enables (1, the default) or disables (0) the certified FP32 occlusion
+ * filter process-wide, for cross-checking it against the FP64 kernel; both
+ * give identical counts.  Returns the previous setting. */
+int glr_occlusion_set_filter(int enable);
+
 /* Self-test of the repulsion kernel's branch-free division against
  * __ddiv_rn on `samples` pseudo-random positive operand pairs (2^-60..2^60,
  * plus near-midpoint quotients); *h_mismatches receives the number of

@@ -59,6 +59,7 @@ SIGNATURES = {
     ),
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_crossing_set_mode": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p]),
+    "glr_occlusion_set_filter": (_c.c_int, [_c.c_int]),
     "glr_strip_crossings": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64,
                                        _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int,
                                        _c.c_double, _c.c_void_p, _c.c_void_p]),

@@ -47,10 +47,14 @@ __device__ inline void occ_row(const double (&xi)[kK], const double (&yi)[kK], d
   }
 }
 
+struct OccHeader;
+__device__ inline int occ_header_use(const void *h) { return *reinterpret_cast<const int *>(h); }
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 occlusion_pairs_kernel(const double2 *__restrict__ xy, int64_t n, const int2 *__restrict__ ulist,
                        uint64_t T, uint64_t ubeg, uint64_t uend, unsigned long long thr_bits,
-                       unsigned long long *__restrict__ cta_cnt) {
+                       const void *__restrict__ hdr, unsigned long long *__restrict__ cta_cnt) {
+  if (hdr != nullptr && occ_header_use(hdr)) return;  // the FP32 filter kernel runs instead
   // ulist == nullptr: units are the implicit upper triangle of tile pairs;
   // otherwise unit u is the explicit tile pair ulist[u] (culled candidates).
   __shared__ __align__(16) double2 sj[kTile];
@@ -95,6 +99,272 @@ occlusion_pairs_kernel(const double2 *__restrict__ xy, int64_t n, const int2 *__
     } else {
 #pragma unroll 4
       for (int jj = 0; jj < kTile; ++jj) occ_row<false>(xi, yi, sj[jj], jj, thr_bits, cnt);
+    }
+    unsigned c = 0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) c += cnt[k];
+    total += c;
+    if (ulist == nullptr && ++tj == T) { ++ti; tj = ti; }
+  }
+  unsigned long long bc = block_sum_u64<kThreads>(total, red);
+  if (threadIdx.x == 0) cta_cnt[blockIdx.x] = bc;
+}
+
+// ---- certified FP32 filter (the default when the input admits it) --------
+//
+// Coordinates translated to their bounding-box corner and scaled by a power
+// of two into [0, 1/2] (X = RN32((x - x0) sc)); per pair S = RN(RN(dX dX) +
+// dY dY) with dX = RN32(Xi - Xj) (FADD2/FMUL2/FFMA2 over two i-vertices).
+// |S - sc^2 d^2| <= E(S) = 3 2^-25 sqrt(2.01 S) + 2^-21 S + 2^-48 (quantisation
+// 2^-26 per coordinate, the subtraction, the two roundings, the reference's
+// own FP64 rounding), so with T = sc^2 thr:
+//   S < T_lo = RD32(T - E(T))       certainly occluding (s_fp64 < thr),
+//   S > T_hi = RU32(T + E(4T))      certainly not,
+// and pairs in [T_lo, T_hi] -- exact ties included -- are re-tested in FP64.
+// Admissible when every coordinate is finite with magnitude <= 2^500, the
+// extent W in [2^-400, 2^500] and T in [1e-14, 1e30]; otherwise the FP64
+// kernel runs (both are launched; the header decides on the device).
+struct OccHeader {
+  int use;
+  int pad;
+  double x0, y0, sc;
+  float tlo, thi, tmid, thw;
+};
+
+__global__ void __launch_bounds__(1024)
+occ_header_kernel(const double2 *__restrict__ xy, int64_t n, double thr, OccHeader *h) {
+  __shared__ double red[5][32];
+  __shared__ int bad_any;
+  if (threadIdx.x == 0) bad_any = 0;
+  __syncthreads();
+  double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY, amax = 0.0;
+  int bad = 0;
+  for (int64_t v = threadIdx.x; v < n; v += blockDim.x) {
+    const double2 p = xy[v];
+    if (!isfinite(p.x) || !isfinite(p.y)) bad = 1;
+    x0 = fmin(x0, p.x); x1 = fmax(x1, p.x);
+    y0 = fmin(y0, p.y); y1 = fmax(y1, p.y);
+    amax = fmax(amax, fmax(fabs(p.x), fabs(p.y)));
+  }
+  if (bad) bad_any = 1;
+  for (int o = 16; o > 0; o >>= 1) {
+    x0 = fmin(x0, __shfl_down_sync(0xffffffffu, x0, o));
+    x1 = fmax(x1, __shfl_down_sync(0xffffffffu, x1, o));
+    y0 = fmin(y0, __shfl_down_sync(0xffffffffu, y0, o));
+    y1 = fmax(y1, __shfl_down_sync(0xffffffffu, y1, o));
+    amax = fmax(amax, __shfl_down_sync(0xffffffffu, amax, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = x0; red[1][w] = x1; red[2][w] = y0; red[3][w] = y1; red[4][w] = amax;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+    x0 = fmin(x0, red[0][i]); x1 = fmax(x1, red[1][i]);
+    y0 = fmin(y0, red[2][i]); y1 = fmax(y1, red[3][i]);
+    amax = fmax(amax, red[4][i]);
+  }
+  OccHeader H;
+  H.use = 0;
+  H.pad = 0;
+  H.x0 = x0;
+  H.y0 = y0;
+  H.sc = 1.0;
+  H.tlo = H.thi = H.tmid = H.thw = 0.0f;
+  const double W = fmax(__dsub_ru(x1, x0), __dsub_ru(y1, y0));
+  if (!bad_any && amax <= 0x1p500 && W >= 0x1p-400 && W <= 0x1p500 && thr >= 0x1p-600) {
+    const double sc = ldexp(1.0, -(ilogb(W) + 2));
+    const double T = thr * sc * sc;  // exact: sc is a power of two, no over/underflow here
+    if (T >= 1e-14 && T <= 1e30) {
+      auto E = [](double S) { return 3.0 * 0x1p-25 * sqrt(2.01 * S) + 0x1p-21 * S + 0x1p-48; };
+      const float tlo = __double2float_rd(T - E(T));
+      const float thi = __double2float_ru(T + E(4.0 * T));
+      H.use = 1;
+      H.sc = sc;
+      H.tlo = tlo;
+      H.thi = thi;
+      // uncertain band [tlo, thi] as |S - tmid| <= thw, widened by rounding
+      H.tmid = __double2float_rn(0.5 * ((double)tlo + (double)thi));
+      H.thw = __double2float_ru(0.5 * ((double)thi - (double)tlo) * (1.0 + 0x1p-20) +
+                                0x1p-100);
+    }
+  }
+  *h = H;
+}
+
+__global__ void occ_scale_kernel(const double2 *__restrict__ xy, int64_t n,
+                                 const OccHeader *__restrict__ h, float2 *__restrict__ sxy) {
+  if (!h->use) return;
+  const double x0 = h->x0, y0 = h->y0, sc = h->sc;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = xy[v];
+    sxy[v] = make_float2(__double2float_rn(__dmul_rn(__dsub_rn(p.x, x0), sc)),
+                         __double2float_rn(__dmul_rn(__dsub_rn(p.y, y0), sc)));
+  }
+}
+
+__device__ __forceinline__ uint64_t o2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float o2_lo(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float o2_hi(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ uint64_t o2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t o2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t o2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+constexpr int kOccFBlock = 4;  // j-vertices per filter block (one warp vote)
+
+// S of one j against the thread's K i-vertices; masked diagonal pairs -> +inf
+template <bool DIAG>
+__device__ __forceinline__ void occ_s(const uint64_t (&X)[kK / 2], const uint64_t (&Y)[kK / 2],
+                                      float2 pj, int jj, float (&S)[kK]) {
+  const uint64_t XJ = o2_pack(pj.x, pj.x), YJ = o2_pack(pj.y, pj.y);
+#pragma unroll
+  for (int g = 0; g < kK / 2; ++g) {
+    const uint64_t dx = o2_sub(XJ, X[g]), dy = o2_sub(YJ, Y[g]);
+    const uint64_t s = o2_fma(dy, dy, o2_mul(dx, dx));
+    S[2 * g] = o2_lo(s);
+    S[2 * g + 1] = o2_hi(s);
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int k = 0; k < kK; ++k)
+      if (!(jj > (int)threadIdx.x + k * kThreads)) S[k] = INFINITY;
+  }
+}
+
+template <bool DIAG>
+__device__ __forceinline__ void occ_filter_block(const uint64_t (&X)[kK / 2],
+                                                 const uint64_t (&Y)[kK / 2], const float2 *sj,
+                                                 int jj0, const OccHeader &H, uint64_t NTLO2,
+                                                 uint64_t NHALF2, float vote_w,
+                                                 const double2 *__restrict__ xy, int64_t ibase,
+                                                 int64_t jbase, int64_t n,
+                                                 unsigned long long thr_bits,
+                                                 unsigned (&cnt)[kK]) {
+  float m = INFINITY;  // min over the block of |(S - tlo) - halfwidth|
+#pragma unroll
+  for (int q = 0; q < kOccFBlock; ++q) {
+    float S[kK];
+    occ_s<DIAG>(X, Y, sj[jj0 + q], jj0 + q, S);
+#pragma unroll
+    for (int g = 0; g < kK / 2; ++g) {
+      // d = S - tlo (packed): S < tlo exactly when d's sign bit is set (RN
+      // keeps the sign of the difference; d is +0 when S == tlo)
+      const uint64_t d = o2_sub(o2_pack(S[2 * g], S[2 * g + 1]), NTLO2);
+      cnt[2 * g] += __float_as_uint(o2_lo(d)) >> 31;
+      cnt[2 * g + 1] += __float_as_uint(o2_hi(d)) >> 31;
+      // uncertain band [tlo, thi] <=> d in [0, thi - tlo] <=> |d - half| <= half
+      const uint64_t e = o2_sub(d, NHALF2);
+      m = fminf(m, fminf(fabsf(o2_lo(e)), fabsf(o2_hi(e))));
+    }
+  }
+  if (__any_sync(0xffffffffu, m <= vote_w)) {
+#pragma unroll 1
+    for (int q = 0; q < kOccFBlock; ++q) {
+      float S[kK];
+      occ_s<DIAG>(X, Y, sj[jj0 + q], jj0 + q, S);
+      const int64_t vj = jbase + jj0 + q;
+#pragma unroll
+      for (int k = 0; k < kK; ++k) {
+        if (S[k] >= H.tlo && S[k] <= H.thi) {  // uncertain: the reference's FP64 test
+          const int64_t vi = ibase + threadIdx.x + k * kThreads;
+          if (vi < n && vj < n) {
+            const double2 a = xy[vi], b = xy[vj];
+            const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y);
+            const double s = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            if ((unsigned long long)__double_as_longlong(s) < thr_bits) cnt[k] += 1u;
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict__ sxy,
+                        const OccHeader *__restrict__ hdr, int64_t n,
+                        const int2 *__restrict__ ulist, uint64_t T, uint64_t ubeg, uint64_t uend,
+                        unsigned long long thr_bits, unsigned long long *__restrict__ cta_cnt) {
+  if (!hdr->use) return;
+  const OccHeader H = *hdr;
+  // packed constants: tlo, and half the band width (rounded up); the vote
+  // threshold is widened further so rounding of d - half never hides a pair
+  const float half = __fmul_ru(__fsub_ru(H.thi, H.tlo), 0.5f);
+  const uint64_t NTLO2 = o2_pack(H.tlo, H.tlo), NHALF2 = o2_pack(half, half);
+  const float vote_w = __fadd_ru(__fmul_ru(half, 1.0f + 0x1p-20f), 0x1p-120f);
+  __shared__ __align__(16) float2 sj[kTile];
+  __shared__ unsigned long long red[kThreads / 32];
+  const uint64_t span = uend - ubeg;
+  const uint64_t b = ubeg + span * blockIdx.x / gridDim.x;
+  const uint64_t e = ubeg + span * (blockIdx.x + 1) / gridDim.x;
+  // pads: i side +3e38, j side -3e38: differences overflow to +-inf, S = inf
+  const float PADF = 3.0e38f;
+  unsigned long long total = 0;
+  uint64_t X[kK / 2], Y[kK / 2];
+  uint64_t ti = 0, tj = 0, cur = ~0ull;
+  if (b < e && ulist == nullptr) tri_unit_coords(b, T, &ti, &tj);
+  for (uint64_t u = b; u < e; ++u) {
+    if (ulist != nullptr) {
+      const int2 p = ulist[u];
+      ti = (uint64_t)p.x;
+      tj = (uint64_t)p.y;
+    }
+    if (ti != cur) {
+#pragma unroll
+      for (int g = 0; g < kK / 2; ++g) {
+        const int64_t v0 = (int64_t)ti * kTile + threadIdx.x + (2 * g) * kThreads;
+        const int64_t v1 = v0 + kThreads;
+        const float2 p0 = v0 < n ? sxy[v0] : make_float2(PADF, PADF);
+        const float2 p1 = v1 < n ? sxy[v1] : make_float2(PADF, PADF);
+        X[g] = o2_pack(p0.x, p1.x);
+        Y[g] = o2_pack(p0.y, p1.y);
+      }
+      cur = ti;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < kTile; q += kThreads) {
+      const int64_t v = (int64_t)tj * kTile + q;
+      sj[q] = v < n ? sxy[v] : make_float2(-PADF, -PADF);
+    }
+    __syncthreads();
+    unsigned cnt[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) cnt[k] = 0;
+    const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
+    if (ti == tj) {
+      for (int jj = 0; jj < kTile; jj += kOccFBlock)
+        occ_filter_block<true>(X, Y, sj, jj, H, NTLO2, NHALF2, vote_w, xy, ibase, jbase, n,
+                               thr_bits, cnt);
+    } else {
+#pragma unroll 1
+      for (int jj = 0; jj < kTile; jj += kOccFBlock)
+        occ_filter_block<false>(X, Y, sj, jj, H, NTLO2, NHALF2, vote_w, xy, ibase, jbase, n,
+                                thr_bits, cnt);
     }
     unsigned c = 0;
 #pragma unroll
@@ -176,6 +446,9 @@ __global__ void vtile_pairs_kernel(const double4 *__restrict__ box, int64_t T, d
   }
 }
 
+// process-wide switch for cross-checks (glr_occlusion_set_filter)
+int g_occ_filter = 1;
+
 int occ_blocks(int64_t work) {
   int64_t b = (work + 127) / 128;
   const int64_t cap = (int64_t)sm_count() * 16;
@@ -186,6 +459,7 @@ int occ_blocks(int64_t work) {
 int occlusion_run(const double *d_xy, int64_t n, double thr, const int2 *d_list,
                   uint64_t list_len, uint64_t ubeg, uint64_t uend, double *d_out,
                   cudaStream_t st, const char *who) {
+  const bool use_filter = g_occ_filter != 0;
   if (d_out == nullptr || n < 0 || (n > 0 && d_xy == nullptr)) {
     set_error("%s: invalid arguments", who);
     return GLR_EARG;
@@ -204,13 +478,28 @@ int occlusion_run(const double *d_xy, int64_t n, double thr, const int2 *d_list,
   uint64_t g = (uint64_t)sm_count() * kMinBlocks;
   if (uend - ubeg < g) g = uend - ubeg;
   const int grid = (int)g;
-  Scratch scr((size_t)grid * sizeof(unsigned long long), st);
+  const size_t a_cta = ((size_t)grid * sizeof(unsigned long long) + 255) & ~(size_t)255;
+  const size_t a_hdr = 256;
+  const size_t a_sxy = ((size_t)n * sizeof(float2) + 255) & ~(size_t)255;
+  Scratch scr(a_cta + a_hdr + (use_filter ? a_sxy : 0), st);
   GLR_CUDA(scr.err);
+  unsigned long long *cta = scr.as<unsigned long long>();
+  OccHeader *hdr = reinterpret_cast<OccHeader *>(scr.as<char>() + a_cta);
+  float2 *sxy = reinterpret_cast<float2 *>(scr.as<char>() + a_cta + a_hdr);
   unsigned long long thr_bits;
   memcpy(&thr_bits, &thr, sizeof(thr));
-  occlusion_pairs_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n,
-                                                    d_list, T, ubeg, uend, thr_bits,
-                                                    scr.as<unsigned long long>());
+  const double2 *xy = reinterpret_cast<const double2 *>(d_xy);
+  if (use_filter) {
+    occ_header_kernel<<<1, 1024, 0, st>>>(xy, n, thr, hdr);
+    GLR_LAUNCHED("occ_header_kernel");
+    occ_scale_kernel<<<occ_blocks(n), 128, 0, st>>>(xy, n, hdr, sxy);
+    GLR_LAUNCHED("occ_scale_kernel");
+    occlusion_filter_kernel<<<grid, kThreads, 0, st>>>(xy, sxy, hdr, n, d_list, T, ubeg, uend,
+                                                       thr_bits, cta);
+    GLR_LAUNCHED("occlusion_filter_kernel");
+  }
+  occlusion_pairs_kernel<<<grid, kThreads, 0, st>>>(xy, n, d_list, T, ubeg, uend, thr_bits,
+                                                    use_filter ? hdr : nullptr, cta);
   GLR_LAUNCHED("occlusion_pairs_kernel");
   occ_finalize_kernel<<<1, 32, 0, st>>>(scr.as<unsigned long long>(), grid, d_out);
   GLR_LAUNCHED("occ_finalize_kernel");
@@ -221,6 +510,12 @@ int occlusion_run(const double *d_xy, int64_t n, double thr, const int2 *d_list,
 }  // namespace glr
 
 extern "C" {
+
+int glr_occlusion_set_filter(int enable) {
+  const int prev = glr::g_occ_filter;
+  glr::g_occ_filter = enable ? 1 : 0;
+  return prev;
+}
 
 int glr_occlusion_tile(void) { return glr::kTile; }
 
