@@ -41,7 +41,8 @@ enum {
   GLR_OK = 0,
   GLR_EARG = 1,       /* invalid argument (ParameterError / InputError side) */
   GLR_ECUDA = 2,      /* CUDA runtime error */
-  GLR_EINVARIANT = 4  /* internal consistency check failed (InvariantError) */
+  GLR_EINVARIANT = 4, /* internal consistency check failed (InvariantError) */
+  GLR_EFALLBACK = 8   /* loaders: the text needs the Python parser (not an error) */
 };
 
 /* ABI version: (major << 16) | minor. */
@@ -219,6 +220,22 @@ int glr_strip_crossings(const double *d_xy, int64_t n, const int64_t *d_edges, i
  * sums, np.add.at order of the spring pulls). */
 int glr_fr_layout(double *d_pos, int64_t n, const int64_t *d_ei, const int64_t *d_ej,
                   int64_t m, int iterations, double extent, void *stream);
+
+/* ---- native loaders: graphio.py:46-117 ----------- */
+
+/* Parses a SNAP-style edge list held in memory (graphio.parse_edgelist
+ * before normalisation): *count = the number of id pairs; the first `cap`
+ * are written to out (2 int64 each); call with out = NULL to size.
+ * GLR_EFALLBACK when the text uses anything beyond plain ASCII decimal ids
+ * on '\n'-separated lines (the caller then applies the reference's rules). */
+int glr_parse_edgelist(const char *buf, size_t len, int64_t *out, int64_t cap,
+                       int64_t *count);
+
+/* Parses an "id,x,y" layout CSV held in memory (graphio.read_layout): ids
+ * and row-major xy of the first `cap` rows, *count = number of rows.
+ * GLR_EFALLBACK as above (also for non-finite values and an empty file). */
+int glr_parse_layout(const char *buf, size_t len, int64_t *ids, double *xy, int64_t cap,
+                     int64_t *count);
 
 /* ---- introspection (tests / bench) --------------------------------------- */
 

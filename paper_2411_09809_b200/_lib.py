@@ -19,6 +19,7 @@ GLR_OK = 0
 GLR_EARG = 1
 GLR_ECUDA = 2
 GLR_EINVARIANT = 4
+GLR_EFALLBACK = 8
 
 # (name, restype, argtypes) for every symbol include/glare_b200.h declares.
 _c = ctypes
@@ -60,6 +61,10 @@ SIGNATURES = {
     "glr_crossing_fast_path": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
     "glr_crossing_set_mode": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p]),
     "glr_occlusion_set_filter": (_c.c_int, [_c.c_int]),
+    "glr_parse_edgelist": (_c.c_int, [_c.c_char_p, _c.c_size_t, _c.c_void_p, _c.c_int64,
+                                      _c.POINTER(_c.c_int64)]),
+    "glr_parse_layout": (_c.c_int, [_c.c_char_p, _c.c_size_t, _c.c_void_p, _c.c_void_p,
+                                    _c.c_int64, _c.POINTER(_c.c_int64)]),
     "glr_strip_crossings": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64,
                                        _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int,
                                        _c.c_double, _c.c_void_p, _c.c_void_p]),
@@ -121,6 +126,20 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     return h
+
+
+_host_handle = None
+
+
+def host_lib() -> ctypes.CDLL:
+    """The library for its host-only entry points (the native loaders): no
+    CUDA device needed."""
+    global _host_handle
+    if _host_handle is None:
+        with _lock:
+            if _host_handle is None:
+                _host_handle = load_library(os.environ.get("GLARE_B200_LIB") or LIB_PATH)
+    return _host_handle
 
 
 def lib() -> ctypes.CDLL:
