@@ -82,13 +82,14 @@ constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bou
 #define GLR_XFBLOCK 4
 #endif
 constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp vote each)
-// CTAs per SM of the filter kernel (5 -> <= 102 registers, 6 -> <= 85):
-// tools/variant_bench.py on a C5-shaped graph, profiles/r01_variants_filter.txt
+// CTAs per SM of the filter kernel (fused 4 -> <= 128 registers, count-only
+// 5 -> <= 102, with kFK = 4):
+// tools/c5_time.py and tools/config_bench.py, profiles/r01_variants_filter.txt
 #ifndef GLR_XFMINB_A
-#define GLR_XFMINB_A 5
+#define GLR_XFMINB_A 4
 #endif
 #ifndef GLR_XFMINB_C
-#define GLR_XFMINB_C 6
+#define GLR_XFMINB_C 5
 #endif
 constexpr int kFilterMinBlocksAngle = GLR_XFMINB_A;
 #ifndef GLR_XFSTAGES
@@ -146,13 +147,27 @@ constexpr int kModeFastDefault = kModeFilter;
 // magnitude certifies both factors' signs.
 enum FField { kFAx, kFAy, kFBx, kFBy, kFSabx, kFNsaby, kFNska, kFFields };
 
+// Filter kernel work split: a unit's i-tile is cut into slices of 32 lanes
+// x kFK i-edges (a warp's work item); lane l, i-edge k of slice s is tile
+// slot s*32*kFK + 32k + l, and i-edges (2g, 2g+1) share packed registers.
+#ifndef GLR_XFK
+#define GLR_XFK 4
+#endif
+constexpr int kFK = GLR_XFK;             // i-edges per lane in the filter kernel
+constexpr int kFGroups = kFK / 2;        // packed i-edge pairs per lane
+constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
+static_assert(kFK % 2 == 0 && kFK <= 4 && kTile % (32 * kFK) == 0, "filter slice shape");
+
+__host__ __device__ inline int fslot(int slice, int k, int lane) {
+  return slice * 32 * kFK + 32 * k + lane;
+}
+
 // In HBM the filter records of a tile are stored field-major and paired the
-// way the kernel packs its i-edges: v[f][g][p] = (field f of tile slot
-// 2g*kThreads + p, of slot (2g+1)*kThreads + p), so each packed i-register
-// pair is one 64-bit load.
-constexpr int kFGroups = GLR_XK / 2;
+// way the kernel packs its i-edges: v[f][P], P = (s*kFGroups + g)*32 + l,
+// holds (field f of slot fslot(s, 2g, l), of slot fslot(s, 2g+1, l)), so
+// each packed i-register pair is one 64-bit load.
 struct __align__(16) FTile {
-  float2 v[kFFields][kFGroups][kThreads];
+  float2 v[kFFields][kTile / 2];
   double theta[kTile];
 };
 static_assert(sizeof(FTile) == (size_t)kTile * 36, "FTile must be 36 B per edge");
@@ -407,9 +422,10 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
     }
     FTile &t = rv.ftile[e / kTile];
     const int slot = (int)(e % kTile);
-    const int g = slot / (2 * kThreads), h = (slot / kThreads) & 1, q = slot % kThreads;
+    const int sl = slot / (32 * kFK), kk = (slot % (32 * kFK)) / 32, ln = slot % 32;
+    const int P = (sl * kFGroups + kk / 2) * 32 + ln, h = kk & 1;
 #pragma unroll
-    for (int k = 0; k < kFFields; ++k) reinterpret_cast<float *>(&t.v[k][g][q])[h] = f[k];
+    for (int k = 0; k < kFFields; ++k) reinterpret_cast<float *>(&t.v[k][P])[h] = f[k];
     t.theta[slot] = theta;
     JRec j;
     j.c = make_float4(f[kFAx], f[kFAy], f[kFBx], f[kFBy]);
@@ -725,26 +741,25 @@ __device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
   return r;
 }
 
-constexpr int kGroups = kK / 2;  // packed i-edge pairs per thread
-static_assert(kK % 2 == 0, "the filter packs i-edges in pairs");
+constexpr int kGroups = kFGroups;  // packed i-edge pairs per lane
 
 struct FIRegs {
   uint64_t ax[kGroups], ay[kGroups], bx[kGroups], by[kGroups];
   uint64_t sabx[kGroups], nsaby[kGroups], nska[kGroups];
-  double th[kK];
+  double th[kFK];
 };
 
-// i-edge k of group g is tile slot islot + (2g + h) * kThreads, h = 0/1 in
-// the low/high half of the packed registers (one 64-bit load each); islot
-// in [0, kThreads) is the thread's slot within its i-tile slice.
+// Lane `lane` of slice `slice`: i-edge k is tile slot fslot(slice, k, lane);
+// group g holds k = 2g (low half) and 2g + 1 (high half), one 64-bit load.
 template <bool ANGLE>
 __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint64_t ti,
-                               int islot) {
+                               int slice, int lane) {
   const FTile &t = ftile[ti];
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][g][islot]);
-    constexpr int kField = kFGroups * kThreads;  // uint64 stride between fields
+    const int P = (slice * kFGroups + g) * 32 + lane;
+    const uint64_t *v = reinterpret_cast<const uint64_t *>(&t.v[0][P]);
+    constexpr int kField = kTile / 2;  // uint64 stride between fields
     R.ax[g] = v[kFAx * kField];
     R.ay[g] = v[kFAy * kField];
     R.bx[g] = v[kFBx * kField];
@@ -752,8 +767,8 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
     R.sabx[g] = v[kFSabx * kField];
     R.nsaby[g] = v[kFNsaby * kField];
     R.nska[g] = v[kFNska * kField];
-    R.th[2 * g] = ANGLE ? t.theta[islot + (2 * g) * kThreads] : 0.0;
-    R.th[2 * g + 1] = ANGLE ? t.theta[islot + (2 * g + 1) * kThreads] : 0.0;
+    R.th[2 * g] = ANGLE ? t.theta[fslot(slice, 2 * g, lane)] : 0.0;
+    R.th[2 * g + 1] = ANGLE ? t.theta[fslot(slice, 2 * g + 1, lane)] : 0.0;
   }
 }
 
@@ -810,7 +825,7 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
 
 template <bool DIAG>
 __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj, int islot,
-                                         float (&M)[kK]) {
+                                         float (&M)[kFK]) {
   const float4 q0 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec));       // cx cy dx dy
   const float4 q1 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec) + 16);  // scdx -scdy -skc
   const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
@@ -829,8 +844,8 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
   }
   if (DIAG) {
 #pragma unroll
-    for (int k = 0; k < kK; ++k)
-      if (!(jj > islot + k * kThreads)) M[k] = 2.0f;
+    for (int k = 0; k < kFK; ++k)
+      if (!(jj > islot + 32 * k)) M[k] = 2.0f;
   }
 }
 
@@ -843,22 +858,22 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 template <bool ANGLE, bool DIAG, int NJ>
 __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
                                              unsigned thaddr, int jj0, int islot, float thr,
-                                             unsigned (&cnt)[kK], double (&dev)[kK],
+                                             unsigned (&cnt)[kFK], double (&dev)[kFK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
                                              int64_t jbase) {
   bool any = false;
-  double hf[kK];
+  double hf[kFK];
 #pragma unroll
-  for (int k = 0; k < kK; ++k) hf[k] = 0.0;
+  for (int k = 0; k < kFK; ++k) hf[k] = 0.0;
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
-    float M[kK];
+    float M[kFK];
     filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
+    for (int k = 0; k < kFK; ++k) {
       any |= fabsf(M[k]) <= thr;
       // @(M < -1) cnt += 1 (and dev += t)
       if (ANGLE) {
@@ -888,12 +903,12 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
   if (__any_sync(0xffffffffu, any)) {
 #pragma unroll 1
     for (int q = 0; q < NJ; ++q) {
-      float M[kK];
+      float M[kFK];
       filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
 #pragma unroll
-      for (int k = 0; k < kK; ++k) {
+      for (int k = 0; k < kFK; ++k) {
         if (fabsf(M[k]) <= thr) {
-          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + islot + k * kThreads,
+          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + islot + 32 * k,
                                              jbase + jj0 + q, kappa);
           if (t >= 0.0) {
             cnt[k] += 1u;
@@ -1065,7 +1080,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 // chunk ownership as cross_pairs_kernel.  The j-tile records (8 KB, + 2 KB
 // of theta) of the CTA's next kStages units sit in a ring of shared-memory
 // stages filled by TMA bulk copies.  Work is handed out in SLICES: a unit's
-// i-tile is cut into kWarps slices of 32 lanes x K i-edges, and each warp
+// i-tile is cut into kFSlices slices of 32 lanes x kFK i-edges, and each warp
 // takes the CTA's next slice from a shared counter, so fast warps simply do
 // more slices -- warps never wait for each other (a per-unit CTA barrier,
 // or a ring where the slowest warp gates the refills, cost 10-19%: warps of
@@ -1109,6 +1124,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
   constexpr int kWarps = kThreads / 32;
+  static_assert(kFSlices >= 1, "at least one slice per unit");
   __shared__ __align__(128) JRec sj[kStages][kTile];
   __shared__ __align__(128) double sth[kStages][ANGLE ? kTile : 2];
   __shared__ __align__(8) uint64_t full[kStages];
@@ -1153,13 +1169,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     unsigned q = 0;
     if (lane == 0) q = atomicAdd(&next_slice, 1u);
     q = __shfl_sync(0xffffffffu, q, 0);
-    const uint64_t uq = q / kWarps;
-    const int slice = (int)(q % kWarps);
+    const uint64_t uq = q / kFSlices;
+    const int slice = (int)(q % kFSlices);
     uint64_t ti, tj;
     if (!cu.at(uq, &ti, &tj)) break;
-    const int islot = slice * 32 + (int)lane;
+    const int islot = fslot(slice, 0, (int)lane);  // slot of i-edge k: islot + 32 k
     if (ti != cur_ti || slice != cur_slice) {
-      load_fi<ANGLE>(R, ftile, ti, islot);
+      load_fi<ANGLE>(R, ftile, ti, slice, (int)lane);
       cur_ti = ti;
       cur_slice = slice;
     }
@@ -1167,15 +1183,15 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     const unsigned use = (unsigned)(uq / kStages);
     // the stage's previous unit must be fully released (its refill issued)
     // before its mbarrier phase parity identifies this use unambiguously
-    while (*(volatile unsigned *)&done[stage] < use * kWarps) {
+    while (*(volatile unsigned *)&done[stage] < use * kFSlices) {
     }
     mbar_wait(&full[stage], use & 1u);  // this unit's j-tile has landed
     const unsigned jr = smem_u32(sj[stage]);
     const unsigned jth = smem_u32(sth[stage]);
-    unsigned cnt[kK];
-    double dev[kK];
+    unsigned cnt[kFK];
+    double dev[kFK];
 #pragma unroll
-    for (int k = 0; k < kK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+    for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     const float thr = unit_threshold(tbox[ti], tbox[tj]);
     if (ti == tj) {
@@ -1193,7 +1209,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     if (lane == 0) {
       __threadfence_block();
       const unsigned old = atomicAdd(&done[stage], 1u);
-      if (old + 1 == (use + 1) * kWarps) {
+      if (old + 1 == (use + 1) * kFSlices) {
         uint64_t a, b;
         if (cu.at(uq + kStages, &a, &b)) {
           __threadfence_block();
@@ -1205,9 +1221,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     unsigned c = 0;
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < kK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
+    for (int k = 0; k < kFK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
     total += c;
-    if (ANGLE) {  // s <= 2 * kTile * pi/2 < 2^10: s * 2^50 < 2^60
+    if (ANGLE) {  // s <= kFK * kTile * pi/2 < 2^11 (kFK <= 4): s * 2^50 < 2^61
       const unsigned long long f = (unsigned long long)__double2ll_rn(s * kDevScale);
       dlo += f;
       dhi += dlo < f ? 1ull : 0ull;
