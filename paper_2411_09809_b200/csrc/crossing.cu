@@ -82,6 +82,10 @@ constexpr int kMaxChunk = GLR_XCHUNK;  // units per round-robin chunk (upper bou
 #define GLR_XFBLOCK 4
 #endif
 constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp vote each)
+#ifndef GLR_XFBLOCK_C
+#define GLR_XFBLOCK_C 2
+#endif
+constexpr int kFilterBlockCount = GLR_XFBLOCK_C;  // same for the count-only kernel
 // CTAs per SM of the filter kernel (fused 4 -> <= 128 registers, count-only
 // 5 -> <= 102, with kFK = 4):
 // tools/c5_time.py and tools/config_bench.py, profiles/r01_variants_filter.txt
@@ -1124,6 +1128,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
   constexpr int kWarps = kThreads / 32;
+  constexpr int kNJ = ANGLE ? kFilterBlock : kFilterBlockCount;
   static_assert(kFSlices >= 1, "at least one slice per unit");
   __shared__ __align__(128) JRec sj[kStages][kTile];
   __shared__ __align__(128) double sth[kStages][ANGLE ? kTile : 2];
@@ -1195,13 +1200,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     const float thr = unit_threshold(tbox[ti], tbox[tj]);
     if (ti == tj) {
-      for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, true, kFilterBlock>(R, jr, jth, jj, islot, thr, cnt, dev, kappa, rec,
+      for (int jj = 0; jj < kTile; jj += kNJ)
+        filter_block<ANGLE, true, kNJ>(R, jr, jth, jj, islot, thr, cnt, dev, kappa, rec,
                                                 ids, theta, ibase, jbase);
     } else {
 #pragma unroll 1
-      for (int jj = 0; jj < kTile; jj += kFilterBlock)
-        filter_block<ANGLE, false, kFilterBlock>(R, jr, jth, jj, islot, thr, cnt, dev, kappa,
+      for (int jj = 0; jj < kTile; jj += kNJ)
+        filter_block<ANGLE, false, kNJ>(R, jr, jth, jj, islot, thr, cnt, dev, kappa,
                                                  rec, ids, theta, ibase, jbase);
     }
     // release the slice; the warp finishing the unit refills its stage
