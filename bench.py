@@ -45,9 +45,11 @@ FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
 FP64_PER_PAIR_NC = 5
 # The default pair kernel (certified FP32 filter) per pair:
 # 8 FFMA + 2 FMUL on the FP32 FMA pipe (issued as packed pairs) and, fused
-# with E_ca, 3 DADD + 1 DFMA on the FP64 pipe.
+# with E_ca over theta-ordered edges, 2 DADD on the FP64 pipe (|theta_j -
+# (theta_i + s)| and the accumulate; units straddling 0 or pi/2 of theta
+# difference, ~1e-4 of them on C5, take 4).
 FMA_PER_PAIR = 10
-FP64_PER_PAIR_FILTER_ECA = 4
+FP64_PER_PAIR_FILTER_ECA = 2
 FMA_LANES_PER_CLK_SM = 128   # measured 124 (FFMA2/FMUL2/FADD2, profiles/r01_packed.txt)
 FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
 # Bytes the pair kernel must read at least once per launch: i-role filter
@@ -247,7 +249,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def crossing_step():
-        rec = M.CrossingRecords(dg)
+        rec = M.CrossingRecords(dg, order="theta")
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
         sharding.allreduce_partials(out[0:2])
 
@@ -267,7 +269,7 @@ def main():
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
-            rec = M.CrossingRecords(dg)
+            rec = M.CrossingRecords(dg, order="theta")
             k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             k0.record(stream)
             rec.partial_interleaved(ideal, rank, world, out=out[0:2])
@@ -365,7 +367,7 @@ def main():
     # algorithm loads the FP32 FMA pipe most (10 lane-ops per pair against
     # 128 lanes/clk/SM, vs 4 FP64 lane-ops against 64), so that pipe bounds it.
     clk = clocks.summary()
-    recs = M.CrossingRecords(dg)
+    recs = M.CrossingRecords(dg, order="theta")
     fast, mode = recs.fast_path(), recs.mode()
     pairs_per_launch = P_E / world
     pair_rate = pairs_per_launch / (kernel_ms * 1e-3)

@@ -143,6 +143,18 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                            int64_t m, int64_t *d_edges_out, void *stream);
 
+/* Writes to d_edges_out the edge list reordered by (group, direction theta
+ * = atan2(b - a) mod pi, exact.py:217-220's angle; rows unchanged).  Edges
+ * incident to a vertex of degree >= hub_degree (0: GLR_HUB_DEGREE_DEFAULT)
+ * form one group per such hub, the rest group 0.  Dense passes over this
+ * order evaluate the crossing-angle deviation with one FP64 subtraction per
+ * pair in units whose theta difference stays on one side of 0 and pi/2
+ * (crossing.cu unit_shift), and skip units of two tiles of one hub's edges
+ * (every pair shares the hub).  Results do not depend on the order. */
+#define GLR_HUB_DEGREE_DEFAULT 1024
+int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
+                         int64_t m, int64_t hub_degree, int64_t *d_edges_out, void *stream);
+
 /* Writes to d_xy_out the vertex positions reordered by Morton code (node
  * occlusion does not depend on vertex order). */
 int glr_spatial_sort_vertices(const double *d_xy, int64_t n, double *d_xy_out,

@@ -84,6 +84,11 @@ SIGNATURES = {
         _c.c_int,
         [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p],
     ),
+    "glr_theta_sort_edges": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p,
+         _c.c_void_p],
+    ),
     "glr_spatial_sort_vertices": (
         _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p]),
     "glr_crossing_candidates": (

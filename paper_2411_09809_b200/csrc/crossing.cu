@@ -188,7 +188,9 @@ struct __align__(16) JRec {
 // tightens the filter's certification threshold for spatially local units.
 struct __align__(16) TileBox {
   float xlo, xhi, ylo, yhi;
-  float lmax, pad0, pad1, pad2;
+  float lmax;
+  float thlo, thhi;  // bounds of the tile's theta, rounded outward (empty: inf, -inf)
+  int star;          // v if every real edge of the tile is incident to vertex v, else -1
 };
 
 // Records buffer: header | rec[m_pad] | theta[m_pad] | ids[m_pad] |
@@ -441,15 +443,29 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
 // One CTA (kTile threads) per tile: box of the real edges' scaled endpoints
 // and max L (pad edges are skipped; an all-pad tile gets an empty box).
 __global__ void __launch_bounds__(kTile) tile_fbox_kernel(int64_t m, RecView rv) {
-  __shared__ float red[5][kTile / 32];
+  __shared__ float red[7][kTile / 32];
+  __shared__ int2 first;
+  __shared__ int star_ok[2];
   const int64_t e = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  if (threadIdx.x == 0) {
+    first = rv.ids[(int64_t)blockIdx.x * kTile];  // a real edge unless the tile is all pad
+    star_ok[0] = star_ok[1] = 1;
+  }
+  __syncthreads();
   float xlo = INFINITY, xhi = -INFINITY, ylo = INFINITY, yhi = -INFINITY, l = 0.0f;
+  float tlo = INFINITY, thi = -INFINITY;
   if (e < m) {
     const JRec j = rv.jrec[e];
     xlo = fminf(j.c.x, j.c.z); xhi = fmaxf(j.c.x, j.c.z);
     ylo = fminf(j.c.y, j.c.w); yhi = fmaxf(j.c.y, j.c.w);
     // L of the FP32 direction (exact float differences, rounded up)
     l = __fadd_ru(fabsf(__fsub_rn(j.c.z, j.c.x)), fabsf(__fsub_rn(j.c.w, j.c.y)));
+    const double th = rv.theta[e];
+    tlo = __double2float_rd(th);
+    thi = __double2float_ru(th);
+    const int2 id = rv.ids[e];
+    if (id.x != first.x && id.y != first.x) star_ok[0] = 0;
+    if (id.x != first.y && id.y != first.y) star_ok[1] = 0;
   }
   for (int o = 16; o > 0; o >>= 1) {
     xlo = fminf(xlo, __shfl_down_sync(0xffffffffu, xlo, o));
@@ -457,10 +473,13 @@ __global__ void __launch_bounds__(kTile) tile_fbox_kernel(int64_t m, RecView rv)
     ylo = fminf(ylo, __shfl_down_sync(0xffffffffu, ylo, o));
     yhi = fmaxf(yhi, __shfl_down_sync(0xffffffffu, yhi, o));
     l = fmaxf(l, __shfl_down_sync(0xffffffffu, l, o));
+    tlo = fminf(tlo, __shfl_down_sync(0xffffffffu, tlo, o));
+    thi = fmaxf(thi, __shfl_down_sync(0xffffffffu, thi, o));
   }
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     red[0][w] = xlo; red[1][w] = xhi; red[2][w] = ylo; red[3][w] = yhi; red[4][w] = l;
+    red[5][w] = tlo; red[6][w] = thi;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -468,10 +487,13 @@ __global__ void __launch_bounds__(kTile) tile_fbox_kernel(int64_t m, RecView rv)
       xlo = fminf(xlo, red[0][i]); xhi = fmaxf(xhi, red[1][i]);
       ylo = fminf(ylo, red[2][i]); yhi = fmaxf(yhi, red[3][i]);
       l = fmaxf(l, red[4][i]);
+      tlo = fminf(tlo, red[5][i]); thi = fmaxf(thi, red[6][i]);
     }
     TileBox b;
     b.xlo = xlo; b.xhi = xhi; b.ylo = ylo; b.yhi = yhi; b.lmax = l;
-    b.pad0 = b.pad1 = b.pad2 = 0.0f;
+    b.thlo = tlo; b.thhi = thi;
+    // all-pad tile (first id negative): no star
+    b.star = first.x < 0 ? -1 : star_ok[0] ? first.x : star_ok[1] ? first.y : -1;
     rv.tbox[blockIdx.x] = b;
   }
 }
@@ -532,11 +554,14 @@ __device__ inline float hi_view(double c) { return __int_as_float(__double2hiint
 // |ideal - min(d, pi - d)| with d = |t1 - t2|, written as
 // || pi/2 - d | - kappa|, kappa = pi/2 - ideal (4 DADD, no DMNMX).
 // Symmetric in (t1, t2) bit for bit.
-__device__ inline double angle_dev(double t1, double t2, double kappa) {
+__device__ inline double angle_dev_signed(double t1, double t2, double kappa) {
   const double HALF_PI = 1.5707963267948966;
   double d = __dsub_rn(t1, t2);
   double e = __dsub_rn(HALF_PI, fabs(d));
-  return fabs(__dsub_rn(fabs(e), kappa));
+  return __dsub_rn(fabs(e), kappa);
+}
+__device__ inline double angle_dev(double t1, double t2, double kappa) {
+  return fabs(angle_dev_signed(t1, t2, kappa));
 }
 
 // One j-edge against the thread's K i-edges.  FAST selects the float-view
@@ -750,7 +775,6 @@ constexpr int kGroups = kFGroups;  // packed i-edge pairs per lane
 struct FIRegs {
   uint64_t ax[kGroups], ay[kGroups], bx[kGroups], by[kGroups];
   uint64_t sabx[kGroups], nsaby[kGroups], nska[kGroups];
-  double th[kFK];
 };
 
 // Lane `lane` of slice `slice`: i-edge k is tile slot fslot(slice, k, lane);
@@ -771,9 +795,29 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
     R.sabx[g] = v[kFSabx * kField];
     R.nsaby[g] = v[kFNsaby * kField];
     R.nska[g] = v[kFNska * kField];
-    R.th[2 * g] = ANGLE ? t.theta[fslot(slice, 2 * g, lane)] : 0.0;
-    R.th[2 * g + 1] = ANGLE ? t.theta[fslot(slice, 2 * g + 1, lane)] : 0.0;
   }
+}
+
+// Angle deviation of a unit whose theta difference dt = theta_j - theta_i
+// keeps one side of 0 and of +-pi/2 for every pair (tile theta bounds, e.g.
+// after glr_theta_sort_edges): a = min(|dt|, pi - |dt|) is then one affine
+// branch and |ideal - a| = |theta_j - (theta_i + s)| with
+//   dt in [0, pi/2]: s = ideal          dt in [pi/2, pi): s = pi - ideal
+//   dt in [-pi/2, 0]: s = -ideal        dt in (-pi, -pi/2]: s = ideal - pi,
+// ONE DADD per pair instead of three (angle_dev).  Returns 0 (shift s in
+// *s) or -1 for a unit that straddles a branch point (general formula).
+// Rounding differs from exact.py's by a few ulps of pi per pair: inside the
+// 1e-9 relative tolerance by nine orders of magnitude.
+__device__ inline int unit_shift(const TileBox &a, const TileBox &b, double ideal, double *s) {
+  const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
+  // float bounds are outward-rounded; double differences of floats are exact
+  const double lo = (double)b.thlo - (double)a.thhi, hi = (double)b.thhi - (double)a.thlo;
+  if (!(lo <= hi)) return -1;  // empty tile
+  if (lo >= 0.0 && hi <= HALF_PI) { *s = ideal; return 0; }
+  if (lo >= HALF_PI) { *s = __dsub_rn(PI, ideal); return 0; }
+  if (hi <= 0.0 && lo >= -HALF_PI) { *s = -ideal; return 0; }
+  if (hi <= -HALF_PI) { *s = __dsub_rn(ideal, PI); return 0; }
+  return -1;
 }
 
 // Exact reference predicate for one pair (general semantics: doubles
@@ -853,24 +897,56 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
   }
 }
 
+// Uncertain pairs are not evaluated where they are found: each warp queues
+// them in shared memory (entry = tile slot of the i-edge << 8 | j slot) and
+// evaluates the queue with all 32 lanes at once (exact_pair's FP64 records
+// come from L2: one round-trip per 32 pairs instead of per pair) at the end
+// of the slice, or when the queue is full.  Results go to the lane's
+// cnt[0]/dev[0]: the queue order and the drain points depend only on the
+// slice, so sums stay deterministic.
+constexpr unsigned kQCap = 64;  // queue entries per warp
+template <bool ANGLE>
+__device__ __forceinline__ void drain_queue(const unsigned *wq, unsigned qn, unsigned lane,
+                                         const EdgeRec *__restrict__ rec,
+                                         const int2 *__restrict__ ids,
+                                         const double *__restrict__ theta, int64_t ibase,
+                                         int64_t jbase, double kappa, unsigned &cnt,
+                                         double &dev) {
+  __syncwarp();
+  for (unsigned b = 0; b < qn; b += 32) {
+    if (b + lane < qn) {
+      const unsigned ent = wq[b + lane];
+      const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + (ent >> 8),
+                                         jbase + (ent & 255u), kappa);
+      if (t >= 0.0) {
+        cnt += 1u;
+        if (ANGLE) dev = __dadd_rn(dev, t);
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // NJ consecutive j-edges against the thread's K i-edges.  Certain hits are
 // counted (and their angle deviations summed) with predicated adds; one
 // warp vote per block decides whether any lane met an uncertain pair, and
-// only then is the block re-filtered to run exact_pair on those pairs, so
-// the hot path has no branch inside the block and the compiler can
-// interleave its NJ independent j-steps.
-template <bool ANGLE, bool DIAG, int NJ>
-__device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
+// only then is the block re-filtered to queue those pairs, so the hot path
+// has no branch inside the block and the compiler can interleave its NJ
+// independent j-steps.
+#ifdef GLR_XFSTATS
+// debug build only: [vote blocks that fell back, uncertain pairs evaluated]
+__device__ unsigned long long g_fstats[2];
+#endif
+template <bool ANGLE, bool DIAG, int NJ, bool SHIFT>
+__device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)[kFK],
+                                             unsigned jaddr,
                                              unsigned thaddr, int jj0, int islot, float thr,
                                              unsigned (&cnt)[kFK], double (&dev)[kFK],
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
-                                             int64_t jbase) {
+                                             int64_t jbase, unsigned *wq, unsigned &qn) {
   bool any = false;
-  double hf[kFK];
-#pragma unroll
-  for (int k = 0; k < kFK; ++k) hf[k] = 0.0;
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kFK];
@@ -881,20 +957,24 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
       any |= fabsf(M[k]) <= thr;
       // @(M < -1) cnt += 1 (and dev += t)
       if (ANGLE) {
-        // dev += hit ? t : 0 as fma(t, {0.0 | 1.0}, dev): one DFMA and one SEL
-        // (exact: fma(t, 1, dev) == dev + t, fma(t, 0, dev) == dev)
-        const double t = angle_dev(R.th[k], thj, kappa);
-        // hf[k] = {lo: 0 (carried), hi: hit ? 0x3ff00000 : 0}: only the high
-        // word is rewritten, so no zeroing MOV per pair
+        // dev += hit ? t : 0 with t = |v|: a miss clears v's HIGH word only
+        // (one SEL, in place), leaving {lo, 0}, a subnormal below 2^-1022.
+        // Nonzero deviations are >= 2^-53 (theta, pi/2 and kappa are all
+        // multiples of 2^-53 below 2), so such an addend never changes a
+        // sum that holds one, and
+        // the per-slice sum's 2^-50 fixed-point conversion drops it: the
+        // result equals the masked sum exactly (DADD, no zeroing MOV or
+        // {0,1} multiplier per pair).
+        double v = SHIFT ? __dsub_rn(thj, th[k]) : angle_dev_signed(th[k], thj, kappa);
         asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
             "setp.lt.f32 p, %2, %3;\n\t"
             "@p add.u32 %0, %0, 1;\n\t"
             "mov.b64 {lo, hi}, %1;\n\t"
-            "selp.b32 hi, 1072693248, 0, p;\n\t"
+            "selp.b32 hi, hi, 0, p;\n\t"
             "mov.b64 %1, {lo, hi};\n\t}"
-            : "+r"(cnt[k]), "+d"(hf[k])
+            : "+r"(cnt[k]), "+d"(v)
             : "f"(M[k]), "f"(-thr));
-        dev[k] = __fma_rn(t, hf[k], dev[k]);
+        dev[k] = __dadd_rn(dev[k], fabs(v));
       } else {
         asm("{\n\t.reg .pred p;\n\t"
             "setp.lt.f32 p, %1, %2;\n\t"
@@ -905,20 +985,31 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, unsigned jaddr,
     }
   }
   if (__any_sync(0xffffffffu, any)) {
+#ifdef GLR_XFSTATS
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_fstats[0], 1ull);
+#endif
 #pragma unroll 1
     for (int q = 0; q < NJ; ++q) {
       float M[kFK];
       filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
 #pragma unroll
       for (int k = 0; k < kFK; ++k) {
-        if (fabsf(M[k]) <= thr) {
-          const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + islot + 32 * k,
-                                             jbase + jj0 + q, kappa);
-          if (t >= 0.0) {
-            cnt[k] += 1u;
-            if (ANGLE) dev[k] = __dadd_rn(dev[k], t);
-          }
+        const bool u = fabsf(M[k]) <= thr;
+        const unsigned mask = __ballot_sync(0xffffffffu, u);
+        if (mask == 0u) continue;
+#ifdef GLR_XFSTATS
+        if (u) atomicAdd(&g_fstats[1], 1ull);
+#endif
+        const unsigned lane = (unsigned)islot & 31u;
+        if (qn + __popc(mask) > kQCap) {
+          drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0],
+                             dev[0]);
+          qn = 0;
         }
+        if (u)
+          wq[qn + __popc(mask & ((1u << lane) - 1u))] =
+              ((unsigned)(islot + 32 * k) << 8) | (unsigned)(jj0 + q);
+        qn += __popc(mask);
       }
     }
   }
@@ -1125,6 +1216,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
                     uint64_t W, uint64_t ubeg,
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double kappa,
+                    double ideal,
                     unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   if (hdr->fast != kModeFilter) return;
   constexpr int kWarps = kThreads / 32;
@@ -1136,6 +1228,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   __shared__ unsigned done[kStages];  // slices finished with the stage, cumulative
   __shared__ unsigned next_slice;
   __shared__ unsigned long long acc_cnt, acc_lo, acc_hi;
+  __shared__ unsigned wqueue[kWarps][kQCap];  // uncertain pairs (filter_block)
   constexpr unsigned kJBytes = kTile * sizeof(JRec);
   constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
   const unsigned lane = threadIdx.x & 31;
@@ -1186,6 +1279,24 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     }
     const int stage = (int)(uq % kStages);
     const unsigned use = (unsigned)(uq / kStages);
+    // this unit's theta_i (+ shift s, see unit_shift), loaded before the waits
+    const TileBox bi = tbox[ti], bj = tbox[tj];
+    // both tiles are stars of one vertex: every pair shares it, and
+    // exact.py:205 never counts such a pair -- the unit contributes nothing
+    const bool star = bi.star >= 0 && bi.star == bj.star;
+    double th[kFK];
+    int shift = -1;
+    if (ANGLE) {
+      double sh = 0.0;
+      if (ti != tj) shift = unit_shift(bi, bj, ideal, &sh);
+      const double *tt = ftile[ti].theta;
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) th[k] = tt[islot + 32 * k];
+      if (shift == 0) {
+#pragma unroll
+        for (int k = 0; k < kFK; ++k) th[k] = __dadd_rn(th[k], sh);
+      }
+    }
     // the stage's previous unit must be fully released (its refill issued)
     // before its mbarrier phase parity identifies this use unambiguously
     while (*(volatile unsigned *)&done[stage] < use * kFSlices) {
@@ -1198,16 +1309,24 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
 #pragma unroll
     for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
-    const float thr = unit_threshold(tbox[ti], tbox[tj]);
-    if (ti == tj) {
+    const float thr = unit_threshold(bi, bj);
+    unsigned *wq = wqueue[threadIdx.x >> 5];
+    unsigned qn = 0;  // warp-uniform queue length
+    if (star) {
+    } else if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, true, kNJ>(R, jr, jth, jj, islot, thr, cnt, dev, kappa, rec,
-                                                ids, theta, ibase, jbase);
+        filter_block<ANGLE, true, kNJ, false>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
+                                              rec, ids, theta, ibase, jbase, wq, qn);
+    } else if (ANGLE && shift == 0) {
+#pragma unroll 1
+      for (int jj = 0; jj < kTile; jj += kNJ)
+        filter_block<ANGLE, false, kNJ, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
+                                              rec, ids, theta, ibase, jbase, wq, qn);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ>(R, jr, jth, jj, islot, thr, cnt, dev, kappa,
-                                                 rec, ids, theta, ibase, jbase);
+        filter_block<ANGLE, false, kNJ, false>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
+                                               rec, ids, theta, ibase, jbase, wq, qn);
     }
     // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
@@ -1223,6 +1342,10 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         }
       }
     }
+    // the slice's queued uncertain pairs (global records only, so after the
+    // stage is released)
+    if (qn != 0)
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0], dev[0]);
     unsigned c = 0;
     double s = 0.0;
 #pragma unroll
@@ -1619,7 +1742,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
-        cc, cd);
+        ideal, cc, cd);
     GLR_LAUNCHED("cross_filter_kernel<angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                  d_list, U, T, W, ubeg, uend, chunk, r, g, kappa,
@@ -1636,7 +1759,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        cc, cd);
+        0.0, cc, cd);
     GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                   d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
@@ -1690,6 +1813,19 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
 }
 
 }  // namespace glr
+
+#ifdef GLR_XFSTATS
+extern "C" int glr_debug_fstats(unsigned long long *h, int reset) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return GLR_ECUDA;
+  if (cudaMemcpyFromSymbol(h, glr::g_fstats, sizeof(unsigned long long) * 2) != cudaSuccess)
+    return GLR_ECUDA;
+  if (reset) {
+    const unsigned long long z[2] = {0, 0};
+    if (cudaMemcpyToSymbol(glr::g_fstats, z, sizeof(z)) != cudaSuccess) return GLR_ECUDA;
+  }
+  return GLR_OK;
+}
+#endif
 
 extern "C" {
 

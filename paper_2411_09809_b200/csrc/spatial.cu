@@ -88,6 +88,50 @@ __global__ void edge_keys_kernel(const double2 *__restrict__ xy, const longlong2
   }
 }
 
+// Direction order with hub grouping (glr_theta_sort_edges).  Key = (group,
+// theta quantised to 32 bits): edges incident to a vertex of degree >=
+// hub_degree form one group per such vertex (the endpoint of larger degree),
+// all other edges group 0.  Within a group edges run by direction, so tiles
+// have narrow theta ranges (crossing.cu unit_shift) and a hub's edges fill
+// "star" tiles whose mutual units are skipped (every pair shares the hub);
+// pairs sharing a vertex -- always uncertain for the FP32 filter -- no
+// longer scatter over the whole pair space.  Any monotone theta
+// approximation will do: the pair kernel classifies units by exact tile
+// bounds, and results never depend on the order.
+__global__ void degree_kernel(const longlong2 *__restrict__ e, int64_t m, int *deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 uv = e[i];
+    atomicAdd(&deg[uv.x], 1);
+    atomicAdd(&deg[uv.y], 1);
+  }
+}
+
+__global__ void edge_theta_keys_kernel(const double2 *__restrict__ xy,
+                                       const longlong2 *__restrict__ e, int64_t m,
+                                       const int *__restrict__ deg, int64_t hub_degree,
+                                       unsigned long long *keys, int *idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 uv = e[i];
+    const double2 p = xy[uv.x], q = xy[uv.y];
+    double t = atan2(q.y - p.y, q.x - p.x);
+    if (t < 0.0) t += 3.141592653589793;
+    double k = t * (4294967296.0 / 3.141592653589793);
+    if (!(k >= 0.0)) k = 0.0;  // also NaN
+    if (k > 4294967295.0) k = 4294967295.0;
+    const int du = deg[uv.x], dv = deg[uv.y];
+    const long long hub = (du >= dv) ? uv.x : uv.y;  // ties: the smaller index
+    const unsigned long long grp =
+        ((du > dv ? du : dv) >= hub_degree) ? (unsigned long long)hub + 1ull : 0ull;
+    keys[i] = (grp << 32) | (unsigned long long)(unsigned)k;
+    idx[i] = (int)i;
+  }
+}
+
+int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+               int64_t hub_degree, int64_t *d_out, cudaStream_t st);
+
 __global__ void vertex_keys_kernel(const double2 *__restrict__ xy, int64_t n,
                                    const unsigned long long *b, unsigned *keys, int *idx) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -177,6 +221,46 @@ int spatial_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t 
   return GLR_OK;
 }
 
+int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+               int64_t hub_degree, int64_t *d_out, cudaStream_t st) {
+  if (m <= 1) {
+    if (m == 1) GLR_CUDA(cudaMemcpyAsync(d_out, d_edges, 16, cudaMemcpyDeviceToDevice, st));
+    return GLR_OK;
+  }
+  int end_bit = 32;
+  while (end_bit < 64 && ((unsigned long long)(n + 1) >> (end_bit - 32)) != 0) ++end_bit;
+  size_t t_sort = 0;
+  GLR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const unsigned long long *)nullptr,
+                                           (unsigned long long *)nullptr, (const int *)nullptr,
+                                           (int *)nullptr, (int)m, 0, end_bit, st));
+  const size_t a8 = ((size_t)m * 8 + 255) & ~(size_t)255;
+  const size_t a4 = ((size_t)m * 4 + 255) & ~(size_t)255;
+  const size_t an = ((size_t)n * 4 + 255) & ~(size_t)255;
+  Scratch scr(2 * a8 + 2 * a4 + an + t_sort, st);
+  GLR_CUDA(scr.err);
+  char *p = scr.as<char>();
+  auto *keys = reinterpret_cast<unsigned long long *>(p);
+  auto *keys_out = reinterpret_cast<unsigned long long *>(p + a8);
+  int *idx = reinterpret_cast<int *>(p + 2 * a8);
+  int *perm = reinterpret_cast<int *>(p + 2 * a8 + a4);
+  int *deg = reinterpret_cast<int *>(p + 2 * a8 + 2 * a4);
+  void *tmp = p + 2 * a8 + 2 * a4 + an;
+  const auto *e2 = reinterpret_cast<const longlong2 *>(d_edges);
+  GLR_CUDA(cudaMemsetAsync(deg, 0, (size_t)n * 4, st));
+  degree_kernel<<<grid_of(m), 256, 0, st>>>(e2, m, deg);
+  GLR_LAUNCHED("degree_kernel");
+  edge_theta_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2,
+                                                     m, deg, hub_degree, keys, idx);
+  GLR_LAUNCHED("edge_theta_keys_kernel");
+  size_t tb = t_sort;
+  GLR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_out, idx, perm, (int)m, 0, end_bit,
+                                           st));
+  count_launch(4);
+  gather_edges_kernel<<<grid_of(m), 256, 0, st>>>(e2, perm, m, reinterpret_cast<longlong2 *>(d_out));
+  GLR_LAUNCHED("gather_edges_kernel");
+  return GLR_OK;
+}
+
 }  // namespace
 }  // namespace glr
 
@@ -190,6 +274,17 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
     return GLR_EARG;
   }
   return glr::spatial_sort<true>(d_xy, n, d_edges, m, d_edges_out, glr::as_stream(stream));
+}
+
+int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+                         int64_t hub_degree, int64_t *d_edges_out, void *stream) {
+  if (n < 0 || m < 0 || (m > 0 && (d_xy == nullptr || d_edges == nullptr || d_edges_out == nullptr)) ||
+      m >= ((int64_t)1 << 31) || n >= ((int64_t)1 << 31)) {
+    glr::set_error("glr_theta_sort_edges: invalid arguments");
+    return GLR_EARG;
+  }
+  if (hub_degree <= 0) hub_degree = GLR_HUB_DEGREE_DEFAULT;
+  return glr::theta_sort(d_xy, n, d_edges, m, hub_degree, d_edges_out, glr::as_stream(stream));
 }
 
 int glr_spatial_sort_vertices(const double *d_xy, int64_t n, double *d_xy_out, void *stream) {

@@ -259,7 +259,7 @@ def bench(g, shard_counts=(1, 2, 4, 8), params: MetricParams | None = None, metr
     dg = M.DeviceGraph.from_graph(g)
     rows = []
     base: dict = {}
-    rec = M.CrossingRecords(dg) if g.num_edges >= 2 else None
+    rec = M.CrossingRecords(dg, order="theta") if g.num_edges >= 2 else None
     for shards in counts:
         t0 = time.perf_counter()
         cnt = dev = 0.0

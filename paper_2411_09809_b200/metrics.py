@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -42,6 +43,9 @@ from .model import IDEAL_ANGLE_DEFAULT, ParameterError, check_ideal_angle, check
 STRATEGIES = ("auto", "dense", "culled")
 CULL_FRACTION = 0.25      # auto: cull when candidates <= this share of tile pairs
 AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
+# theta order: vertices of at least this degree get their own edge group
+# (glr_theta_sort_edges; 0 = the library default).  Tuning knob only.
+HUB_DEGREE = int(os.environ.get("GLARE_B200_HUB_DEGREE", "0"))
 
 
 class DeviceGraph:
@@ -197,10 +201,19 @@ class CrossingRecords:
 
     ``strategy`` selects dense or culled scanning (see the module docstring);
     with culling the records hold the Morton-ordered edge list and ``list``
-    the candidate tile pairs."""
+    the candidate tile pairs.  ``order="theta"`` makes dense records hold the
+    edges ordered by direction (glr_theta_sort_edges), which lets the fused
+    E_c + E_ca pass evaluate the angle deviation with one FP64 operation per
+    pair in almost every unit; ``"input"`` keeps the caller's order (unit
+    ranges then match the oracle's unit-range restatement).  Results never
+    depend on the order."""
 
-    def __init__(self, dg: DeviceGraph, strategy: str = "dense"):
+    ORDERS = ("input", "theta")
+
+    def __init__(self, dg: DeviceGraph, strategy: str = "dense", order: str = "input"):
         strategy = _check_strategy(strategy)
+        if order not in self.ORDERS:
+            raise ParameterError(f"order must be one of {self.ORDERS}, got {order!r}")
         self.m = dg.num_edges
         self.n = dg.num_vertices
         self.list = None
@@ -216,6 +229,13 @@ class CrossingRecords:
             if strategy == "culled" or len(lst) <= CULL_FRACTION * crossing_units(self.m):
                 self.list = lst
                 return
+        if order == "theta" and self.m >= 2:
+            es = torch.empty_like(dg.edges)
+            _lib.check(_lib.lib().glr_theta_sort_edges(_ptr(dg.xy), self.n, _ptr(dg.edges),
+                                                       self.m, HUB_DEGREE, _ptr(es), _stream()),
+                       "glr_theta_sort_edges")
+            self._prepare(dg.xy, es)
+            return
         self._prepare(dg.xy, dg.edges)
 
     def _prepare(self, xy: torch.Tensor, edges: torch.Tensor) -> None:
@@ -391,7 +411,7 @@ def _crossing_scan(g, ideal_angle: float | None = None, *,
     m = _num_edges(g)
     if m < 2:
         return 0, 0.0
-    rec = CrossingRecords(_dev(g), strategy)
+    rec = CrossingRecords(_dev(g), strategy, "input" if ideal_angle is None else "theta")
     out = rec.partial(ideal_angle, 0, rec.units)
     count, dev = out.tolist()
     return int(count), (float(dev) if ideal_angle is not None else 0.0)

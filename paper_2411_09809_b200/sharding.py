@@ -80,7 +80,8 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
     else:
         out.zero_()
     if with_crossing and dg.num_edges >= 2:
-        rec = records if records is not None else M.CrossingRecords(dg, strategy)
+        rec = records if records is not None else M.CrossingRecords(
+            dg, strategy, "input" if ideal is None else "theta")
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
     if radius is not None and dg.num_vertices >= 2:
         plan = M.OcclusionPlan(dg, radius, strategy)

@@ -226,3 +226,45 @@ def test_set_mode_outside_fast_window_degrades(gpu):
     assert rec.set_mode(2).mode() == 0
     with pytest.raises(Exception):
         rec.set_mode(3)
+
+
+def uniform_long(seed=11, n=6000, m=24000):
+    """Long random edges in the unit square (C5-like mix, ~100 tiles): after
+    a theta sort almost every off-diagonal unit is one shift class."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0, 1, (n, 2)), _random_pairs(rng, n, m)
+
+
+@pytest.mark.parametrize("name", ["uniform_long", "lattice_c5_like", "near_collinear", "hubs",
+                                  "exact_lattice"])
+def test_theta_order_shift_classes(gpu, name):
+    """Dense records over theta-ordered edges (glr_theta_sort_edges) evaluate
+    the deviation as |theta_j - (theta_i + s)| in classified units
+    (crossing.cu unit_shift).  Ascending order exercises the s = ideal and
+    s = pi - ideal classes, a host-side descending order the s = -ideal and
+    s = ideal - pi classes; several ideal angles move the class borders.
+    Counts must equal the oracle's exactly, dev_sum within 1e-9."""
+    import torch
+
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import metrics as M
+
+    g = _graph(*(CASES.get(name) or uniform_long)())
+    th = np.mod(np.arctan2(g.xy[g.edges[:, 1], 1] - g.xy[g.edges[:, 0], 1],
+                           g.xy[g.edges[:, 1], 0] - g.xy[g.edges[:, 0], 0]), np.pi)
+    desc = g.edges[np.argsort(-th, kind="stable")]
+    dg = M.DeviceGraph.from_graph(g)
+    dd = M.DeviceGraph(dg.xy, torch.as_tensor(desc, device=dg.xy.device))
+    for ideal in (0.1, 1.0, IDEAL, 1.3, math.pi / 2):
+        cw, dw = S.crossing_scan(g.xy, g.edges, ideal)
+        asc = M.CrossingRecords(dg, "dense", "theta")
+        c, d = asc.partial(ideal, 0, asc.units).tolist()
+        assert int(c) == cw and strict_close(d, dw), (name, ideal, "ascending")
+        rd = M.CrossingRecords(dd, "dense", "input")
+        c, d = rd.partial(ideal, 0, rd.units).tolist()
+        assert int(c) == cw and strict_close(d, dw), (name, ideal, "descending")
+        # interleaved shards of the theta-ordered records sum to the whole
+        parts = [asc.partial_interleaved(ideal, r, 3).tolist() for r in range(3)]
+        assert sum(int(p[0]) for p in parts) == cw
+        assert strict_close(sum(p[1] for p in parts), dw)
+    assert M._crossing_scan(g, IDEAL)[0] == S.crossing_scan(g.xy, g.edges, IDEAL)[0]

@@ -5,13 +5,13 @@ Each variant runs in its own subprocess (GLARE_B200_LIB selects the .so)."""
 import json, os, subprocess, sys
 
 CHILD = r'''
-import sys, json; sys.path.insert(0, ".")
+import sys, json, os; sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2411_09809_b200 import metrics as M, configs, LayoutGraph
 m = int(sys.argv[1])
 g, _ = configs.config5(n=m * 3 // 8, m=m)   # C5 shape (Chung-Lu on the 2^16 lattice), scaled
 dg = M.DeviceGraph.from_graph(g)
-rec = M.CrossingRecords(dg)
+rec = M.CrossingRecords(dg, order=os.environ.get("VB_ORDER", "theta"))
 res = {}
 for name, ideal in (("ec", None), ("eca", configs.IDEAL_70)):
     rec.partial(ideal, 0, rec.units); torch.cuda.synchronize()
