@@ -898,15 +898,15 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 }
 
 // Uncertain pairs are not evaluated where they are found: each warp queues
-// them in shared memory (entry = tile slot of the i-edge << 8 | j slot) and
+// them in shared memory (16-bit entry = tile slot of the i-edge << 8 | j slot) and
 // evaluates the queue with all 32 lanes at once (exact_pair's FP64 records
 // come from L2: one round-trip per 32 pairs instead of per pair) at the end
 // of the slice, or when the queue is full.  Results go to the lane's
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
-constexpr unsigned kQCap = 64;  // queue entries per warp
+constexpr unsigned kQCap = 512;  // queue entries per warp (>= 32 lanes x NJ x kFK)
 template <bool ANGLE>
-__device__ __forceinline__ void drain_queue(const unsigned *wq, unsigned qn, unsigned lane,
+__device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
                                          const EdgeRec *__restrict__ rec,
                                          const int2 *__restrict__ ids,
                                          const double *__restrict__ theta, int64_t ibase,
@@ -915,7 +915,7 @@ __device__ __forceinline__ void drain_queue(const unsigned *wq, unsigned qn, uns
   __syncwarp();
   for (unsigned b = 0; b < qn; b += 32) {
     if (b + lane < qn) {
-      const unsigned ent = wq[b + lane];
+      const unsigned ent = wq[b + lane];  // i slot << 8 | j slot
       const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + (ent >> 8),
                                          jbase + (ent & 255u), kappa);
       if (t >= 0.0) {
@@ -945,7 +945,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
                                              double kappa, const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
-                                             int64_t jbase, unsigned *wq, unsigned &qn) {
+                                             int64_t jbase, unsigned short *wq, unsigned &qn) {
   bool any = false;
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
@@ -985,33 +985,44 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     }
   }
   if (__any_sync(0xffffffffu, any)) {
-#ifdef GLR_XFSTATS
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_fstats[0], 1ull);
-#endif
-#pragma unroll 1
+    // re-filter the block into a per-lane mask (bit q*kFK + k), then place
+    // the lanes' entries by a warp prefix sum: positions depend only on lane
+    // and bit order (deterministic), and the path has no vote per pair
+    unsigned U = 0;
+#pragma unroll
     for (int q = 0; q < NJ; ++q) {
       float M[kFK];
       filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
 #pragma unroll
-      for (int k = 0; k < kFK; ++k) {
-        const bool u = fabsf(M[k]) <= thr;
-        const unsigned mask = __ballot_sync(0xffffffffu, u);
-        if (mask == 0u) continue;
-#ifdef GLR_XFSTATS
-        if (u) atomicAdd(&g_fstats[1], 1ull);
-#endif
-        const unsigned lane = (unsigned)islot & 31u;
-        if (qn + __popc(mask) > kQCap) {
-          drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0],
-                             dev[0]);
-          qn = 0;
-        }
-        if (u)
-          wq[qn + __popc(mask & ((1u << lane) - 1u))] =
-              ((unsigned)(islot + 32 * k) << 8) | (unsigned)(jj0 + q);
-        qn += __popc(mask);
-      }
+      for (int k = 0; k < kFK; ++k) U |= (fabsf(M[k]) <= thr ? 1u : 0u) << (q * kFK + k);
     }
+    const unsigned lane = (unsigned)islot & 31u;
+    const unsigned n = __popc(U);
+    unsigned incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+#ifdef GLR_XFSTATS
+    if (lane == 0) {
+      atomicAdd(&g_fstats[0], 1ull);
+      atomicAdd(&g_fstats[1], (unsigned long long)total);
+    }
+#endif
+    if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0], dev[0]);
+      qn = 0;
+    }
+    unsigned pos = qn + incl - n;
+    while (U != 0u) {
+      const int b = __ffs(U) - 1;
+      U &= U - 1u;
+      wq[pos++] = (unsigned short)(((unsigned)(islot + 32 * (b % kFK)) << 8) |
+                                   (unsigned)(jj0 + b / kFK));
+    }
+    qn += total;
   }
 }
 
@@ -1222,13 +1233,14 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   constexpr int kWarps = kThreads / 32;
   constexpr int kNJ = ANGLE ? kFilterBlock : kFilterBlockCount;
   static_assert(kFSlices >= 1, "at least one slice per unit");
+  static_assert(kQCap >= 32u * kNJ * kFK, "a block's uncertain pairs must fit the queue");
   __shared__ __align__(128) JRec sj[kStages][kTile];
   __shared__ __align__(128) double sth[kStages][ANGLE ? kTile : 2];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ unsigned done[kStages];  // slices finished with the stage, cumulative
   __shared__ unsigned next_slice;
   __shared__ unsigned long long acc_cnt, acc_lo, acc_hi;
-  __shared__ unsigned wqueue[kWarps][kQCap];  // uncertain pairs (filter_block)
+  __shared__ unsigned short wqueue[kWarps][kQCap];  // uncertain pairs (filter_block)
   constexpr unsigned kJBytes = kTile * sizeof(JRec);
   constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
   const unsigned lane = threadIdx.x & 31;
@@ -1310,7 +1322,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     const float thr = unit_threshold(bi, bj);
-    unsigned *wq = wqueue[threadIdx.x >> 5];
+    unsigned short *wq = wqueue[threadIdx.x >> 5];
     unsigned qn = 0;  // warp-uniform queue length
     if (star) {
     } else if (ti == tj) {

@@ -12,7 +12,7 @@ a = ap.parse_args()
 g, _ = configs.config5(n=a.m * 3 // 8, m=a.m)
 dg = M.DeviceGraph.from_graph(g)
 for _ in range(a.reps):
-    rec = M.CrossingRecords(dg)
+    rec = M.CrossingRecords(dg, order="theta")
     out = rec.partial(configs.IDEAL_70, 0, rec.units)
     out2 = rec.partial(None, 0, rec.units)
     o = M.occlusion_partial(dg, M.occlusion_threshold(8.0), 0, M.occlusion_units(g.num_vertices))
