@@ -160,6 +160,20 @@ enum FField { kFAx, kFAy, kFBx, kFBy, kFSabx, kFNsaby, kFNska, kFFields };
 constexpr int kFK = GLR_XFK;             // i-edges per lane in the filter kernel
 constexpr int kFGroups = kFK / 2;        // packed i-edge pairs per lane
 constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
+// independent hit counters / angle accumulators per lane (ILP vs registers;
+// one counter makes the count-only kernel 3% faster, profiles/r01_variants_filter.txt)
+#ifndef GLR_XFCNT_A
+#define GLR_XFCNT_A 4
+#endif
+#ifndef GLR_XFCNT_C
+#define GLR_XFCNT_C 1
+#endif
+#ifndef GLR_XFDEV
+#define GLR_XFDEV 4
+#endif
+constexpr int kCntAccAngle = GLR_XFCNT_A;
+constexpr int kCntAccCount = GLR_XFCNT_C;
+constexpr int kDevAcc = GLR_XFDEV;
 static_assert(kFK % 2 == 0 && kFK <= 4 && kTile % (32 * kFK) == 0, "filter slice shape");
 
 __host__ __device__ inline int fslot(int slice, int k, int lane) {
@@ -972,14 +986,14 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
             "mov.b64 {lo, hi}, %1;\n\t"
             "selp.b32 hi, hi, 0, p;\n\t"
             "mov.b64 %1, {lo, hi};\n\t}"
-            : "+r"(cnt[k]), "+d"(v)
+            : "+r"(cnt[k % kCntAccAngle]), "+d"(v)
             : "f"(M[k]), "f"(-thr));
-        dev[k] = __dadd_rn(dev[k], fabs(v));
+        dev[k % kDevAcc] = __dadd_rn(dev[k % kDevAcc], fabs(v));
       } else {
         asm("{\n\t.reg .pred p;\n\t"
             "setp.lt.f32 p, %1, %2;\n\t"
             "@p add.u32 %0, %0, 1;\n\t}"
-            : "+r"(cnt[k])
+            : "+r"(cnt[k % kCntAccCount])
             : "f"(M[k]), "f"(-thr));
       }
     }
