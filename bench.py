@@ -252,6 +252,7 @@ def main():
         rec = M.CrossingRecords(dg, order="theta")
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
         sharding.allreduce_partials(out[0:2])
+        del rec  # release before the next step builds its own (allocator reuse)
 
     def occlusion_step():
         U = M.occlusion_units(n)
@@ -276,6 +277,7 @@ def main():
             k1.record(stream)
             sharding.allreduce_partials(out[0:2])
             kern_ms.append((k0, k1))
+            del rec
         ev1.record(stream)
         barrier()
     launches = int(L.glr_take_launch_count())
