@@ -55,7 +55,7 @@ FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
 # Bytes the pair kernel must read at least once per launch: i-role filter
 # record 36 B + j-role record 32 B + theta 8 B per edge.
 REC_BYTES_PER_EDGE = 76
-C5_DRAM_BYTES_PER_LAUNCH = 289_670_264_576 + 339_670_528   # profiles/r01_dram_c5_filter.txt
+C5_DRAM_BYTES_PER_LAUNCH = 250_230_000_000 + 185_480_000   # profiles/r01_dram_c5_filter_v2.txt
 CPU_SAMPLE_EDGES = 120_000
 CPU_SAMPLE_SEED = 99
 
