@@ -317,6 +317,28 @@ def main():
     occ_culled_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / args.steps)
     assert out[2].item() == occ_count, (out[2].item(), occ_count)
 
+    # ---- crossing, culled plan (4-D bbox Morton order + candidate tile
+    # pairs; what strategy="auto" runs on C5) -- effective rate, same result
+    def crossing_culled_step():
+        rec = M.CrossingRecords(dg, "culled")
+        rec.partial_interleaved(ideal, rank, world, out=out[0:2])
+        sharding.allreduce_partials(out[0:2])
+        units = rec.units
+        del rec
+        return units
+
+    for _ in range(min(args.warmup, 1)):
+        crossing_culled_step()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cross_units = crossing_culled_step()
+    torch.cuda.synchronize()
+    barrier()
+    cross_culled_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / args.steps)
+    assert out[0].item() == count, (out[0].item(), count)
+
     # ---- fr_layout: repulsion pairs/s, rank 0 ----
     layout = None
     if rank == 0 and not args.no_layout:
@@ -422,6 +444,13 @@ def main():
                                  "dense_units": M.occlusion_units(n),
                                  "note": "effective rate: same count, Morton order + "
                                          "candidate tile pairs (incl. plan build)"}},
+        "crossing_culled": {"metric": "edge-pair crossing tests/s (E_c+E_ca fused), culled plan",
+                            "value": P_E / (cross_culled_ms * 1e-3), "unit": "pairs/s",
+                            "ms_per_step": cross_culled_ms, "candidate_units": cross_units,
+                            "dense_units": M.crossing_units(m),
+                            "note": "effective rate (m(m-1)/2 / time): same count and sum, 4-D "
+                                    "bbox Morton order + candidate tile pairs (incl. plan "
+                                    "build); the public API's strategy='auto' on C5"},
         "layout": layout,
         "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": peak_run,
                      "unit": "T lane-op/s (FP32 FFMA/FMUL on the FMA pipe)",

@@ -136,10 +136,12 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
 
 /* ---- culled variants (results identical) ---------- */
 
-/* Writes to d_edges_out the edge list reordered by the Morton code of each
- * edge's bbox centre (rows unchanged, only their order).  The metrics do not
- * depend on edge order; spatially compact tiles let most tile pairs be
- * skipped by glr_crossing_candidates. */
+/* Writes to d_edges_out the edge list reordered by (hub group, 4-D Morton
+ * code of the edge's bbox sides xmin, xmax, ymin, ymax, diagonal orientation)
+ * -- rows unchanged, only their order; hub groups as in
+ * glr_theta_sort_edges.  The metrics do not depend on edge order; tiles
+ * compact in all four sides let glr_crossing_candidates skip most tile
+ * pairs of short-edge graphs and ~40% of them for long random edges. */
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                            int64_t m, int64_t *d_edges_out, void *stream);
 

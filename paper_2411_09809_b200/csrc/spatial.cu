@@ -4,10 +4,12 @@
 // The exact metrics do not depend on the order of edges or vertices (the pair
 // predicate is symmetric and every unordered pair is visited once, the
 // adjacency correction uses the same indexing), so a permutation is free to
-// choose.  Sorting by the Morton code of the bbox centre makes each 256- or
-// 1024-element tile spatially compact, so most tile pairs have disjoint tile
-// bounding boxes and are skipped by the candidate lists built in crossing.cu
-// and occlusion.cu.  The permutation only affects speed, never results.
+// choose.  Sorting vertices by the Morton code of the position, and edges by
+// the 4-D Morton code of their bbox sides, makes each 1024- or 256-element
+// tile spatially compact, so most tile pairs have disjoint tile bounding
+// boxes and are skipped by the candidate lists built in occlusion.cu and
+// crossing.cu.  The direction order (glr_theta_sort_edges) serves the dense
+// crossing pass instead.  The permutation only affects speed, never results.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -75,29 +77,6 @@ __device__ inline unsigned morton(double x, double y, const unsigned long long *
   return spread16(quant16(x, x0, sx)) | (spread16(quant16(y, y0, sy)) << 1);
 }
 
-__global__ void edge_keys_kernel(const double2 *__restrict__ xy, const longlong2 *__restrict__ e,
-                                 int64_t m, const unsigned long long *b, unsigned *keys,
-                                 int *idx) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const longlong2 uv = e[i];
-    const double2 p = xy[uv.x], q = xy[uv.y];
-    // bbox centre (halves first: no overflow for huge coordinates)
-    keys[i] = morton(0.5 * p.x + 0.5 * q.x, 0.5 * p.y + 0.5 * q.y, b);
-    idx[i] = (int)i;
-  }
-}
-
-// Direction order with hub grouping (glr_theta_sort_edges).  Key = (group,
-// theta quantised to 32 bits): edges incident to a vertex of degree >=
-// hub_degree form one group per such vertex (the endpoint of larger degree),
-// all other edges group 0.  Within a group edges run by direction, so tiles
-// have narrow theta ranges (crossing.cu unit_shift) and a hub's edges fill
-// "star" tiles whose mutual units are skipped (every pair shares the hub);
-// pairs sharing a vertex -- always uncertain for the FP32 filter -- no
-// longer scatter over the whole pair space.  Any monotone theta
-// approximation will do: the pair kernel classifies units by exact tile
-// bounds, and results never depend on the order.
 __global__ void degree_kernel(const longlong2 *__restrict__ e, int64_t m, int *deg) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -129,8 +108,59 @@ __global__ void edge_theta_keys_kernel(const double2 *__restrict__ xy,
   }
 }
 
+// Crossing-cull order (glr_spatial_sort_edges): key = (hub group, 4-D
+// Morton code of the bbox (xmin, xmax, ymin, ymax), 8 bits per axis,
+// diagonal orientation).  Tiles of edges with similar extents on all four sides have
+// tight tile boxes even for long edges (a 2-D centre key leaves long random
+// edges' tiles spanning the domain), so glr_crossing_candidates can drop
+// tile pairs whose boxes are disjoint -- on random long edges about half of
+// them (C5: 60% of the tile pairs remain).  Hub groups keep shared-vertex
+// pairs in star tiles.
+__device__ inline unsigned long long spread8x4(unsigned v) {
+  unsigned long long r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r |= (unsigned long long)((v >> i) & 1u) << (4 * i);
+  return r;
+}
+__device__ inline unsigned quant8(double v, double lo, double scale) {
+  double q = (v - lo) * scale;  // scale = 255 / (hi - lo), or 0 for a flat axis
+  if (!(q >= 0.0)) q = 0.0;
+  if (q > 255.0) q = 255.0;
+  return (unsigned)q;
+}
+__global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
+                                     const longlong2 *__restrict__ e, int64_t m,
+                                     const unsigned long long *b, const int *__restrict__ deg,
+                                     int64_t hub_degree, unsigned long long *keys, int *idx) {
+  const double x0 = dunkey(b[0]), x1 = dunkey(b[1]), y0 = dunkey(b[2]), y1 = dunkey(b[3]);
+  const double sx = (x1 > x0 && isfinite(x1 - x0)) ? 255.0 / (x1 - x0) : 0.0;
+  const double sy = (y1 > y0 && isfinite(y1 - y0)) ? 255.0 / (y1 - y0) : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 uv = e[i];
+    const double2 p = xy[uv.x], q = xy[uv.y];
+    const unsigned long long mk =
+        spread8x4(quant8(fmin(p.x, q.x), x0, sx)) |
+        (spread8x4(quant8(fmax(p.x, q.x), x0, sx)) << 1) |
+        (spread8x4(quant8(fmin(p.y, q.y), y0, sy)) << 2) |
+        (spread8x4(quant8(fmax(p.y, q.y), y0, sy)) << 3);
+    const unsigned long long up = ((q.x - p.x) * (q.y - p.y) >= 0.0) ? 1ull : 0ull;
+    const int du = deg[uv.x], dv = deg[uv.y];
+    const long long hub = (du >= dv) ? uv.x : uv.y;
+    const unsigned long long grp =
+        ((du > dv ? du : dv) >= hub_degree) ? (unsigned long long)hub + 1ull : 0ull;
+    // orientation below the Morton code: on short-edge graphs a top-level
+    // split would give every region tiles of both orientations (C3 culled
+    // units 22,229 vs 11,688; C5 76.0M vs 73.3M, tools/cull_probe.py)
+    keys[i] = (grp << 33) | (mk << 1) | up;
+    idx[i] = (int)i;
+  }
+}
+
 int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
                int64_t hub_degree, int64_t *d_out, cudaStream_t st);
+int box_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+             int64_t hub_degree, int64_t *d_out, cudaStream_t st);
 
 __global__ void vertex_keys_kernel(const double2 *__restrict__ xy, int64_t n,
                                    const unsigned long long *b, unsigned *keys, int *idx) {
@@ -163,22 +193,18 @@ int grid_of(int64_t work) {
   return (int)(b < 1 ? 1 : b);
 }
 
-// Shared driver: bounds, keys, stable radix sort of (key, index), gather.
-template <bool EDGES>
-int spatial_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t len, void *d_out,
-                 cudaStream_t st) {
-  if (len <= 1) {
-    if (len == 1) {
-      GLR_CUDA(cudaMemcpyAsync(d_out, EDGES ? (const void *)d_edges : (const void *)d_xy, 16,
-                               cudaMemcpyDeviceToDevice, st));
-    }
+// Vertex order: bounds, Morton keys of the positions, stable radix sort of
+// (key, index), gather.
+int vertex_sort(const double *d_xy, int64_t n, double *d_out, cudaStream_t st) {
+  if (n <= 1) {
+    if (n == 1) GLR_CUDA(cudaMemcpyAsync(d_out, d_xy, 16, cudaMemcpyDeviceToDevice, st));
     return GLR_OK;
   }
   size_t t_sort = 0;
   GLR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const unsigned *)nullptr,
                                            (unsigned *)nullptr, (const int *)nullptr,
-                                           (int *)nullptr, (int)len, 0, 32, st));
-  const size_t a4 = ((size_t)len * 4 + 255) & ~(size_t)255;
+                                           (int *)nullptr, (int)n, 0, 32, st));
+  const size_t a4 = ((size_t)n * 4 + 255) & ~(size_t)255;
   Scratch scr(4 * a4 + 256 + t_sort, st);
   GLR_CUDA(scr.err);
   char *p = scr.as<char>();
@@ -195,40 +221,28 @@ int spatial_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t 
   GLR_CUDA(cudaMemsetAsync(b + 3, 0x00, 8, st));
   bounds_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n, b);
   GLR_LAUNCHED("bounds_kernel");
-  if (EDGES) {
-    edge_keys_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
-                                                  reinterpret_cast<const longlong2 *>(d_edges),
-                                                  len, b, keys, idx);
-    GLR_LAUNCHED("edge_keys_kernel");
-  } else {
-    vertex_keys_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
-                                                    len, b, keys, idx);
-    GLR_LAUNCHED("vertex_keys_kernel");
-  }
+  vertex_keys_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n, b,
+                                                 keys, idx);
+  GLR_LAUNCHED("vertex_keys_kernel");
   size_t tb = t_sort;
-  GLR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_out, idx, perm, (int)len, 0, 32, st));
+  GLR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_out, idx, perm, (int)n, 0, 32, st));
   count_launch(4);
-  if (EDGES) {
-    gather_edges_kernel<<<grid_of(len), 256, 0, st>>>(
-        reinterpret_cast<const longlong2 *>(d_edges), perm, len,
-        reinterpret_cast<longlong2 *>(d_out));
-    GLR_LAUNCHED("gather_edges_kernel");
-  } else {
-    gather_xy_kernel<<<grid_of(len), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), perm,
-                                                  len, reinterpret_cast<double2 *>(d_out));
-    GLR_LAUNCHED("gather_xy_kernel");
-  }
+  gather_xy_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), perm, n,
+                                               reinterpret_cast<double2 *>(d_out));
+  GLR_LAUNCHED("gather_xy_kernel");
   return GLR_OK;
 }
 
-int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+template <bool BOX>
+int keyed_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
                int64_t hub_degree, int64_t *d_out, cudaStream_t st) {
   if (m <= 1) {
     if (m == 1) GLR_CUDA(cudaMemcpyAsync(d_out, d_edges, 16, cudaMemcpyDeviceToDevice, st));
     return GLR_OK;
   }
-  int end_bit = 32;
-  while (end_bit < 64 && ((unsigned long long)(n + 1) >> (end_bit - 32)) != 0) ++end_bit;
+  const int low = BOX ? 33 : 32;  // key bits below the group
+  int end_bit = low;
+  while (end_bit < 64 && ((unsigned long long)(n + 1) >> (end_bit - low)) != 0) ++end_bit;
   size_t t_sort = 0;
   GLR_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const unsigned long long *)nullptr,
                                            (unsigned long long *)nullptr, (const int *)nullptr,
@@ -236,7 +250,7 @@ int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
   const size_t a8 = ((size_t)m * 8 + 255) & ~(size_t)255;
   const size_t a4 = ((size_t)m * 4 + 255) & ~(size_t)255;
   const size_t an = ((size_t)n * 4 + 255) & ~(size_t)255;
-  Scratch scr(2 * a8 + 2 * a4 + an + t_sort, st);
+  Scratch scr(2 * a8 + 2 * a4 + an + 256 + t_sort, st);
   GLR_CUDA(scr.err);
   char *p = scr.as<char>();
   auto *keys = reinterpret_cast<unsigned long long *>(p);
@@ -244,14 +258,27 @@ int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
   int *idx = reinterpret_cast<int *>(p + 2 * a8);
   int *perm = reinterpret_cast<int *>(p + 2 * a8 + a4);
   int *deg = reinterpret_cast<int *>(p + 2 * a8 + 2 * a4);
-  void *tmp = p + 2 * a8 + 2 * a4 + an;
+  unsigned long long *b = reinterpret_cast<unsigned long long *>(p + 2 * a8 + 2 * a4 + an);
+  void *tmp = p + 2 * a8 + 2 * a4 + an + 256;
   const auto *e2 = reinterpret_cast<const longlong2 *>(d_edges);
   GLR_CUDA(cudaMemsetAsync(deg, 0, (size_t)n * 4, st));
   degree_kernel<<<grid_of(m), 256, 0, st>>>(e2, m, deg);
   GLR_LAUNCHED("degree_kernel");
-  edge_theta_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2,
-                                                     m, deg, hub_degree, keys, idx);
-  GLR_LAUNCHED("edge_theta_keys_kernel");
+  if (BOX) {
+    GLR_CUDA(cudaMemsetAsync(b, 0xff, 8, st));
+    GLR_CUDA(cudaMemsetAsync(b + 1, 0x00, 8, st));
+    GLR_CUDA(cudaMemsetAsync(b + 2, 0xff, 8, st));
+    GLR_CUDA(cudaMemsetAsync(b + 3, 0x00, 8, st));
+    bounds_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n, b);
+    GLR_LAUNCHED("bounds_kernel");
+    edge_box_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2,
+                                                     m, b, deg, hub_degree, keys, idx);
+    GLR_LAUNCHED("edge_box_keys_kernel");
+  } else {
+    edge_theta_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),
+                                                       e2, m, deg, hub_degree, keys, idx);
+    GLR_LAUNCHED("edge_theta_keys_kernel");
+  }
   size_t tb = t_sort;
   GLR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_out, idx, perm, (int)m, 0, end_bit,
                                            st));
@@ -259,6 +286,15 @@ int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
   gather_edges_kernel<<<grid_of(m), 256, 0, st>>>(e2, perm, m, reinterpret_cast<longlong2 *>(d_out));
   GLR_LAUNCHED("gather_edges_kernel");
   return GLR_OK;
+}
+
+int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+               int64_t hub_degree, int64_t *d_out, cudaStream_t st) {
+  return keyed_sort<false>(d_xy, n, d_edges, m, hub_degree, d_out, st);
+}
+int box_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
+             int64_t hub_degree, int64_t *d_out, cudaStream_t st) {
+  return keyed_sort<true>(d_xy, n, d_edges, m, hub_degree, d_out, st);
 }
 
 }  // namespace
@@ -273,7 +309,12 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
     glr::set_error("glr_spatial_sort_edges: invalid arguments");
     return GLR_EARG;
   }
-  return glr::spatial_sort<true>(d_xy, n, d_edges, m, d_edges_out, glr::as_stream(stream));
+  if (n >= ((int64_t)1 << 31)) {
+    glr::set_error("glr_spatial_sort_edges: invalid arguments");
+    return GLR_EARG;
+  }
+  return glr::box_sort(d_xy, n, d_edges, m, GLR_HUB_DEGREE_DEFAULT, d_edges_out,
+                       glr::as_stream(stream));
 }
 
 int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
@@ -292,7 +333,7 @@ int glr_spatial_sort_vertices(const double *d_xy, int64_t n, double *d_xy_out, v
     glr::set_error("glr_spatial_sort_vertices: invalid arguments");
     return GLR_EARG;
   }
-  return glr::spatial_sort<false>(d_xy, n, nullptr, n, d_xy_out, glr::as_stream(stream));
+  return glr::vertex_sort(d_xy, n, d_xy_out, glr::as_stream(stream));
 }
 
 }  // extern "C"

@@ -19,13 +19,17 @@ live in HBM.  The arithmetic runs in the hand-written sm_100a kernels of
 
 Each all-pairs metric takes a keyword-only ``strategy``:
 
-* ``"dense"`` -- every tile pair of the upper triangle (the FP64-roofline
-  kernel; edges in input order so runs sharing a first endpoint reuse terms);
-* ``"culled"`` -- elements reordered by Morton code, only tile pairs whose
-  tile bounding boxes can interact are scanned (exactly the same result;
-  orders of magnitude fewer pair tests on spatially local inputs);
+* ``"dense"`` -- every tile pair of the upper triangle (the roofline-judged
+  kernel; with an ideal angle the edges are put in direction order with hub
+  groups, see ``CrossingRecords``);
+* ``"culled"`` -- elements reordered by Morton code (vertices: position;
+  edges: the 4-D code of the bbox sides, with hub groups), only tile pairs
+  whose tile bounding boxes can interact are scanned (exactly the same
+  result; orders of magnitude fewer pair tests on spatially local inputs,
+  40% fewer on C5's long random edges);
 * ``"auto"`` (default) -- culled when the candidate tile pairs are at most
-  ``CULL_FRACTION`` of all tile pairs, dense otherwise.
+  ``CULL_FRACTION`` (occlusion) / ``CROSS_CULL_FRACTION`` (crossing) of all
+  tile pairs, dense otherwise.
 """
 
 from __future__ import annotations
@@ -41,7 +45,11 @@ from . import _lib
 from .model import IDEAL_ANGLE_DEFAULT, ParameterError, check_ideal_angle, check_radius
 
 STRATEGIES = ("auto", "dense", "culled")
-CULL_FRACTION = 0.25      # auto: cull when candidates <= this share of tile pairs
+CULL_FRACTION = 0.25      # auto (occlusion): cull when candidates <= this share of tile pairs
+# auto (crossing): a culled unit costs about as much as a dense one (the
+# dense pass has the one-DADD angle in most units, the culled list does not,
+# but needs no band order); C5 keeps 60% of the tile pairs: 3.2 s vs 5.1 s
+CROSS_CULL_FRACTION = 0.75
 AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
 # theta order: vertices of at least this degree get their own edge group
 # (glr_theta_sort_edges; 0 = the library default).  Tuning knob only.
@@ -226,7 +234,7 @@ class CrossingRecords:
                        "glr_spatial_sort_edges")
             self._prepare(dg.xy, es)
             lst = _candidates(L.glr_crossing_candidates, _ptr(self.buf), self.n, self.m)
-            if strategy == "culled" or len(lst) <= CULL_FRACTION * crossing_units(self.m):
+            if strategy == "culled" or len(lst) <= CROSS_CULL_FRACTION * crossing_units(self.m):
                 self.list = lst
                 return
         if order == "theta" and self.m >= 2:

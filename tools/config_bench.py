@@ -34,7 +34,7 @@ def run(k):
     dg = M.DeviceGraph.from_graph(g)
     m, n = g.num_edges, g.num_vertices
     res = {"config": k, "n": n, "m": m, "gen_s": round(gen, 2)}
-    for strat in ("auto", "dense") if k != 5 else ("auto",):
+    for strat in ("auto", "dense") if k != 5 else ("auto", "culled"):
         def cross():
             rec = M.CrossingRecords(dg, strat)
             if os.environ.get("GLR_BENCH_MODE"):  # force a pair-kernel mode (0/1/2)
