@@ -64,6 +64,13 @@ def test_argument_errors_reported_without_gpu(L):
     assert b"invalid" in L.glr_last_error()
     rc = L.glr_occlusion_count(None, -1, 1.0, 0, 1, None, None)
     assert rc == _lib.GLR_EARG
+    # edge orders (direction / 4-D bbox Morton): null buffers, > 2^31 edges
+    rc = L.glr_theta_sort_edges(None, 10, None, 5, 0, None, None)
+    assert rc == _lib.GLR_EARG and b"glr_theta_sort_edges" in L.glr_last_error()
+    rc = L.glr_theta_sort_edges(None, 10, None, 1 << 31, 0, None, None)
+    assert rc == _lib.GLR_EARG
+    rc = L.glr_spatial_sort_edges(None, 10, None, 5, None, None)
+    assert rc == _lib.GLR_EARG and b"glr_spatial_sort_edges" in L.glr_last_error()
 
 
 def test_product_path_fails_loudly_without_gpu():

@@ -268,3 +268,39 @@ def test_theta_order_shift_classes(gpu, name):
         assert sum(int(p[0]) for p in parts) == cw
         assert strict_close(sum(p[1] for p in parts), dw)
     assert M._crossing_scan(g, IDEAL)[0] == S.crossing_scan(g.xy, g.edges, IDEAL)[0]
+
+
+def star_graphs(seed=12):
+    """Hubs only: one star (every pair shares the centre: E_c = 0, E_ca = 1)
+    and two interleaved stars whose spokes cross each other."""
+    rng = np.random.default_rng(seed)
+    n = 3000
+    xy = rng.uniform(0, 1, (n, 2))
+    one = np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1)
+    two = np.concatenate([np.stack([np.zeros(1499, np.int64), np.arange(2, 1501)], 1),
+                          np.stack([np.ones(1499, np.int64), np.arange(1501, 3000)], 1)])
+    return (xy, one), (xy, two)
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_star_tiles_skip_exactly(gpu, which):
+    """Units of two star tiles of one vertex are skipped (crossing.cu
+    TileBox.star): dense input order, direction order with hub groups
+    (2,999 spokes > the hub degree) and the culled plan all equal the
+    oracle."""
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import metrics as M
+
+    g = _graph(*star_graphs()[which])
+    dg = M.DeviceGraph.from_graph(g)
+    cw, dw = S.crossing_scan(g.xy, g.edges, IDEAL)
+    if which == 0:
+        assert cw == 0
+    for strategy, order in (("dense", "input"), ("dense", "theta"), ("culled", "input")):
+        rec = M.CrossingRecords(dg, strategy, order)
+        c, d = rec.partial(IDEAL, 0, rec.units).tolist()
+        assert int(c) == cw and strict_close(d, dw), (strategy, order)
+        c0, _ = rec.partial(None, 0, rec.units).tolist()
+        assert int(c0) == cw
+    assert M.edge_crossing_angle(g, IDEAL) == pytest.approx(
+        1.0 if cw == 0 else 1.0 - (dw / IDEAL) / cw, rel=1e-9)
