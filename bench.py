@@ -49,6 +49,10 @@ FP64_PER_PAIR_NC = 5
 # (theta_i + s)| and the accumulate; units straddling 0 or pi/2 of theta
 # difference, ~1e-4 of them on C5, take 4).
 FMA_PER_PAIR = 10
+# SASS instructions per pair of the hot block of cross_filter_kernel<angle>
+# in classified units (201 per 16 pairs, tools/sass_loop.py): the issue-slot
+# bound is 4 schedulers x 32 lanes x 148 SMs x clock / this.
+SASS_PER_PAIR = 201 / 16
 FP64_PER_PAIR_FILTER_ECA = 2
 FMA_LANES_PER_CLK_SM = 128   # measured 124 (FFMA2/FMUL2/FADD2, profiles/r01_packed.txt)
 FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
@@ -479,6 +483,11 @@ def main():
                      # (profiles/r01_dram_c5_filter.txt); per-rank share for N>1.
                      "traffic": C5_DRAM_BYTES_PER_LAUNCH / world,
                      "traffic_unit": "bytes/launch (dram__bytes_read+write, ncu)",
+                     # the binding resource per ncu (FMA pipe ~49% busy): issue slots
+                     "issue_bound": {"sass_per_pair": SASS_PER_PAIR,
+                                     "pairs_per_s": 4 * 32 * 148 * sm_mhz * 1e6 / SASS_PER_PAIR,
+                                     "frac": pair_rate / (4 * 32 * 148 * sm_mhz * 1e6
+                                                          / SASS_PER_PAIR)},
                      "algorithmic_bytes": REC_BYTES_PER_EDGE * m},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
