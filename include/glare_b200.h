@@ -139,7 +139,7 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
 /* Writes to d_edges_out the edge list reordered by (hub group, 4-D Morton
  * code of the edge's bbox sides xmin, xmax, ymin, ymax, diagonal orientation)
  * -- rows unchanged, only their order; hub groups as in
- * glr_theta_sort_edges.  The metrics do not depend on edge order; tiles
+ * glr_theta_sort_edges, for vertices of degree >= 16384.  The metrics do not depend on edge order; tiles
  * compact in all four sides let glr_crossing_candidates skip most tile
  * pairs of short-edge graphs and ~40% of them for long random edges. */
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
@@ -153,7 +153,9 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
  * pair in units whose theta difference stays on one side of 0 and pi/2
  * (crossing.cu unit_shift), and skip units of two tiles of one hub's edges
  * (every pair shares the hub).  Results do not depend on the order. */
+#ifndef GLR_HUB_DEGREE_DEFAULT
 #define GLR_HUB_DEGREE_DEFAULT 1024
+#endif
 int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                          int64_t m, int64_t hub_degree, int64_t *d_edges_out, void *stream);
 

@@ -159,6 +159,14 @@ __global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
 
 int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
                int64_t hub_degree, int64_t *d_out, cudaStream_t st);
+// Hub degree of the culled (4-D bbox) order: a hub group's tiles have boxes
+// anchored at the hub, so only hubs whose shared-vertex pairs would cost more
+// fallbacks than their boxes cost candidate units get a group (C5 culled:
+// 3.70 s at 256, 3.19 s at 1024, 2.98 s at 4096, 2.92 s at 16384, 3.05 s
+// with none; tools/cull_probe.py).
+#ifndef GLR_BOX_HUB_DEGREE
+#define GLR_BOX_HUB_DEGREE 16384
+#endif
 int box_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
              int64_t hub_degree, int64_t *d_out, cudaStream_t st);
 
@@ -313,7 +321,7 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
     glr::set_error("glr_spatial_sort_edges: invalid arguments");
     return GLR_EARG;
   }
-  return glr::box_sort(d_xy, n, d_edges, m, GLR_HUB_DEGREE_DEFAULT, d_edges_out,
+  return glr::box_sort(d_xy, n, d_edges, m, GLR_BOX_HUB_DEGREE, d_edges_out,
                        glr::as_stream(stream));
 }
 
