@@ -141,7 +141,7 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
  * -- rows unchanged, only their order; hub groups as in
  * glr_theta_sort_edges, for vertices of degree >= 16384.  The metrics do not depend on edge order; tiles
  * compact in all four sides let glr_crossing_candidates skip most tile
- * pairs of short-edge graphs and ~40% of them for long random edges. */
+ * pairs of short-edge graphs and ~46% of them for long random edges. */
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                            int64_t m, int64_t *d_edges_out, void *stream);
 

@@ -26,7 +26,7 @@ Each all-pairs metric takes a keyword-only ``strategy``:
   edges: the 4-D code of the bbox sides, with hub groups), only tile pairs
   whose tile bounding boxes can interact are scanned (exactly the same
   result; orders of magnitude fewer pair tests on spatially local inputs,
-  40% fewer on C5's long random edges);
+  46% fewer on C5's long random edges);
 * ``"auto"`` (default) -- culled when the candidate tile pairs are at most
   ``CULL_FRACTION`` (occlusion) / ``CROSS_CULL_FRACTION`` (crossing) of all
   tile pairs, dense otherwise.
@@ -48,7 +48,7 @@ STRATEGIES = ("auto", "dense", "culled")
 CULL_FRACTION = 0.25      # auto (occlusion): cull when candidates <= this share of tile pairs
 # auto (crossing): a culled unit costs about as much as a dense one (the
 # dense pass has the one-DADD angle in most units, the culled list does not,
-# but needs no band order); C5 keeps 60% of the tile pairs: 3.2 s vs 5.1 s
+# but needs no band order); C5 keeps 54% of the tile pairs: 2.9 s vs 5.1 s
 CROSS_CULL_FRACTION = 0.75
 AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
 # theta order: vertices of at least this degree get their own edge group
