@@ -134,7 +134,13 @@ int glr_crossing_pairs_interleaved(const void *d_records, int64_t n, int64_t m,
 int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
                               double beta, double *d_w, void *stream);
 
-/* ---- culled variants (results identical) ---------- */
+/* ---- culled variants (results identical) ---------- *
+ * The GPU form of the reference oracle's own pruning: exact.py:170-199 sorts
+ * edges by xmin and skips pairs whose x-ranges are disjoint (they fail the
+ * closed-bbox test of exact.py:191-194); node_occlusion_grid
+ * (metrics/enhanced.py:42-127) buckets vertices so only neighbouring cells
+ * are compared.  Here whole tile pairs are skipped when their boxes are
+ * disjoint (crossing) or farther apart than 2r (occlusion). */
 
 /* Writes to d_edges_out the edge list reordered by (hub group, 4-D Morton
  * code of the edge's bbox sides xmin, xmax, ymin, ymax, diagonal orientation)
