@@ -304,3 +304,21 @@ def test_star_tiles_skip_exactly(gpu, which):
         assert int(c0) == cw
     assert M.edge_crossing_angle(g, IDEAL) == pytest.approx(
         1.0 if cw == 0 else 1.0 - (dw / IDEAL) / cw, rel=1e-9)
+
+
+@pytest.mark.parametrize("strategy,order", [("dense", "theta"), ("dense", "input"),
+                                            ("culled", "input")])
+def test_repeatable_bit_for_bit(gpu, strategy, order):
+    """Slices go to warps dynamically and uncertain pairs are queued per warp,
+    yet count and dev_sum are identical bit for bit across runs (integer
+    counts, per-slice 2^-50 fixed-point angle sums, queue order fixed by the
+    slice)."""
+    from paper_2411_09809_b200 import metrics as M
+
+    g = _graph(*uniform_long(seed=13, n=5000, m=30000))
+    dg = M.DeviceGraph.from_graph(g)
+    runs = []
+    for _ in range(3):
+        rec = M.CrossingRecords(dg, strategy, order)
+        runs.append(tuple(rec.partial(IDEAL, 0, rec.units).tolist()))
+    assert runs[0] == runs[1] == runs[2], runs
