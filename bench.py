@@ -405,8 +405,8 @@ def main():
     peak_max = FMA_LANES_PER_CLK_SM * 148 * 1965e6 / 1e12
     achieved = FMA_PER_PAIR * pair_rate / 1e12
     fp64_peak_run = FP64_LANES_PER_CLK_SM * 148 * sm_mhz * 1e6 / 1e12
-    cpu = None
-    if not args.no_cpu_baseline:
+    cpu = None  # the CPU reference sample runs on rank 0 at N=1 only
+    if not args.no_cpu_baseline and world == 1:
         from oracle import sweep as S
 
         threads = S.default_threads()
