@@ -322,3 +322,20 @@ def test_repeatable_bit_for_bit(gpu, strategy, order):
         rec = M.CrossingRecords(dg, strategy, order)
         runs.append(tuple(rec.partial(IDEAL, 0, rec.units).tolist()))
     assert runs[0] == runs[1] == runs[2], runs
+
+
+@pytest.mark.parametrize("hub", [1, 2, 64, 10**9])
+def test_theta_order_hub_degree_is_only_an_order(gpu, hub, monkeypatch):
+    """glr_theta_sort_edges' hub groups (every edge grouped by its
+    higher-degree endpoint at hub degree 1, none at 10^9) change the edge
+    order only: counts exact and dev_sum within 1e-9 of the oracle."""
+    from oracle import sweep as S
+    from paper_2411_09809_b200 import metrics as M
+
+    monkeypatch.setattr(M, "HUB_DEGREE", hub)
+    g = _graph(*hubs())
+    dg = M.DeviceGraph.from_graph(g)
+    cw, dw = S.crossing_scan(g.xy, g.edges, IDEAL)
+    rec = M.CrossingRecords(dg, "dense", "theta")
+    c, d = rec.partial(IDEAL, 0, rec.units).tolist()
+    assert int(c) == cw and strict_close(d, dw)
