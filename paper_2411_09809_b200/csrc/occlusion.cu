@@ -261,12 +261,16 @@ template <bool DIAG>
 __device__ __forceinline__ void occ_filter_block(const uint64_t (&X)[kK / 2],
                                                  const uint64_t (&Y)[kK / 2], const float2 *sj,
                                                  int jj0, const OccHeader &H, uint64_t NTLO2,
-                                                 uint64_t NHALF2, float vote_w,
+                                                 unsigned vote_bits,
                                                  const double2 *__restrict__ xy, int64_t ibase,
                                                  int64_t jbase, int64_t n,
                                                  unsigned long long thr_bits,
                                                  unsigned (&cnt)[kK]) {
-  float m = INFINITY;  // min over the block of |(S - tlo) - halfwidth|
+  // min over the block of d = S - tlo viewed as unsigned: a non-negative
+  // float orders like its bit pattern and a negative one (certain hit) is
+  // above every non-negative, so one VIMNMX3 per two pairs finds whether any
+  // d lies in [0, RU(thi - tlo)] -- a superset of the uncertain band
+  unsigned m = 0xffffffffu;
 #pragma unroll
   for (int q = 0; q < kOccFBlock; ++q) {
     float S[kK];
@@ -276,14 +280,15 @@ __device__ __forceinline__ void occ_filter_block(const uint64_t (&X)[kK / 2],
       // d = S - tlo (packed): S < tlo exactly when d's sign bit is set (RN
       // keeps the sign of the difference; d is +0 when S == tlo)
       const uint64_t d = o2_sub(o2_pack(S[2 * g], S[2 * g + 1]), NTLO2);
-      cnt[2 * g] += __float_as_uint(o2_lo(d)) >> 31;
-      cnt[2 * g + 1] += __float_as_uint(o2_hi(d)) >> 31;
-      // uncertain band [tlo, thi] <=> d in [0, thi - tlo] <=> |d - half| <= half
-      const uint64_t e = o2_sub(d, NHALF2);
-      m = fminf(m, fminf(fabsf(o2_lo(e)), fabsf(o2_hi(e))));
+      const unsigned dlo = __float_as_uint(o2_lo(d)), dhi = __float_as_uint(o2_hi(d));
+      cnt[2 * g] += dlo >> 31;
+      cnt[2 * g + 1] += dhi >> 31;
+      // uncertain band [tlo, thi] => RN(S - tlo) in [+0, RN(thi - tlo)] (RN is
+      // monotone and S - tlo = +0 at S = tlo)
+      m = min(m, min(dlo, dhi));
     }
   }
-  if (__any_sync(0xffffffffu, m <= vote_w)) {
+  if (__any_sync(0xffffffffu, m <= vote_bits)) {
 #pragma unroll 1
     for (int q = 0; q < kOccFBlock; ++q) {
       float S[kK];
@@ -312,11 +317,9 @@ occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict
                         unsigned long long thr_bits, unsigned long long *__restrict__ cta_cnt) {
   if (!hdr->use) return;
   const OccHeader H = *hdr;
-  // packed constants: tlo, and half the band width (rounded up); the vote
-  // threshold is widened further so rounding of d - half never hides a pair
-  const float half = __fmul_ru(__fsub_ru(H.thi, H.tlo), 0.5f);
-  const uint64_t NTLO2 = o2_pack(H.tlo, H.tlo), NHALF2 = o2_pack(half, half);
-  const float vote_w = __fadd_ru(__fmul_ru(half, 1.0f + 0x1p-20f), 0x1p-120f);
+  // packed constant tlo; vote bound = the band width rounded up, as bits
+  const uint64_t NTLO2 = o2_pack(H.tlo, H.tlo);
+  const unsigned vote_bits = __float_as_uint(__fsub_ru(H.thi, H.tlo));
   __shared__ __align__(16) float2 sj[kTile];
   __shared__ unsigned long long red[kThreads / 32];
   const uint64_t span = uend - ubeg;
@@ -358,12 +361,12 @@ occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kOccFBlock)
-        occ_filter_block<true>(X, Y, sj, jj, H, NTLO2, NHALF2, vote_w, xy, ibase, jbase, n,
+        occ_filter_block<true>(X, Y, sj, jj, H, NTLO2, vote_bits, xy, ibase, jbase, n,
                                thr_bits, cnt);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kOccFBlock)
-        occ_filter_block<false>(X, Y, sj, jj, H, NTLO2, NHALF2, vote_w, xy, ibase, jbase, n,
+        occ_filter_block<false>(X, Y, sj, jj, H, NTLO2, vote_bits, xy, ibase, jbase, n,
                                 thr_bits, cnt);
     }
     unsigned c = 0;
