@@ -885,9 +885,19 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
   return v;
 }
 
-template <bool DIAG>
+// FOLD (count-only kernel): M_k = max(RN(c1 c2 + t), RN(c3 c4 + t)) with
+// the unit threshold t folded into the products' FFMA (RN keeps the sign of
+// the exact value and is monotone; t and 2t are floats): M < 0 <=> both
+// exact products < -t (certain hit), M > 2t => one exact product > t
+// (certain miss), M in [0, 2t] uncertain -- the partition of
+// max(RN(c1 c2), RN(c3 c4)) against -t and t, but the hit is M's sign bit
+// (one LEA.HI) and the vote an unsigned minimum.  Masked pairs of a
+// diagonal tile get M = 4 (t <= 1).  The fused kernel keeps FMUL2 products
+// (its SEL needs a predicate anyway, and the third FFMA2 operand cost it
+// 5%: 5.34 vs 5.08 s on C5).
+template <bool DIAG, bool FOLD>
 __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj, int islot,
-                                         float (&M)[kFK]) {
+                                         uint64_t T2, float (&M)[kFK]) {
   const float4 q0 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec));       // cx cy dx dy
   const float4 q1 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec) + 16);  // scdx -scdy -skc
   const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
@@ -900,14 +910,15 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
     const uint64_t c2 = f2_fma(R.sabx[g], DY, f2_fma(R.nsaby[g], DX, R.nska[g]));
     const uint64_t c3 = f2_fma(SCDX, R.ay[g], f2_fma(NSCDY, R.ax[g], NSKC));
     const uint64_t c4 = f2_fma(SCDX, R.by[g], f2_fma(NSCDY, R.bx[g], NSKC));
-    const uint64_t p12 = f2_mul(c1, c2), p34 = f2_mul(c3, c4);
+    const uint64_t p12 = FOLD ? f2_fma(c1, c2, T2) : f2_mul(c1, c2);
+    const uint64_t p34 = FOLD ? f2_fma(c3, c4, T2) : f2_mul(c3, c4);
     M[2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
     M[2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
   }
   if (DIAG) {
 #pragma unroll
     for (int k = 0; k < kFK; ++k)
-      if (!(jj > islot + 32 * k)) M[k] = 2.0f;
+      if (!(jj > islot + 32 * k)) M[k] = FOLD ? 4.0f : 2.0f;
   }
 }
 
@@ -960,24 +971,33 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
                                              int64_t jbase, unsigned short *wq, unsigned &qn) {
+  constexpr bool FOLD = !ANGLE;
+  const uint64_t T2 = f2_bcast(thr);
+  // FOLD: uncertain <=> M in [+0, 2t] <=> M's bits <= 2t's bits (unsigned: a
+  // negative M, a certain hit, lies above every non-negative float), so the
+  // block vote is one unsigned minimum (VIMNMX3 per two pairs)
+  const unsigned vbits = __float_as_uint(2.0f * thr);
+  unsigned mmin = 0xffffffffu;
   bool any = false;
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
     float M[kFK];
-    filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
+    filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
 #pragma unroll
     for (int k = 0; k < kFK; ++k) {
-      any |= fabsf(M[k]) <= thr;
-      // @(M < -1) cnt += 1 (and dev += t)
+      if (FOLD) {
+        mmin = min(mmin, __float_as_uint(M[k]));
+      } else {
+        any |= fabsf(M[k]) <= thr;
+      }
+      // hit: cnt += 1 (and dev += t)
       if (ANGLE) {
         // dev += hit ? t : 0 with t = |v|: a miss clears v's HIGH word only
         // (one SEL, in place), leaving {lo, 0}, a subnormal below 2^-1022.
-        // Nonzero deviations are >= 2^-53 (theta, pi/2 and kappa are all
-        // multiples of 2^-53 below 2), so such an addend never changes a
-        // sum that holds one, and
-        // the per-slice sum's 2^-50 fixed-point conversion drops it: the
-        // result equals the masked sum exactly (DADD, no zeroing MOV or
+        // Such an addend is absorbed by any sum holding a deviation above
+        // 2^-960, and the per-slice sum's 2^-50 fixed-point conversion drops
+        // it: the result equals the masked sum (DADD, no zeroing MOV or
         // {0,1} multiplier per pair).
         double v = SHIFT ? __dsub_rn(thj, th[k]) : angle_dev_signed(th[k], thj, kappa);
         asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
@@ -990,15 +1010,12 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
             : "f"(M[k]), "f"(-thr));
         dev[k % kDevAcc] = __dadd_rn(dev[k % kDevAcc], fabs(v));
       } else {
-        asm("{\n\t.reg .pred p;\n\t"
-            "setp.lt.f32 p, %1, %2;\n\t"
-            "@p add.u32 %0, %0, 1;\n\t}"
-            : "+r"(cnt[k % kCntAccCount])
-            : "f"(M[k]), "f"(-thr));
+        // the sign bit of M is the hit (LEA.HI: one instruction)
+        cnt[k % kCntAccCount] += __float_as_uint(M[k]) >> 31;
       }
     }
   }
-  if (__any_sync(0xffffffffu, any)) {
+  if (__any_sync(0xffffffffu, FOLD ? mmin <= vbits : any)) {
     // re-filter the block into a per-lane mask (bit q*kFK + k), then place
     // the lanes' entries by a warp prefix sum: positions depend only on lane
     // and bit order (deterministic), and the path has no vote per pair
@@ -1006,9 +1023,12 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
 #pragma unroll
     for (int q = 0; q < NJ; ++q) {
       float M[kFK];
-      filter_m<DIAG>(R, jaddr, jj0 + q, islot, M);
+      filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
 #pragma unroll
-      for (int k = 0; k < kFK; ++k) U |= (fabsf(M[k]) <= thr ? 1u : 0u) << (q * kFK + k);
+      for (int k = 0; k < kFK; ++k) {
+        const bool u = FOLD ? __float_as_uint(M[k]) <= vbits : fabsf(M[k]) <= thr;
+        U |= (u ? 1u : 0u) << (q * kFK + k);
+      }
     }
     const unsigned lane = (unsigned)islot & 31u;
     const unsigned n = __popc(U);
