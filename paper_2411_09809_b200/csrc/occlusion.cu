@@ -23,7 +23,10 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kK = 8;
 constexpr int kTile = kThreads * kK;
-constexpr int kMinBlocks = 4;
+#ifndef GLR_OMINB
+#define GLR_OMINB 4
+#endif
+constexpr int kMinBlocks = GLR_OMINB;  // CTAs per SM
 
 inline int64_t pad_vertices(int64_t n) { return ((n + kTile - 1) / kTile) * kTile; }
 
