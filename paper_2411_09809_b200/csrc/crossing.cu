@@ -103,6 +103,10 @@ constexpr int kStages = GLR_XFSTAGES;  // j-tile ring depth of the filter kernel
 constexpr int kFilterMinBlocksCount = GLR_XFMINB_C;
 
 
+// Largest edge count whose pair count m(m-1)/2 stays below 2^53, where the
+// float64 count slot of d_out is exact.
+constexpr int64_t kMaxExactEdges = (int64_t)1 << 27;
+
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
 constexpr double kMinAbsFast = 0x1p-160;
@@ -565,17 +569,21 @@ __device__ inline void load_i(IRegs<IDS> &R, const EdgeRec *__restrict__ rec,
 
 __device__ inline float hi_view(double c) { return __int_as_float(__double2hiint(c)); }
 
-// |ideal - min(d, pi - d)| with d = |t1 - t2|, written as
-// || pi/2 - d | - kappa|, kappa = pi/2 - ideal (4 DADD, no DMNMX).
+// ideal - min(d, pi - d) with d = |t1 - t2| (its absolute value is the
+// pair's deviation): the reference's own operation sequence
+// (geometry.py:107-110, exact.py:219-221), so every pair's deviation is
+// bit-identical to numpy's for the same axis angles.  For d in [0, pi]
+// (pi = 2 fl(pi/2) exactly), min(d, fl(pi - d)) == (d <= fl(pi/2) ? d :
+// fl(pi - d)) by monotone rounding: one compare instead of a NaN-aware min.
 // Symmetric in (t1, t2) bit for bit.
-__device__ inline double angle_dev_signed(double t1, double t2, double kappa) {
-  const double HALF_PI = 1.5707963267948966;
-  double d = __dsub_rn(t1, t2);
-  double e = __dsub_rn(HALF_PI, fabs(d));
-  return __dsub_rn(fabs(e), kappa);
+__device__ inline double angle_dev_signed(double t1, double t2, double ideal) {
+  const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
+  const double d = fabs(__dsub_rn(t1, t2));
+  const double a = d <= HALF_PI ? d : __dsub_rn(PI, d);
+  return __dsub_rn(ideal, a);
 }
-__device__ inline double angle_dev(double t1, double t2, double kappa) {
-  return fabs(angle_dev_signed(t1, t2, kappa));
+__device__ inline double angle_dev(double t1, double t2, double ideal) {
+  return fabs(angle_dev_signed(t1, t2, ideal));
 }
 
 // One j-edge against the thread's K i-edges.  FAST selects the float-view
@@ -585,7 +593,7 @@ __device__ inline double angle_dev(double t1, double t2, double kappa) {
 template <bool FAST, bool ANGLE, bool DIAG>
 __device__ inline void pair_row(const IRegs<!FAST> &R, const EdgeRec *sj, const double *sth,
                                 const int2 *sid, int jj, unsigned (&cnt)[kK],
-                                double (&dev)[kK], double kappa) {
+                                double (&dev)[kK], double ideal) {
   const double4 cq = reinterpret_cast<const double4 *>(sj + jj)[0];
   const double2 cdq = reinterpret_cast<const double2 *>(sj + jj)[2];
   const int4 rk = reinterpret_cast<const int4 *>(sj + jj)[3];
@@ -627,7 +635,7 @@ __device__ inline void pair_row(const IRegs<!FAST> &R, const EdgeRec *sj, const 
     }
     cnt[k] += hit ? 1u : 0u;
     if (ANGLE) {
-      const double t = angle_dev(R.th[k], thj, kappa);
+      const double t = angle_dev(R.th[k], thj, ideal);
       if (hit) dev[k] = __dadd_rn(dev[k], t);
     }
   }
@@ -684,7 +692,7 @@ __device__ inline void tail_count_dev(unsigned &cnt, double &dev, double t, int 
 template <bool ANGLE, bool DIAG>
 __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const EdgeRec *sj,
                                      const double *sth, const int *snew, int jj,
-                                     unsigned (&cnt)[kK], double (&dev)[kK], double kappa) {
+                                     unsigned (&cnt)[kK], double (&dev)[kK], double ideal) {
   const double4 cq = reinterpret_cast<const double4 *>(sj + jj)[0];
   const double2 cdq = reinterpret_cast<const double2 *>(sj + jj)[2];
   const int4 rk = reinterpret_cast<const int4 *>(sj + jj)[3];
@@ -716,7 +724,7 @@ __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const Edge
     (void)ok;
     const int diag_ok = DIAG ? (jj > (int)threadIdx.x + k * kThreads) : 1;
     if (ANGLE)
-      tail_count_dev(cnt[k], dev[k], angle_dev(R.th[k], thj, kappa), rk.y, R.rx0[k], R.rx1[k],
+      tail_count_dev(cnt[k], dev[k], angle_dev(R.th[k], thj, ideal), rk.y, R.rx0[k], R.rx1[k],
                      rk.x, rk.w, R.ry0[k], R.ry1[k], rk.z, p12, p34, diag_ok);
     else
       tail_count(cnt[k], rk.y, R.rx0[k], R.rx1[k], rk.x, rk.w, R.ry0[k], R.ry1[k], rk.z, p12,
@@ -725,7 +733,7 @@ __device__ inline void pair_row_fast(const IRegs<false> &R, SRegs &S, const Edge
     const bool hit = ok & (p12 <= 0.0f) & (p34 <= 0.0f);
     cnt[k] += hit ? 1u : 0u;
     if (ANGLE) {
-      const double t = angle_dev(R.th[k], thj, kappa);
+      const double t = angle_dev(R.th[k], thj, ideal);
       if (hit) dev[k] = __dadd_rn(dev[k], t);
     }
 #endif
@@ -812,26 +820,42 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
   }
 }
 
-// Angle deviation of a unit whose theta difference dt = theta_j - theta_i
-// keeps one side of 0 and of +-pi/2 for every pair (tile theta bounds, e.g.
-// after glr_theta_sort_edges): a = min(|dt|, pi - |dt|) is then one affine
-// branch and |ideal - a| = |theta_j - (theta_i + s)| with
+// Signed units.  If a unit's theta difference dt = theta_j - theta_i keeps
+// one side of 0 and of +-pi/2 for every pair (tile theta bounds, e.g. after
+// glr_theta_sort_edges), a = min(|dt|, pi - |dt|) is one affine branch and
+// |ideal - a| = |theta_j - (theta_i + s)| with
 //   dt in [0, pi/2]: s = ideal          dt in [pi/2, pi): s = pi - ideal
-//   dt in [-pi/2, 0]: s = -ideal        dt in (-pi, -pi/2]: s = ideal - pi,
-// ONE DADD per pair instead of three (angle_dev).  Returns 0 (shift s in
-// *s) or -1 for a unit that straddles a branch point (general formula).
-// Rounding differs from exact.py's by a few ulps of pi per pair: inside the
-// 1e-9 relative tolerance by nine orders of magnitude.
-__device__ inline int unit_shift(const TileBox &a, const TileBox &b, double ideal, double *s) {
+//   dt in [-pi/2, 0]: s = -ideal        dt in (-pi, -pi/2]: s = ideal - pi.
+// If the dt range also keeps kSignMargin away from s (return 1), every
+// pair's v = theta_j - (theta_i + s) has the sign *sigma, and the lane's
+// deviation sum over hits is
+//   sigma * (sum_j h_j theta_j - sum_k C_k x_k),  x_k = theta_i_k + s,
+// with h_j the lane's hits on j-edge j and C_k those of i-edge k: one DFMA
+// per j-edge (4 pairs) instead of the per-pair formula.  Rounding: the sum
+// of at most kTile terms of at most kFK pi each loses <= kTile kFK pi 2^-53
+// per hit, against a deviation of >= kSignMargin per hit: relative error
+// <= 256 * 4 pi 2^-53 / 2^-8 < 1e-10 (tests/test_filter_bound.py).  Every
+// other unit (0: within the margin of s; -1: straddles a branch point)
+// evaluates the reference's per-pair formula (angle_dev), so small
+// deviations are bit-identical to numpy's.
+constexpr double kSignMargin = 0x1p-8;
+__device__ inline int unit_shift(const TileBox &a, const TileBox &b, double ideal, double *s,
+                                 double *sigma) {
   const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
-  // float bounds are outward-rounded; double differences of floats are exact
+  // float bounds are outward-rounded; their double differences are exact
+  // or off by far less than kSignMargin
   const double lo = (double)b.thlo - (double)a.thhi, hi = (double)b.thhi - (double)a.thlo;
   if (!(lo <= hi)) return -1;  // empty tile
-  if (lo >= 0.0 && hi <= HALF_PI) { *s = ideal; return 0; }
-  if (lo >= HALF_PI) { *s = __dsub_rn(PI, ideal); return 0; }
-  if (hi <= 0.0 && lo >= -HALF_PI) { *s = -ideal; return 0; }
-  if (hi <= -HALF_PI) { *s = __dsub_rn(ideal, PI); return 0; }
-  return -1;
+  double sh;
+  if (lo >= 0.0 && hi <= HALF_PI) sh = ideal;
+  else if (lo >= HALF_PI) sh = __dsub_rn(PI, ideal);
+  else if (hi <= 0.0 && lo >= -HALF_PI) sh = -ideal;
+  else if (hi <= -HALF_PI) sh = __dsub_rn(ideal, PI);
+  else return -1;
+  *s = sh;
+  if (hi <= sh - kSignMargin) { *sigma = -1.0; return 1; }
+  if (lo >= sh + kSignMargin) { *sigma = 1.0; return 1; }
+  return 0;
 }
 
 // Exact reference predicate for one pair (general semantics: doubles
@@ -841,7 +865,7 @@ template <bool ANGLE>
 __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ei,
-                                             int64_t ej, double kappa) {
+                                             int64_t ej, double ideal) {
   const EdgeRec a = rec[ei], c = rec[ej];
   const int2 ia = ids[ei], ic = ids[ej];
   bool ok = (c.rxmax >= a.rxmin) & (a.rxmax >= c.rxmin) & (c.rymax >= a.rymin) &
@@ -860,7 +884,7 @@ __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
   const bool s_cd = ((c1 <= 0.0) & (c2 >= 0.0)) | ((c1 >= 0.0) & (c2 <= 0.0));
   const bool s_ab = ((c3 <= 0.0) & (c4 >= 0.0)) | ((c3 >= 0.0) & (c4 <= 0.0));
   if (!(ok & s_cd & s_ab)) return -1.0;
-  return ANGLE ? angle_dev(theta[ei], theta[ej], kappa) : 0.0;
+  return ANGLE ? angle_dev(theta[ei], theta[ej], ideal) : 0.0;
 }
 
 // M_k = max(P12, P34) of one j-edge (shared memory) against the thread's K
@@ -912,6 +936,18 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
     const uint64_t c4 = f2_fma(SCDX, R.by[g], f2_fma(NSCDY, R.bx[g], NSKC));
     const uint64_t p12 = FOLD ? f2_fma(c1, c2, T2) : f2_mul(c1, c2);
     const uint64_t p34 = FOLD ? f2_fma(c3, c4, T2) : f2_mul(c3, c4);
+#ifndef GLR_XFMNMX
+    if (FOLD) {
+      // the signed-integer maximum of the bit patterns (ALU pipe; FMNMX
+      // competes with FFMA2): it equals max(P12, P34) when either is
+      // non-negative, and is negative (sign bit set) when both are -- all
+      // FOLD's hit (sign bit) and uncertain (bits in [+0, 2t]) tests read
+      M[2 * g] = __int_as_float(max(__float_as_int(f2_lo(p12)), __float_as_int(f2_lo(p34))));
+      M[2 * g + 1] =
+          __int_as_float(max(__float_as_int(f2_hi(p12)), __float_as_int(f2_hi(p34))));
+      continue;
+    }
+#endif
     M[2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
     M[2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
   }
@@ -930,19 +966,20 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
 constexpr unsigned kQCap = 512;  // queue entries per warp (>= 32 lanes x NJ x kFK)
+static_assert(kTile <= 256, "queue entries hold 8-bit tile slots");
 template <bool ANGLE>
 __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
                                          const EdgeRec *__restrict__ rec,
                                          const int2 *__restrict__ ids,
                                          const double *__restrict__ theta, int64_t ibase,
-                                         int64_t jbase, double kappa, unsigned &cnt,
+                                         int64_t jbase, double ideal, unsigned &cnt,
                                          double &dev) {
   __syncwarp();
   for (unsigned b = 0; b < qn; b += 32) {
     if (b + lane < qn) {
       const unsigned ent = wq[b + lane];  // i slot << 8 | j slot
       const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + (ent >> 8),
-                                         jbase + (ent & 255u), kappa);
+                                         jbase + (ent & 255u), ideal);
       if (t >= 0.0) {
         cnt += 1u;
         if (ANGLE) dev = __dadd_rn(dev, t);
@@ -962,16 +999,21 @@ __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned q
 // debug build only: [vote blocks that fell back, uncertain pairs evaluated]
 __device__ unsigned long long g_fstats[2];
 #endif
-template <bool ANGLE, bool DIAG, int NJ, bool SHIFT>
+// AM (angle mode of the unit): 0 the reference's per-pair formula
+// (angle_dev), 2 the signed form (unit_shift); the count-only kernel uses 0.
+template <bool ANGLE, bool DIAG, int NJ, int AM>
 __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)[kFK],
                                              unsigned jaddr,
                                              unsigned thaddr, int jj0, int islot, float thr,
                                              unsigned (&cnt)[kFK], double (&dev)[kFK],
-                                             double kappa, const EdgeRec *__restrict__ rec,
+                                             double (&A2)[2], double ideal,
+                                             const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
-                                             int64_t jbase, unsigned short *wq, unsigned &qn) {
-  constexpr bool FOLD = !ANGLE;
+                                             int64_t jbase, unsigned short *wq, unsigned &qn,
+                                             unsigned &qc, double &qd) {
+  constexpr bool SIGNED = ANGLE && AM == 2;
+  constexpr bool FOLD = !ANGLE || SIGNED;
   const uint64_t T2 = f2_bcast(thr);
   // FOLD: uncertain <=> M in [+0, 2t] <=> M's bits <= 2t's bits (unsigned: a
   // negative M, a certain hit, lies above every non-negative float), so the
@@ -984,6 +1026,27 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     float M[kFK];
     filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
+    if (SIGNED) {
+      // hits are M's sign bits: C_k += hit (LEA.HI), h = hits on this j-edge,
+      // A += h * theta_j (one DFMA per j-edge; unit_shift).  Short dependency
+      // chains: pairwise hit sums, two alternating A accumulators, and the
+      // vote minimum as a tree over the block (one chain per j-edge here).
+      unsigned b[kFK];
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) {
+        b[k] = __float_as_uint(M[k]);
+        cnt[k] += b[k] >> 31;
+      }
+      unsigned h = b[0] >> 31;
+#pragma unroll
+      for (int k = 1; k < kFK; ++k) h += b[k] >> 31;
+      A2[q & 1] = fma((double)h, thj, A2[q & 1]);
+      unsigned mq = b[0];
+#pragma unroll
+      for (int k = 1; k < kFK; ++k) mq = min(mq, b[k]);
+      mmin = q == 0 ? mq : min(mmin, mq);
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < kFK; ++k) {
       if (FOLD) {
@@ -994,12 +1057,12 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
       // hit: cnt += 1 (and dev += t)
       if (ANGLE) {
         // dev += hit ? t : 0 with t = |v|: a miss clears v's HIGH word only
-        // (one SEL, in place), leaving {lo, 0}, a subnormal below 2^-1022.
-        // Such an addend is absorbed by any sum holding a deviation above
-        // 2^-960, and the per-slice sum's 2^-50 fixed-point conversion drops
-        // it: the result equals the masked sum (DADD, no zeroing MOV or
-        // {0,1} multiplier per pair).
-        double v = SHIFT ? __dsub_rn(thj, th[k]) : angle_dev_signed(th[k], thj, kappa);
+        // (one SEL, in place), leaving {lo, 0}, a subnormal below 2^-1042.
+        // A genuine deviation is 0 or at least 2^-766, so the
+        // slice's sum is cleared when below 2^-900 and otherwise differs
+        // from the masked sum by a relative 2^-265 at most (DADD, no zeroing
+        // MOV or {0,1} multiplier per pair).
+        double v = angle_dev_signed(th[k], thj, ideal);
         asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
             "setp.lt.f32 p, %2, %3;\n\t"
             "@p add.u32 %0, %0, 1;\n\t"
@@ -1046,7 +1109,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     }
 #endif
     if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
-      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0], dev[0]);
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, qd);
       qn = 0;
     }
     unsigned pos = qn + incl - n;
@@ -1066,11 +1129,13 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                    const double *__restrict__ theta, const int2 *__restrict__ ids,
                    const int *__restrict__ newc, const int2 *__restrict__ ulist, uint64_t T,
                    uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk,
-                   unsigned srank, unsigned sworld, double kappa,
+                   unsigned srank, unsigned sworld, double ideal, int filter_ok,
                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
   // ulist == nullptr: units are the implicit upper triangle of tile pairs;
   // otherwise unit u is the explicit tile pair ulist[u] (culled candidates).
-  if (hdr->fast != (FAST ? 1 : 0)) return;
+  // The sign kernel also stands in for the filter when !filter_ok.
+  const int mode = (hdr->fast == kModeFilter && !filter_ok) ? kModeSign : hdr->fast;
+  if (mode != (FAST ? kModeSign : kModeGeneral)) return;
   constexpr bool IDS = !FAST;
   __shared__ __align__(16) EdgeRec sj[kTile];
   __shared__ double sth[ANGLE ? kTile : 1];
@@ -1128,20 +1193,20 @@ cross_pairs_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
     if constexpr (FAST) {
       if (ti == tj) {
         for (int jj = 0; jj < kTile; ++jj)
-          pair_row_fast<ANGLE, true>(R, S, sj, sth, snew, jj, cnt, dev, kappa);
+          pair_row_fast<ANGLE, true>(R, S, sj, sth, snew, jj, cnt, dev, ideal);
       } else {
 #pragma unroll kUnroll
         for (int jj = 0; jj < kTile; ++jj)
-          pair_row_fast<ANGLE, false>(R, S, sj, sth, snew, jj, cnt, dev, kappa);
+          pair_row_fast<ANGLE, false>(R, S, sj, sth, snew, jj, cnt, dev, ideal);
       }
     } else {
       if (ti == tj) {
         for (int jj = 0; jj < kTile; ++jj)
-          pair_row<FAST, ANGLE, true>(R, sj, sth, sid, jj, cnt, dev, kappa);
+          pair_row<FAST, ANGLE, true>(R, sj, sth, sid, jj, cnt, dev, ideal);
       } else {
 #pragma unroll kUnroll
         for (int jj = 0; jj < kTile; ++jj)
-          pair_row<FAST, ANGLE, false>(R, sj, sth, sid, jj, cnt, dev, kappa);
+          pair_row<FAST, ANGLE, false>(R, sj, sth, sid, jj, cnt, dev, ideal);
       }
     }
     unsigned c = 0;
@@ -1231,6 +1296,64 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 // fixed-point integer into a 128-bit accumulator.
 // Shared-vertex pairs are never certain (an exact c is 0), so they reach
 // exact_pair, which tests ids: no adjacency correction in this mode.
+//
+// Exact accumulator of the angle sums.  Every warp-slice's deviation sum S
+// (a non-negative double below 2^16: 32 lanes x kFK x kTile deviations of at
+// most pi/2) is added EXACTLY to a per-warp fixed-point number in units of
+// 2^-1074 (the smallest subnormal), stored as kAccWords 64-bit words of
+// 32-bit digits (w[i] weighs 2^(32 i - 1074)) with 32 bits of carry room:
+// the final sum is the exact sum of the S rounded once, whatever order the
+// slices ran in -- deterministic AND relatively accurate at any magnitude
+// (a fixed 2^-50 quantum is not: 1e-12 deviations would lose 4 digits).
+constexpr int kAccWords = 36;  // 36 x 32 bits above 2^-1074: values < 2^78
+
+// w += v for a finite v >= 0 (no carries propagated: each digit word takes
+// < 2^32 additions, see the launch bound in crossing_pairs)
+__device__ __forceinline__ void xacc_add(unsigned long long *w, double v) {
+  // (-0.0 adds nothing: the sign bit is dropped)
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  unsigned long long mant = b & 0xfffffffffffffull;
+  int p = 0;  // weight of mant's LSB: 2^(p - 1074)
+  if (ex != 0) {
+    mant |= 1ull << 52;
+    p = ex - 1;
+  }
+  const int k = p >> 5, o = p & 31;
+  const unsigned long long lo = mant << o;                // bits 0..63 of mant * 2^o
+  const unsigned long long hi = o ? mant >> (64 - o) : 0;  // bits 64..84
+  w[k] += lo & 0xffffffffull;
+  w[k + 1] += lo >> 32;
+  w[k + 2] += hi;
+}
+
+// carries out of every digit word (in place); afterwards w[i] < 2^32 for
+// i < kAccWords - 1
+__device__ __forceinline__ void xacc_normalize(unsigned long long *w) {
+  for (int i = 0; i + 1 < kAccWords; ++i) {
+    w[i + 1] += w[i] >> 32;
+    w[i] &= 0xffffffffull;
+  }
+}
+
+// the normalised accumulator as the correctly rounded double
+__device__ inline double xacc_value(const unsigned long long *w) {
+  int t = kAccWords - 1;
+  while (t > 0 && w[t] == 0) --t;
+  if (t <= 1 && (w[1] >> 21) == 0) {  // integer < 2^53 units: exact as a double
+    return ldexp((double)((w[1] << 32) | w[0]), -1074);
+  }
+  // 64 bits from the top digit down, the rest folded into a sticky bit
+  // (>= 54 significant bits, so __ull2double_rn rounds it correctly)
+  const unsigned long long w1 = t >= 1 ? w[t - 1] : 0, w2 = t >= 2 ? w[t - 2] : 0;
+  const int lz = __clzll(w[t]) - 32;  // w[t] < 2^32 (t < kAccWords - 1)
+  unsigned long long top = (w[t] << (32 + lz)) | (w1 << lz) | (lz ? w2 >> (32 - lz) : 0ull);
+  bool sticky = lz ? (w2 & ((1ull << (32 - lz)) - 1)) != 0 : w2 != 0;
+  for (int i = t - 3; i >= 0 && !sticky; --i) sticky = w[i] != 0;
+  top |= sticky ? 1ull : 0ull;
+  return ldexp(__ull2double_rn(top), 32 * t + 31 - lz - 63 - 1074);
+}
+
 struct CtaUnits {  // the CTA's units as a flat sequence (see cross_pairs_kernel)
   const int2 *ulist;
   uint64_t T, W, ubeg, uend, chunk, nchunks, step, ch0;
@@ -1250,8 +1373,6 @@ struct CtaUnits {  // the CTA's units as a flat sequence (see cross_pairs_kernel
   }
 };
 
-constexpr double kDevScale = 0x1p50;  // fixed-point scale of the angle sums
-
 template <bool ANGLE>
 __global__ void __launch_bounds__(kThreads,
                                   ANGLE ? kFilterMinBlocksAngle : kFilterMinBlocksCount)
@@ -1260,10 +1381,11 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     const TileBox *__restrict__ tbox, const double *__restrict__ theta,
                     const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
                     uint64_t W, uint64_t ubeg,
-                    uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double kappa,
-                    double ideal,
-                    unsigned long long *__restrict__ cta_cnt, double *__restrict__ cta_dev) {
-  if (hdr->fast != kModeFilter) return;
+                    uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double ideal,
+                    int filter_ok,
+                    unsigned long long *__restrict__ cta_cnt,
+                    unsigned long long *__restrict__ cta_acc) {
+  if (hdr->fast != kModeFilter || !filter_ok) return;
   constexpr int kWarps = kThreads / 32;
   constexpr int kNJ = ANGLE ? kFilterBlock : kFilterBlockCount;
   static_assert(kFSlices >= 1, "at least one slice per unit");
@@ -1273,11 +1395,14 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ unsigned done[kStages];  // slices finished with the stage, cumulative
   __shared__ unsigned next_slice;
-  __shared__ unsigned long long acc_cnt, acc_lo, acc_hi;
+  __shared__ unsigned long long acc_cnt;
+  // per-warp exact accumulators of the slices' angle sums (xacc_add)
+  __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
   __shared__ unsigned short wqueue[kWarps][kQCap];  // uncertain pairs (filter_block)
   constexpr unsigned kJBytes = kTile * sizeof(JRec);
   constexpr unsigned kThBytes = ANGLE ? kTile * sizeof(double) : 0;
   const unsigned lane = threadIdx.x & 31;
+  const int warp = (int)(threadIdx.x >> 5);
 
   CtaUnits cu;
   cu.ulist = ulist; cu.T = T; cu.W = W; cu.ubeg = ubeg; cu.uend = uend; cu.chunk = chunk;
@@ -1290,13 +1415,15 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     bulk_g2s(sj[st], jrec + (int64_t)tj_ * kTile, kJBytes, &full[st]);
     if (ANGLE) bulk_g2s(sth[st], theta + (int64_t)tj_ * kTile, kThBytes, &full[st]);
   };
+  if (ANGLE)
+    for (int i = threadIdx.x; i < kWarps * kAccWords; i += kThreads) (&wacc[0][0])[i] = 0;
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
       done[st] = 0;
     }
     next_slice = 0;
-    acc_cnt = acc_lo = acc_hi = 0;
+    acc_cnt = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int st = 0; st < kStages; ++st) {
       uint64_t a, b;
@@ -1305,10 +1432,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
   }
   __syncthreads();
 
-  unsigned long long total = 0, dlo = 0, dhi = 0;
+  unsigned long long total = 0;
   FIRegs R;
   uint64_t cur_ti = ~0ull;
   int cur_slice = -1;
+  // shift / signed forms need ideal >= 2^-100 (genuine deviations then are
+  // 0 or >= 2^-766, see filter_block)
+  const bool shift_ok = ANGLE && ideal >= 0x1p-100;
   for (;;) {
     unsigned q = 0;
     if (lane == 0) q = atomicAdd(&next_slice, 1u);
@@ -1331,14 +1461,15 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // exact.py:205 never counts such a pair -- the unit contributes nothing
     const bool star = bi.star >= 0 && bi.star == bj.star;
     double th[kFK];
-    int shift = -1;
+    int am = 0;  // angle mode: 0 general (reference formula), 2 signed
+    double sigma = 1.0;
     if (ANGLE) {
       double sh = 0.0;
-      if (ti != tj) shift = unit_shift(bi, bj, ideal, &sh);
+      if (ti != tj && shift_ok && unit_shift(bi, bj, ideal, &sh, &sigma) == 1) am = 2;
       const double *tt = ftile[ti].theta;
 #pragma unroll
       for (int k = 0; k < kFK; ++k) th[k] = tt[islot + 32 * k];
-      if (shift == 0) {
+      if (am != 0) {
 #pragma unroll
         for (int k = 0; k < kFK; ++k) th[k] = __dadd_rn(th[k], sh);
       }
@@ -1354,25 +1485,31 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     double dev[kFK];
 #pragma unroll
     for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+    double A2[2] = {0.0, 0.0};  // signed form: sum_j h_j theta_j (even / odd j)
+    unsigned qc = 0;  // queued (uncertain) pairs that hit, and their deviations
+    double qd = 0.0;
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     const float thr = unit_threshold(bi, bj);
-    unsigned short *wq = wqueue[threadIdx.x >> 5];
+    unsigned short *wq = wqueue[warp];
     unsigned qn = 0;  // warp-uniform queue length
     if (star) {
+#ifdef GLR_XONLYSIGNED  // measurement only: registers / speed of the signed path alone
+    } else if (!(ANGLE && am == 2)) {
+#endif
     } else if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, true, kNJ, false>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
-                                              rec, ids, theta, ibase, jbase, wq, qn);
-    } else if (ANGLE && shift == 0) {
+        filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
+                                          rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
+    } else if (ANGLE && am == 2) {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
-                                              rec, ids, theta, ibase, jbase, wq, qn);
+        filter_block<ANGLE, false, kNJ, 2>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
+                                           rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, false>(R, th, jr, jth, jj, islot, thr, cnt, dev, kappa,
-                                               rec, ids, theta, ibase, jbase, wq, qn);
+        filter_block<ANGLE, false, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
+                                           rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
     }
     // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
@@ -1391,30 +1528,47 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // the slice's queued uncertain pairs (global records only, so after the
     // stage is released)
     if (qn != 0)
-      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, kappa, cnt[0], dev[0]);
-    unsigned c = 0;
-    double s = 0.0;
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, qd);
+    unsigned c = qc;
 #pragma unroll
-    for (int k = 0; k < kFK; ++k) { c += cnt[k]; s = __dadd_rn(s, dev[k]); }
+    for (int k = 0; k < kFK; ++k) c += cnt[k];
     total += c;
-    if (ANGLE) {  // s <= kFK * kTile * pi/2 < 2^11 (kFK <= 4): s * 2^50 < 2^61
-      const unsigned long long f = (unsigned long long)__double2ll_rn(s * kDevScale);
-      dlo += f;
-      dhi += dlo < f ? 1ull : 0ull;
+    if (ANGLE) {
+      double s = 0.0;
+      if (am == 2) {
+        // sigma * (sum_j h_j theta_j - sum_k C_k x_k): every term has sign
+        // sigma by the unit's margin, so this is the sum of |v| over hits
+        double cx = 0.0;
+#pragma unroll
+        for (int k = 0; k < kFK; ++k) cx = fma((double)cnt[k], th[k], cx);
+        s = sigma * __dsub_rn(__dadd_rn(A2[0], A2[1]), cx);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
+        s = s < 0x1p-900 ? 0.0 : s;  // only cleared-miss leftovers (< 2^-1031)
+      }
+      s = __dadd_rn(s, qd);
+      // warp sum in a fixed shuffle tree, then lane 0 adds it exactly
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+      if (lane == 0) xacc_add(wacc[warp], s);
     }
   }
   // order-independent CTA reduction (integer atomics commute)
   for (int o = 16; o > 0; o >>= 1) total += __shfl_down_sync(0xffffffffu, total, o);
-  if (lane == 0) atomicAdd(&acc_cnt, total);
-  if (ANGLE) {
-    const unsigned long long old = atomicAdd(&acc_lo, dlo);
-    atomicAdd(&acc_hi, dhi + (old + dlo < old ? 1ull : 0ull));
+  if (lane == 0) {
+    atomicAdd(&acc_cnt, total);
+    if (ANGLE) xacc_normalize(wacc[warp]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    cta_cnt[blockIdx.x] = acc_cnt;
-    cta_dev[blockIdx.x] =
-        ANGLE ? ((double)acc_hi * 0x1p64 + (double)acc_lo) / kDevScale : 0.0;
+  if (threadIdx.x == 0) cta_cnt[blockIdx.x] = acc_cnt;
+  if (ANGLE) {
+    for (int i = threadIdx.x; i < kAccWords; i += kThreads) {
+      unsigned long long v = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
+      cta_acc[(size_t)blockIdx.x * kAccWords + i] = v;
+    }
   }
 }
 
@@ -1428,7 +1582,7 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
            const int *__restrict__ inc, const int *__restrict__ offs,
            const long long *__restrict__ wofs, const int2 *__restrict__ ulist, uint64_t ulen,
            uint64_t T, uint64_t W, uint64_t ubeg, uint64_t uend, uint64_t chunk,
-           unsigned srank, unsigned sworld, double kappa,
+           unsigned srank, unsigned sworld, double ideal, int filter_ok,
            unsigned long long *__restrict__ part_cnt, double *__restrict__ part_dev) {
   // Each adjacent pair belongs to the unit of its tile pair (tl, th): for the
   // implicit space its index is band_unit_index(tl, th); a culled candidate
@@ -1442,7 +1596,8 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
   __shared__ long long s_v;
   __shared__ unsigned long long red_u[kAdjTile / 32];
   __shared__ double red_d[kAdjTile / 32];
-  if (hdr->fast != 1) {  // general path tests ids per pair: nothing to remove
+  const int mode = (hdr->fast == kModeFilter && !filter_ok) ? kModeSign : hdr->fast;
+  if (mode != kModeSign) {  // the other kernels test ids per pair: nothing to remove
     if (threadIdx.x == 0) {
       part_cnt[blockIdx.x] = 0;
       part_dev[blockIdx.x] = 0.0;
@@ -1502,7 +1657,7 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
                         ((unit - ubeg) / chunk) % sworld == srank;
         if (in) {
           ++cnt;
-          if (ANGLE) s = __dadd_rn(s, angle_dev(t1, s_t[qq], kappa));
+          if (ANGLE) s = __dadd_rn(s, angle_dev(t1, s_t[qq], ideal));
         }
       }
     }
@@ -1522,15 +1677,32 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
   }
 }
 
-__global__ void cross_finalize_kernel(const unsigned long long *cta_cnt, const double *cta_dev,
-                                      int ncta, const unsigned long long *adj_cnt,
-                                      const double *adj_dev, int nadj, double *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
+// Totals: count = sum of the CTA counts minus the adjacency correction
+// (mode 1); dev = the pair kernels' CTA sums (modes 0/1, Kahan) minus the
+// correction, or the exact sum of the filter kernel's per-CTA accumulators
+// (mode 2: zero words otherwise).  One warp per accumulator word.
+__global__ void __launch_bounds__(1024)
+cross_finalize_kernel(const unsigned long long *cta_cnt, const double *cta_dev,
+                      const unsigned long long *cta_acc, int ncta,
+                      const unsigned long long *adj_cnt, const double *adj_dev, int nadj,
+                      double *out) {
+  __shared__ unsigned long long w[kAccWords];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = warp; i < kAccWords; i += 32) {
+    unsigned long long v = 0;  // < ncta * 2^34: no overflow
+    for (int c = lane; c < ncta; c += 32) v += cta_acc[(size_t)c * kAccWords + i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) w[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     unsigned long long c = 0, a = 0;
     for (int i = 0; i < ncta; ++i) c += cta_cnt[i];
     for (int i = 0; i < nadj; ++i) a += adj_cnt[i];
     out[0] = (double)(c - a);
-    out[1] = __dsub_rn(kahan_sum(cta_dev, ncta), kahan_sum(adj_dev, nadj));
+    xacc_normalize(w);
+    const double fsum = xacc_value(w);
+    out[1] = __dadd_rn(__dsub_rn(kahan_sum(cta_dev, ncta), kahan_sum(adj_dev, nadj)), fsum);
   }
 }
 
@@ -1735,6 +1907,11 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     set_error("glr_crossing_pairs: invalid arguments");
     return GLR_EARG;
   }
+  if (m > kMaxExactEdges) {  // the float64 count slot is exact below 2^53
+    set_error("glr_crossing_pairs: m=%lld edges: m(m-1)/2 reaches 2^53, counts would round",
+              (long long)m);
+    return GLR_EARG;
+  }
   const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
   const uint64_t T = (uint64_t)(m_pad / kTile);
   const uint64_t U = d_list != nullptr ? list_len : tri_units(T);
@@ -1758,61 +1935,68 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
                              with_angle ? kFilterMinBlocksAngle : kFilterMinBlocksCount);
   const int cgrid = grid > fgrid ? grid : fgrid;  // CTA partial slots
   const int agrid = sm_count() * 8;
-  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)), st);
+  const size_t a_acc = (size_t)cgrid * kAccWords * sizeof(unsigned long long);
+  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc,
+              st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
   unsigned long long *ac = cc + cgrid;
   double *cd = reinterpret_cast<double *>(ac + agrid);
   double *ad = cd + cgrid;
+  unsigned long long *xa = reinterpret_cast<unsigned long long *>(ad + agrid);
   // only the kernel of the records' mode writes its CTA slots
   GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)cgrid * sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)cgrid * sizeof(double), st));
-  const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
+  GLR_CUDA(cudaMemsetAsync(xa, 0, a_acc, st));
   // chunk: >= 8 chunks per CTA of every rank, <= kMaxChunk units per chunk
   // (each chunk reloads its i-tile, so longer chunks mean less L2/DRAM
-  // traffic); a function of the whole range and the rank count only, so all
-  // ranks agree
-  uint64_t chunk = span / ((uint64_t)grid_for(span) * 8 * (uint64_t)sworld);
+  // traffic).  A function of the whole range, the rank count and constants
+  // only (not of this device's SM count), so all ranks cut the same chunks.
+  const uint64_t cta_ref = (uint64_t)kNumSmB200 * kMinBlocks;
+  uint64_t chunk = span / ((span < cta_ref ? span : cta_ref) * 8 * (uint64_t)sworld);
   if (chunk > (uint64_t)kMaxChunk) chunk = (uint64_t)kMaxChunk;
   if (chunk < 1) chunk = 1;
   const uint64_t W = (uint64_t)kBandTiles;
   const unsigned r = (unsigned)srank, g = (unsigned)sworld;
+  // the filter's shift/signed forms and cleared-miss leftovers assume an
+  // ideal angle >= 2^-100; below it the FP64 sign kernel (mode 1) runs
+  const int filter_ok = (!with_angle || ideal >= 0x1p-100) ? 1 : 0;
   if (with_angle) {
     cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
-        cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
+        filter_ok, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
     cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
-        cc, cd);
+        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
+        filter_ok, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
     cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, kappa,
-        ideal, cc, cd);
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
+        chunk, r, g, ideal, filter_ok, cc, xa);
     GLR_LAUNCHED("cross_filter_kernel<angle>");
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
-                                                 d_list, U, T, W, ubeg, uend, chunk, r, g, kappa,
-                                                 ac, ad);
+                                                 d_list, U, T, W, ubeg, uend, chunk, r, g, ideal,
+                                                 filter_ok, ac, ad);
     GLR_LAUNCHED("adj_kernel<angle>");
   } else {
     cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        cc, cd);
+        filter_ok, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<fast>");
     cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        cc, cd);
+        filter_ok, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        0.0, cc, cd);
+        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
+        chunk, r, g, 0.0, filter_ok, cc, xa);
     GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                   d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
-                                                  ac, ad);
+                                                  filter_ok, ac, ad);
     GLR_LAUNCHED("adj_kernel");
   }
-  cross_finalize_kernel<<<1, 32, 0, st>>>(cc, cd, cgrid, ac, ad, agrid, d_out);
+  cross_finalize_kernel<<<1, 1024, 0, st>>>(cc, cd, xa, cgrid, ac, ad, agrid, d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
   return GLR_OK;
 }
