@@ -42,7 +42,8 @@ enum {
   GLR_EARG = 1,       /* invalid argument (ParameterError / InputError side) */
   GLR_ECUDA = 2,      /* CUDA runtime error */
   GLR_EINVARIANT = 4, /* internal consistency check failed (InvariantError) */
-  GLR_EFALLBACK = 8   /* loaders: the text needs the Python parser (not an error) */
+  GLR_EFALLBACK = 8,  /* reserved (earlier loaders deferred to Python with it) */
+  GLR_EPARSE = 16     /* loaders: malformed input, see glr_parse_status() */
 };
 
 /* ABI version: (major << 16) | minor. */
@@ -245,19 +246,44 @@ int glr_fr_layout(double *d_pos, int64_t n, const int64_t *d_ei, const int64_t *
 
 /* ---- native loaders: graphio.py:46-117 ----------- */
 
+/* Both loaders take the reference's whole input grammar: UTF-8 text, the
+ * line boundaries of str.splitlines(), the whitespace of str.isspace(), and
+ * int() / float() of a str (Unicode decimal digits, underscores between
+ * digits, int()'s 4300-digit limit, inf/infinity/nan).  On a malformed
+ * input they return GLR_EPARSE and glr_parse_status() describes it; the
+ * caller formats the reference's message (graphio.py:46-117) from it. */
+enum {
+  GLR_PARSE_UTF8 = 1,         /* not valid UTF-8 (open(..., encoding="utf-8").read() fails) */
+  GLR_PARSE_TOKENS = 2,       /* edge list: "expected two ids per line, got {line!r}" */
+  GLR_PARSE_NOT_INT = 3,      /* edge list: "ids must be integers, got {line!r}" */
+  GLR_PARSE_NEGATIVE = 4,     /* edge list: "ids must be nonnegative" */
+  GLR_PARSE_NO_EDGES = 5,     /* edge list: "no edges found" */
+  GLR_PARSE_OVERFLOW = 6,     /* an id beyond int64 (OverflowError of the int64 conversion) */
+  GLR_PARSE_EMPTY_LAYOUT = 7, /* layout: "empty layout file" */
+  GLR_PARSE_HEADER = 8,       /* layout: "expected header 'id,x,y', got {lines[0]!r}" */
+  GLR_PARSE_FIELDS = 9,       /* layout: "expected 3 fields, got {line!r}" */
+  GLR_PARSE_MALFORMED = 10,   /* layout: "malformed row {line!r}" */
+  GLR_PARSE_NONFINITE = 11,   /* layout: "non-finite coordinate" */
+  GLR_PARSE_DUPLICATE = 12,   /* layout: "duplicate vertex id {vid}" */
+  GLR_PARSE_NO_ROWS = 13      /* layout: "layout file has no rows" */
+};
+
 /* Parses a SNAP-style edge list held in memory (graphio.parse_edgelist
  * before normalisation): *count = the number of id pairs; the first `cap`
- * are written to out (2 int64 each); call with out = NULL to size.
- * GLR_EFALLBACK when the text uses anything beyond plain ASCII decimal ids
- * on '\n'-separated lines (the caller then applies the reference's rules). */
+ * are written to out (2 int64 each); call with out = NULL to size. */
 int glr_parse_edgelist(const char *buf, size_t len, int64_t *out, int64_t cap,
                        int64_t *count);
 
 /* Parses an "id,x,y" layout CSV held in memory (graphio.read_layout): ids
- * and row-major xy of the first `cap` rows, *count = number of rows.
- * GLR_EFALLBACK as above (also for non-finite values and an empty file). */
+ * and row-major xy of the first `cap` rows in file order, *count = number of
+ * rows. */
 int glr_parse_layout(const char *buf, size_t len, int64_t *ids, double *xy, int64_t cap,
                      int64_t *count);
+
+/* The last GLR_EPARSE on this thread: info[0] = GLR_PARSE_* kind, info[1] =
+ * 1-based line number (0 if none), info[2..3] = byte span [begin, end) of
+ * the line the message quotes (GLR_PARSE_DUPLICATE: info[2] = the id). */
+int glr_parse_status(int64_t *info);
 
 /* ---- introspection (tests / bench) --------------------------------------- */
 

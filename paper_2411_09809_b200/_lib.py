@@ -20,6 +20,7 @@ GLR_EARG = 1
 GLR_ECUDA = 2
 GLR_EINVARIANT = 4
 GLR_EFALLBACK = 8
+GLR_EPARSE = 16
 
 # (name, restype, argtypes) for every symbol include/glare_b200.h declares.
 _c = ctypes
@@ -65,6 +66,7 @@ SIGNATURES = {
                                       _c.POINTER(_c.c_int64)]),
     "glr_parse_layout": (_c.c_int, [_c.c_char_p, _c.c_size_t, _c.c_void_p, _c.c_void_p,
                                     _c.c_int64, _c.POINTER(_c.c_int64)]),
+    "glr_parse_status": (_c.c_int, [_c.c_void_p]),
     "glr_strip_crossings": (_c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_int64,
                                        _c.c_void_p, _c.c_int64, _c.c_int, _c.c_int,
                                        _c.c_double, _c.c_void_p, _c.c_void_p]),
@@ -169,7 +171,7 @@ def check(rc: int, what: str) -> None:
         return
     from .model import InvariantError, ParameterError
 
-    msg = lib().glr_last_error()
+    msg = host_lib().glr_last_error()
     msg = msg.decode() if msg else ""
     if rc == GLR_EARG:
         raise ParameterError(f"{what}: {msg}")

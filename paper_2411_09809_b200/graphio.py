@@ -1,21 +1,26 @@
 """Edge-list and layout loaders: drop-ins for the reference's
-graphio.parse_edgelist and graphio.read_layout (graphio.py:46-117), with a
-native fast path (csrc/io.cu: `glr_parse_edgelist`, `glr_parse_layout`).
+graphio.parse_edgelist and graphio.read_layout (graphio.py:46-117).
 
-The native parsers handle plain-ASCII files whose ids are decimal digit
-strings and whose reals are ordinary decimal numbers; anything else --
-non-ASCII text, other line breaks, underscores, inf/nan, malformed rows --
-makes them defer (GLR_EFALLBACK) to the Python restatement below, which
-follows the reference's rules line by line, so results and error messages
-are the reference's in every case.  ``read_layout_arrays`` returns
-(ids, xy) arrays for building a LayoutGraph without a million-entry dict.
+All parsing is native (csrc/io.cu: ``glr_parse_edgelist`` /
+``glr_parse_layout``), over the reference's whole input grammar -- UTF-8,
+str.splitlines() line boundaries, str.isspace() whitespace, and int() /
+float() of a str.  A malformed input comes back as a ``GLR_PARSE_*`` kind
+with a line number and the byte span of the offending line
+(``glr_parse_status``); ``_raise`` below turns that into the exception the
+reference raises, with its message (the quoted line is ``repr`` of the
+decoded span, as the reference's f-strings do).
+``read_layout_arrays`` returns (ids, xy) arrays for building a LayoutGraph
+without a million-entry dict.
+
+One deliberate difference: a layout id beyond the int64 range raises the
+``OverflowError`` that any int64 id array raises (the reference's dict would
+hold it and fail later, when a LayoutGraph is built from it).
 """
 
 from __future__ import annotations
 
 import ctypes
 import logging
-import math
 
 import numpy as np
 
@@ -23,6 +28,23 @@ from . import _lib
 from .model import InputError, LayoutGraph, normalize_edges
 
 log = logging.getLogger(__name__)
+
+# message templates of the reference's loaders (graphio.py:59-79, 89-117),
+# by GLR_PARSE_* kind ({q}: repr of the quoted line)
+_MESSAGES = {
+    2: "expected two ids per line, got {q}",
+    3: "ids must be integers, got {q}",
+    4: "ids must be nonnegative",
+    5: "no edges found",
+    7: "empty layout file",
+    8: "expected header 'id,x,y', got {q}",
+    9: "expected 3 fields, got {q}",
+    10: "malformed row {q}",
+    11: "non-finite coordinate",
+    12: "duplicate vertex id {vid}",
+    13: "layout file has no rows",
+}
+_KIND_UTF8, _KIND_OVERFLOW, _KIND_HEADER = 1, 6, 8
 
 
 def _read_bytes(path) -> bytes:
@@ -33,73 +55,30 @@ def _read_bytes(path) -> bytes:
         raise InputError(f"cannot read {path}: {exc}") from exc
 
 
-def _decode(path, raw: bytes) -> str:
-    """graphio._read_text: the file as UTF-8 text."""
-    try:
-        return raw.decode("utf-8")
-    except UnicodeDecodeError as exc:  # open(..., encoding="utf-8").read() raises the same
-        raise exc
+def _raise(path, raw: bytes) -> None:
+    """Raise what the reference raises for the parse failure just reported."""
+    info = (ctypes.c_int64 * 4)()
+    _lib.host_lib().glr_parse_status(info)
+    kind, lineno, a, b = info
+    if kind == _KIND_UTF8:
+        # the reference reads the file as UTF-8 text (graphio.py:_read_text);
+        # the same read raises the same UnicodeDecodeError here
+        with open(path, encoding="utf-8") as fh:
+            fh.read()
+        raise InputError(f"{path}: invalid UTF-8")  # unreachable: the decoder agrees
+    if kind == _KIND_OVERFLOW:
+        raise OverflowError("Python int too large to convert to C long")
+    msg = _MESSAGES[kind].format(q=repr(raw[a:b].decode("utf-8")), vid=a)
+    where = f"{path}:{lineno}" if lineno and kind != _KIND_HEADER else f"{path}"
+    raise InputError(f"{where}: {msg}")
 
 
-# -- Python restatement of the reference parsers (fallback path) --------------
-
-def _edge_pairs_py(path, text: str) -> list:
-    pairs = []
-    for lineno, raw in enumerate(text.splitlines(), start=1):
-        line = raw.strip()
-        if not line or line.startswith("#"):
-            continue
-        parts = line.split()
-        if len(parts) != 2:
-            raise InputError(f"{path}:{lineno}: expected two ids per line, got {line!r}")
-        try:
-            a, b = int(parts[0]), int(parts[1])
-        except ValueError as exc:
-            raise InputError(f"{path}:{lineno}: ids must be integers, got {line!r}") from exc
-        if a < 0 or b < 0:
-            raise InputError(f"{path}:{lineno}: ids must be nonnegative")
-        pairs.append((a, b))
-    return pairs
-
-
-def _layout_py(path, text: str) -> dict:
-    lines = text.splitlines()
-    if not lines:
-        raise InputError(f"{path}: empty layout file")
-    header = [c.strip() for c in lines[0].split(",")]
-    if header != ["id", "x", "y"]:
-        raise InputError(f"{path}: expected header 'id,x,y', got {lines[0]!r}")
-    positions: dict = {}
-    for lineno, line in enumerate(lines[1:], start=2):
-        if not line.strip():
-            continue
-        parts = [c.strip() for c in line.split(",")]
-        if len(parts) != 3:
-            raise InputError(f"{path}:{lineno}: expected 3 fields, got {line!r}")
-        try:
-            vid = int(parts[0])
-            x = float(parts[1])
-            y = float(parts[2])
-        except ValueError as exc:
-            raise InputError(f"{path}:{lineno}: malformed row {line!r}") from exc
-        if not (math.isfinite(x) and math.isfinite(y)):
-            raise InputError(f"{path}:{lineno}: non-finite coordinate")
-        if vid in positions:
-            raise InputError(f"{path}:{lineno}: duplicate vertex id {vid}")
-        positions[vid] = (x, y)
-    if not positions:
-        raise InputError(f"{path}: layout file has no rows")
-    return positions
-
-
-# -- native fast paths ---------------------------------------------------------
-
-def _native_pairs(raw: bytes):
+def _native_pairs(path, raw: bytes) -> np.ndarray:
     L = _lib.host_lib()
     n = ctypes.c_int64(0)
     rc = L.glr_parse_edgelist(raw, len(raw), None, 0, ctypes.byref(n))
-    if rc == _lib.GLR_EFALLBACK:
-        return None
+    if rc == _lib.GLR_EPARSE:
+        _raise(path, raw)
     _lib.check(rc, "glr_parse_edgelist")
     out = np.empty((n.value, 2), dtype=np.int64)
     rc = L.glr_parse_edgelist(raw, len(raw), out.ctypes.data, n.value, ctypes.byref(n))
@@ -107,34 +86,25 @@ def _native_pairs(raw: bytes):
     return out
 
 
-def _native_layout(raw: bytes):
+def _native_layout(path, raw: bytes):
     L = _lib.host_lib()
     n = ctypes.c_int64(0)
     rc = L.glr_parse_layout(raw, len(raw), None, None, 0, ctypes.byref(n))
-    if rc == _lib.GLR_EFALLBACK:
-        return None
+    if rc == _lib.GLR_EPARSE:
+        _raise(path, raw)
     _lib.check(rc, "glr_parse_layout")
     ids = np.empty(n.value, dtype=np.int64)
     xy = np.empty((n.value, 2), dtype=np.float64)
     rc = L.glr_parse_layout(raw, len(raw), ids.ctypes.data, xy.ctypes.data, n.value,
                             ctypes.byref(n))
     _lib.check(rc, "glr_parse_layout")
-    if len(ids) == 0 or len(np.unique(ids)) != len(ids):
-        return None  # the Python path raises the reference's error
     return ids, xy
 
 
 def parse_edgelist(path) -> np.ndarray:
     """Normalized (m, 2) id pairs from a SNAP-style edge list file
     (graphio.py:46-79)."""
-    raw = _read_bytes(path)
-    pairs = _native_pairs(raw)
-    if pairs is None:
-        pairs = _edge_pairs_py(path, _decode(path, raw))
-        if not pairs:
-            raise InputError(f"{path}: no edges found")
-    elif len(pairs) == 0:
-        raise InputError(f"{path}: no edges found")
+    pairs = _native_pairs(path, _read_bytes(path))
     edges, loops, dupes = normalize_edges(pairs)
     if loops or dupes:
         log.info("%s: dropped %d self-loop(s) and %d duplicate edge(s)", path, loops, dupes)
@@ -144,14 +114,7 @@ def parse_edgelist(path) -> np.ndarray:
 def read_layout_arrays(path) -> tuple:
     """(ids int64 (n,), xy float64 (n, 2)) in file order, with read_layout's
     validation and errors."""
-    raw = _read_bytes(path)
-    got = _native_layout(raw)
-    if got is not None:
-        return got
-    pos = _layout_py(path, _decode(path, raw))
-    ids = np.fromiter(pos.keys(), dtype=np.int64, count=len(pos))
-    xy = np.array(list(pos.values()), dtype=np.float64).reshape(-1, 2)
-    return ids, xy
+    return _native_layout(path, _read_bytes(path))
 
 
 def read_layout(path) -> dict:

@@ -72,6 +72,12 @@ class DeviceGraph:
             raise ValueError("DeviceGraph.edges must be an int64 (m, 2) tensor")
         if edges.device != xy.device:
             raise ValueError("DeviceGraph tensors must share a device")
+        if edges.numel():
+            # the kernels index xy[edges] unchecked: one device min/max here
+            lo, hi = (int(v) for v in torch.aminmax(edges))
+            if lo < 0 or hi >= xy.shape[0]:
+                raise ValueError(f"DeviceGraph.edges index out of range [0, {xy.shape[0]}): "
+                                 f"min {lo}, max {hi}")
         self.xy = xy.contiguous()
         self.edges = edges.contiguous()
 

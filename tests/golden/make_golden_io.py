@@ -32,8 +32,12 @@ def _sha(a) -> str:
 def run(fn, text, summarize):
     with tempfile.TemporaryDirectory() as d:
         path = os.path.join(d, "f.txt")
-        with open(path, "w", encoding="utf-8", newline="") as fh:
-            fh.write(text)
+        if isinstance(text, bytes):
+            with open(path, "wb") as fh:
+                fh.write(text)
+        else:
+            with open(path, "w", encoding="utf-8", newline="") as fh:
+                fh.write(text)
         try:
             return {"ok": summarize(fn(path))}
         except Exception as exc:  # noqa: BLE001 - the reference's error is the golden

@@ -28,8 +28,12 @@ def _sha(a) -> str:
 
 def _write(tmp_path, text):
     path = tmp_path / "f.txt"
-    with open(path, "w", encoding="utf-8", newline="") as fh:
-        fh.write(text)
+    if isinstance(text, bytes):
+        with open(path, "wb") as fh:
+            fh.write(text)
+    else:
+        with open(path, "w", encoding="utf-8", newline="") as fh:
+            fh.write(text)
     return str(path)
 
 
@@ -62,19 +66,25 @@ def test_read_layout_matches_reference(io_golden, tmp_path, name):
     assert _run(read_layout, path, summ) == io_golden["layouts"][name]
 
 
-def test_native_fast_path_taken_and_deferred():
-    from paper_2411_09809_b200.graphio import _native_layout, _native_pairs
+def test_every_text_is_parsed_natively():
+    """No Python parsing path is left: the native parsers answer every case
+    with a result or a GLR_PARSE_* error (never the old fallback code)."""
+    import ctypes
 
-    for name in ("simple", "comments_blanks", "loops_dupes", "plus_leading_zeros",
-                 "random_20000"):
-        assert _native_pairs(io_cases.EDGELISTS[name].encode()) is not None, name
-    for name in ("underscores", "crlf", "unicode_digit", "negative", "three_tokens", "huge_id"):
-        assert _native_pairs(io_cases.EDGELISTS[name].encode()) is None, name
-    for name in ("simple", "spaces", "blank_rows", "subnormal", "negative_id", "random_5000"):
-        assert _native_layout(io_cases.LAYOUTS[name].encode()) is not None, name
-    for name in ("inf", "nan", "overflow", "duplicate", "bad_header", "empty", "underscores",
-                 "crlf"):
-        assert _native_layout(io_cases.LAYOUTS[name].encode()) is None, name
+    from paper_2411_09809_b200 import _lib, graphio
+
+    assert not hasattr(graphio, "_edge_pairs_py") and not hasattr(graphio, "_layout_py")
+    L = _lib.host_lib()
+    n = ctypes.c_int64(0)
+    for texts, fn in ((io_cases.EDGELISTS, L.glr_parse_edgelist),
+                      (io_cases.LAYOUTS, None)):
+        for name, text in texts.items():
+            raw = text if isinstance(text, bytes) else text.encode("utf-8")
+            if fn is None:
+                rc = L.glr_parse_layout(raw, len(raw), None, None, 0, ctypes.byref(n))
+            else:
+                rc = fn(raw, len(raw), None, 0, ctypes.byref(n))
+            assert rc in (_lib.GLR_OK, _lib.GLR_EPARSE), (name, rc)
 
 
 def test_load_graph(tmp_path):
