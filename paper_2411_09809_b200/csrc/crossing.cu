@@ -86,6 +86,10 @@ constexpr int kFilterBlock = GLR_XFBLOCK;  // j-edges per filter block (one warp
 #define GLR_XFBLOCK_C 2
 #endif
 constexpr int kFilterBlockCount = GLR_XFBLOCK_C;  // same for the count-only kernel
+#ifndef GLR_XFBLOCK_S
+#define GLR_XFBLOCK_S 4
+#endif
+constexpr int kFilterBlockSigned = GLR_XFBLOCK_S;  // same for signed units
 // CTAs per SM of the filter kernel (fused 4 -> <= 128 registers, count-only
 // 5 -> <= 102, with kFK = 4):
 // tools/c5_time.py and tools/config_bench.py, profiles/r01_variants_filter.txt
@@ -106,6 +110,8 @@ constexpr int kFilterMinBlocksCount = GLR_XFMINB_C;
 // Largest edge count whose pair count m(m-1)/2 stays below 2^53, where the
 // float64 count slot of d_out is exact.
 constexpr int64_t kMaxExactEdges = (int64_t)1 << 27;
+// units per launch segment of the angle pass (fixup bitmap <= 1 GB)
+constexpr uint64_t kMaxSegUnits = (uint64_t)1 << 32;
 
 // Fast sign path admissibility bounds on nonzero |coordinate|.
 constexpr double kMaxAbsFast = 0x1p500;
@@ -585,6 +591,18 @@ __device__ inline double angle_dev_signed(double t1, double t2, double ideal) {
 __device__ inline double angle_dev(double t1, double t2, double ideal) {
   return fabs(angle_dev_signed(t1, t2, ideal));
 }
+// The same deviation as ||pi/2 - d| - kappa|, kappa = fl(pi/2 - ideal):
+// 3 DADD and no select, within 2^-50 of angle_dev (each of the two
+// formulas is within 2^-51 of the exact function of the rounded d).  The
+// filter kernel's general units use it; a warp-slice whose mean deviation
+// per hit is below 2^-16 -- where 2^-50 per pair could exceed 1e-9 of the
+// sum -- is re-evaluated with angle_dev by cross_fixup_kernel.
+__device__ inline double angle_dev_fast_signed(double t1, double t2, double kappa) {
+  const double HALF_PI = 1.5707963267948966;
+  const double d = __dsub_rn(t1, t2);
+  const double e = __dsub_rn(HALF_PI, fabs(d));
+  return __dsub_rn(fabs(e), kappa);
+}
 
 // One j-edge against the thread's K i-edges.  FAST selects the float-view
 // sign test and skips the vertex-id test (corrected by adj_kernel); otherwise
@@ -965,7 +983,7 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
 // of the slice, or when the queue is full.  Results go to the lane's
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
-constexpr unsigned kQCap = 512;  // queue entries per warp (>= 32 lanes x NJ x kFK)
+constexpr unsigned kQCap = GLR_XFBLOCK_S > 4 ? 32 * GLR_XFBLOCK_S * 4 : 512;  // per warp (>= 32 lanes x NJ x kFK)
 static_assert(kTile <= 256, "queue entries hold 8-bit tile slots");
 template <bool ANGLE>
 __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
@@ -999,19 +1017,21 @@ __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned q
 // debug build only: [vote blocks that fell back, uncertain pairs evaluated]
 __device__ unsigned long long g_fstats[2];
 #endif
-// AM (angle mode of the unit): 0 the reference's per-pair formula
-// (angle_dev), 2 the signed form (unit_shift); the count-only kernel uses 0.
+// AM (angle mode of the unit): 0 the fast per-pair formula
+// (angle_dev_fast_signed), 2 the signed form (unit_shift), 3 the reference's
+// per-pair formula (angle_dev: cross_fixup_kernel); the count-only kernel
+// uses 0.
 template <bool ANGLE, bool DIAG, int NJ, int AM>
 __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)[kFK],
                                              unsigned jaddr,
                                              unsigned thaddr, int jj0, int islot, float thr,
                                              unsigned (&cnt)[kFK], double (&dev)[kFK],
-                                             double (&A2)[2], double ideal,
+                                             double (&A2)[2], double ideal, double kappa,
                                              const EdgeRec *__restrict__ rec,
                                              const int2 *__restrict__ ids,
                                              const double *__restrict__ theta, int64_t ibase,
                                              int64_t jbase, unsigned short *wq, unsigned &qn,
-                                             unsigned &qc, double &qd) {
+                                             unsigned &qc) {
   constexpr bool SIGNED = ANGLE && AM == 2;
   constexpr bool FOLD = !ANGLE || SIGNED;
   const uint64_t T2 = f2_bcast(thr);
@@ -1062,7 +1082,8 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         // slice's sum is cleared when below 2^-900 and otherwise differs
         // from the masked sum by a relative 2^-265 at most (DADD, no zeroing
         // MOV or {0,1} multiplier per pair).
-        double v = angle_dev_signed(th[k], thj, ideal);
+        double v = AM == 3 ? angle_dev_signed(th[k], thj, ideal)
+                           : angle_dev_fast_signed(th[k], thj, kappa);
         asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
             "setp.lt.f32 p, %2, %3;\n\t"
             "@p add.u32 %0, %0, 1;\n\t"
@@ -1109,7 +1130,10 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     }
 #endif
     if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
-      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, qd);
+      // queued hits: the signed form's C_k multiply x_k, so they count
+      // apart (qc); their deviations go to dev[0], unused by that form
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
+                         SIGNED ? qc : cnt[0], dev[0]);
       qn = 0;
     }
     unsigned pos = qn + incl - n;
@@ -1306,6 +1330,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 // slices ran in -- deterministic AND relatively accurate at any magnitude
 // (a fixed 2^-50 quantum is not: 1e-12 deviations would lose 4 digits).
 constexpr int kAccWords = 36;  // 36 x 32 bits above 2^-1074: values < 2^78
+// mean deviation per hit below which a fast-formula slice is re-evaluated
+#ifndef GLR_XFIXUPDEV
+#define GLR_XFIXUPDEV 0x1p-16
+#endif
+constexpr double kFixupMeanDev = GLR_XFIXUPDEV;
 
 // w += v for a finite v >= 0 (no carries propagated: each digit word takes
 // < 2^32 additions, see the launch bound in crossing_pairs)
@@ -1357,11 +1386,12 @@ __device__ inline double xacc_value(const unsigned long long *w) {
 struct CtaUnits {  // the CTA's units as a flat sequence (see cross_pairs_kernel)
   const int2 *ulist;
   uint64_t T, W, ubeg, uend, chunk, nchunks, step, ch0;
-  __device__ bool at(uint64_t uq, uint64_t *ti, uint64_t *tj) const {
+  __device__ bool at(uint64_t uq, uint64_t *ti, uint64_t *tj, uint64_t *unit = nullptr) const {
     const uint64_t ch = ch0 + (uq / chunk) * step;
     if (ch >= nchunks) return false;
     const uint64_t u = ubeg + ch * chunk + uq % chunk;
     if (u >= uend) return false;
+    if (unit != nullptr) *unit = u;
     if (ulist != nullptr) {
       const int2 p = ulist[u];
       *ti = (uint64_t)p.x;
@@ -1382,9 +1412,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
                     uint64_t W, uint64_t ubeg,
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double ideal,
-                    int filter_ok,
+                    double kappa, int filter_ok,
                     unsigned long long *__restrict__ cta_cnt,
-                    unsigned long long *__restrict__ cta_acc) {
+                    unsigned long long *__restrict__ cta_acc, unsigned *__restrict__ fixup) {
   if (hdr->fast != kModeFilter || !filter_ok) return;
   constexpr int kWarps = kThreads / 32;
   constexpr int kNJ = ANGLE ? kFilterBlock : kFilterBlockCount;
@@ -1445,8 +1475,8 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     q = __shfl_sync(0xffffffffu, q, 0);
     const uint64_t uq = q / kFSlices;
     const int slice = (int)(q % kFSlices);
-    uint64_t ti, tj;
-    if (!cu.at(uq, &ti, &tj)) break;
+    uint64_t ti, tj, unit;
+    if (!cu.at(uq, &ti, &tj, &unit)) break;
     const int islot = fslot(slice, 0, (int)lane);  // slot of i-edge k: islot + 32 k
     if (ti != cur_ti || slice != cur_slice) {
       load_fi<ANGLE>(R, ftile, ti, slice, (int)lane);
@@ -1486,8 +1516,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
 #pragma unroll
     for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
     double A2[2] = {0.0, 0.0};  // signed form: sum_j h_j theta_j (even / odd j)
-    unsigned qc = 0;  // queued (uncertain) pairs that hit, and their deviations
-    double qd = 0.0;
+    unsigned qc = 0;  // signed form: queued (uncertain) pairs that hit
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     const float thr = unit_threshold(bi, bj);
     unsigned short *wq = wqueue[warp];
@@ -1498,18 +1527,18 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
 #endif
     } else if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
-                                          rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
+        filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
+                                          rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else if (ANGLE && am == 2) {
 #pragma unroll 1
-      for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, 2>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
-                                           rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
+      for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
+        filter_block<ANGLE, false, kFilterBlockSigned, 2>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
+                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal,
-                                           rec, ids, theta, ibase, jbase, wq, qn, qc, qd);
+        filter_block<ANGLE, false, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
+                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     }
     // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
@@ -1527,8 +1556,12 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     }
     // the slice's queued uncertain pairs (global records only, so after the
     // stage is released)
-    if (qn != 0)
-      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, qd);
+    if (qn != 0) {
+      if (ANGLE && am == 2)
+        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
+      else
+        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+    }
     unsigned c = qc;
 #pragma unroll
     for (int k = 0; k < kFK; ++k) c += cnt[k];
@@ -1541,17 +1574,31 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         double cx = 0.0;
 #pragma unroll
         for (int k = 0; k < kFK; ++k) cx = fma((double)cnt[k], th[k], cx);
-        s = sigma * __dsub_rn(__dadd_rn(A2[0], A2[1]), cx);
+        // + the queued hits' deviations (dev[0])
+        s = __dadd_rn(sigma * __dsub_rn(__dadd_rn(A2[0], A2[1]), cx), dev[0]);
       } else {
 #pragma unroll
         for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
         s = s < 0x1p-900 ? 0.0 : s;  // only cleared-miss leftovers (< 2^-1031)
       }
-      s = __dadd_rn(s, qd);
-      // warp sum in a fixed shuffle tree, then lane 0 adds it exactly
+      // warp sums in a fixed shuffle tree; lane 0 adds the deviation sum
+      // exactly, unless the slice's mean deviation per hit is below 2^-16
+      // in a unit of the fast formula: then the slice is marked for
+      // cross_fixup_kernel, which re-evaluates it with the reference formula
+      unsigned cw = c;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
-      if (lane == 0) xacc_add(wacc[warp], s);
+      for (int o = 16; o > 0; o >>= 1) {
+        s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+        cw += __shfl_down_sync(0xffffffffu, cw, o);
+      }
+      if (lane == 0) {
+        if (am != 2 && s < (double)cw * kFixupMeanDev) {
+          const uint64_t bit = (unit - ubeg) * kFSlices + (uint64_t)slice;
+          atomicOr(&fixup[bit >> 5], 1u << (bit & 31));
+        } else {
+          xacc_add(wacc[warp], s);
+        }
+      }
     }
   }
   // order-independent CTA reduction (integer atomics commute)
@@ -1561,14 +1608,115 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     if (ANGLE) xacc_normalize(wacc[warp]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) cta_cnt[blockIdx.x] = acc_cnt;
+  // += : crossing_pairs may launch several unit segments into the same slots
+  if (threadIdx.x == 0) cta_cnt[blockIdx.x] += acc_cnt;
   if (ANGLE) {
     for (int i = threadIdx.x; i < kAccWords; i += kThreads) {
       unsigned long long v = 0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
-      cta_acc[(size_t)blockIdx.x * kAccWords + i] = v;
+      cta_acc[(size_t)blockIdx.x * kAccWords + i] += v;
     }
+  }
+}
+
+// Re-evaluates the warp-slices cross_filter_kernel marked in `fixup` (a
+// fast-formula unit whose slice has a mean deviation per hit below
+// kFixupMeanDev) with the reference's per-pair formula (AM 3): one warp per
+// marked slice, its j-tile staged into the warp's own shared memory, the
+// same filter, queue and exact fallback.  Only the deviation sums are taken
+// (the filter kernel counted the slice's hits); they go to this kernel's own
+// CTA accumulators.  Marked slices are rare (all hits of a slice within
+// ~1.5e-5 rad of the ideal angle on average), so the kernel mostly scans an
+// all-zero bitmap.
+constexpr int kFixThreads = 64;  // 2 warps: a staged j-tile (10 KB) per warp
+__global__ void __launch_bounds__(kFixThreads)
+cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
+                   const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
+                   const TileBox *__restrict__ tbox, const double *__restrict__ theta,
+                   const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
+                   uint64_t W, uint64_t ubeg, uint64_t nbits, double ideal, double kappa,
+                   int filter_ok, const unsigned *__restrict__ fixup,
+                   unsigned long long *__restrict__ cta_acc) {
+  if (hdr->fast != kModeFilter || !filter_ok) return;
+  constexpr int kWarps = kFixThreads / 32;
+  __shared__ __align__(128) JRec sj[kWarps][kTile];
+  __shared__ __align__(16) double sth[kWarps][kTile];
+  __shared__ unsigned short wqueue[kWarps][kQCap];
+  __shared__ unsigned long long wacc[kWarps][kAccWords];
+  const unsigned lane = threadIdx.x & 31;
+  const int warp = (int)(threadIdx.x >> 5);
+  for (int i = threadIdx.x; i < kWarps * kAccWords; i += kFixThreads) (&wacc[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t nwords = (nbits + 31) / 32;
+  for (uint64_t wd = (uint64_t)blockIdx.x * kWarps + warp; wd < nwords;
+       wd += (uint64_t)gridDim.x * kWarps) {
+    unsigned bits = fixup[wd];
+    while (bits != 0u) {
+      const uint64_t bit = wd * 32 + (uint64_t)(__ffs(bits) - 1);
+      bits &= bits - 1u;
+      const uint64_t u = ubeg + bit / kFSlices;
+      const int slice = (int)(bit % kFSlices);
+      uint64_t ti, tj;
+      if (ulist != nullptr) {
+        ti = (uint64_t)ulist[u].x;
+        tj = (uint64_t)ulist[u].y;
+      } else {
+        band_unit_coords(u, T, W, &ti, &tj);
+      }
+      __syncwarp();
+      for (int q = (int)lane; q < kTile; q += 32) {
+        sj[warp][q] = jrec[(int64_t)tj * kTile + q];
+        sth[warp][q] = theta[(int64_t)tj * kTile + q];
+      }
+      __syncwarp();
+      FIRegs R;
+      load_fi<true>(R, ftile, ti, slice, (int)lane);
+      const int islot = fslot(slice, 0, (int)lane);
+      double th[kFK];
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) th[k] = ftile[ti].theta[islot + 32 * k];
+      const TileBox bi = tbox[ti], bj = tbox[tj];
+      const float thr = unit_threshold(bi, bj);
+      unsigned cnt[kFK];
+      double dev[kFK];
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) { cnt[k] = 0; dev[k] = 0.0; }
+      double A2[2] = {0.0, 0.0};
+      unsigned qc = 0, qn = 0;
+      const unsigned jr = smem_u32(sj[warp]), jth = smem_u32(sth[warp]);
+      const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
+      unsigned short *wq = wqueue[warp];
+      if (ti == tj) {
+        for (int jj = 0; jj < kTile; jj += kFilterBlock)
+          filter_block<true, true, kFilterBlock, 3>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                                    ideal, kappa, rec, ids, theta, ibase, jbase,
+                                                    wq, qn, qc);
+      } else {
+#pragma unroll 1
+        for (int jj = 0; jj < kTile; jj += kFilterBlock)
+          filter_block<true, false, kFilterBlock, 3>(R, th, jr, jth, jj, islot, thr, cnt, dev,
+                                                     A2, ideal, kappa, rec, ids, theta, ibase,
+                                                     jbase, wq, qn, qc);
+      }
+      if (qn != 0)
+        drain_queue<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
+      s = s < 0x1p-900 ? 0.0 : s;  // only cleared-miss leftovers (< 2^-1031)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+      if (lane == 0) xacc_add(wacc[warp], s);
+    }
+  }
+  if (lane == 0) xacc_normalize(wacc[warp]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAccWords; i += kFixThreads) {
+    unsigned long long v = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
+    cta_acc[(size_t)blockIdx.x * kAccWords + i] += v;
   }
 }
 
@@ -1683,14 +1831,14 @@ adj_kernel(const RecHeader *__restrict__ hdr, const double *__restrict__ theta,
 // (mode 2: zero words otherwise).  One warp per accumulator word.
 __global__ void __launch_bounds__(1024)
 cross_finalize_kernel(const unsigned long long *cta_cnt, const double *cta_dev,
-                      const unsigned long long *cta_acc, int ncta,
+                      const unsigned long long *cta_acc, int ncta, int nacc,
                       const unsigned long long *adj_cnt, const double *adj_dev, int nadj,
                       double *out) {
   __shared__ unsigned long long w[kAccWords];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = warp; i < kAccWords; i += 32) {
-    unsigned long long v = 0;  // < ncta * 2^34: no overflow
-    for (int c = lane; c < ncta; c += 32) v += cta_acc[(size_t)c * kAccWords + i];
+    unsigned long long v = 0;  // < nacc * segments * 2^34: no overflow
+    for (int c = lane; c < nacc; c += 32) v += cta_acc[(size_t)c * kAccWords + i];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (lane == 0) w[i] = v;
   }
@@ -1935,19 +2083,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
                              with_angle ? kFilterMinBlocksAngle : kFilterMinBlocksCount);
   const int cgrid = grid > fgrid ? grid : fgrid;  // CTA partial slots
   const int agrid = sm_count() * 8;
-  const size_t a_acc = (size_t)cgrid * kAccWords * sizeof(unsigned long long);
-  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc,
-              st);
-  GLR_CUDA(scr.err);
-  unsigned long long *cc = scr.as<unsigned long long>();
-  unsigned long long *ac = cc + cgrid;
-  double *cd = reinterpret_cast<double *>(ac + agrid);
-  double *ad = cd + cgrid;
-  unsigned long long *xa = reinterpret_cast<unsigned long long *>(ad + agrid);
-  // only the kernel of the records' mode writes its CTA slots
-  GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)cgrid * sizeof(unsigned long long), st));
-  GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)cgrid * sizeof(double), st));
-  GLR_CUDA(cudaMemsetAsync(xa, 0, a_acc, st));
+  const int xgrid = with_angle ? sm_count() * 4 : 0;  // cross_fixup_kernel CTAs
   // chunk: >= 8 chunks per CTA of every rank, <= kMaxChunk units per chunk
   // (each chunk reloads its i-tile, so longer chunks mean less L2/DRAM
   // traffic).  A function of the whole range, the rank count and constants
@@ -1956,11 +2092,37 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   uint64_t chunk = span / ((span < cta_ref ? span : cta_ref) * 8 * (uint64_t)sworld);
   if (chunk > (uint64_t)kMaxChunk) chunk = (uint64_t)kMaxChunk;
   if (chunk < 1) chunk = 1;
+  // The angle pass runs in unit segments of at most kMaxSegUnits whose
+  // offsets are multiples of chunk * world (so chunk ownership is the one of
+  // the whole range); each segment's warp-slices have one bit in the fixup
+  // bitmap (cross_fixup_kernel).
+  const uint64_t seg_align = chunk * (uint64_t)sworld;
+  uint64_t seg_len = (kMaxSegUnits / seg_align) * seg_align;
+  if (seg_len < seg_align) seg_len = seg_align;
+  const uint64_t seg_max = span < seg_len ? span : seg_len;
+  const size_t a_fix = with_angle ? al256((size_t)((seg_max * kFSlices + 31) / 32) * 4) : 0;
+  const size_t a_acc = (size_t)(cgrid + xgrid) * kAccWords * sizeof(unsigned long long);
+  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc +
+                  a_fix + 256,
+              st);
+  GLR_CUDA(scr.err);
+  unsigned long long *cc = scr.as<unsigned long long>();
+  unsigned long long *ac = cc + cgrid;
+  double *cd = reinterpret_cast<double *>(ac + agrid);
+  double *ad = cd + cgrid;
+  unsigned long long *xa = reinterpret_cast<unsigned long long *>(ad + agrid);
+  unsigned *fix = reinterpret_cast<unsigned *>(
+      (reinterpret_cast<uintptr_t>(xa + (size_t)(cgrid + xgrid) * kAccWords) + 255) & ~(uintptr_t)255);
+  // only the kernel of the records' mode writes its CTA slots
+  GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)cgrid * sizeof(unsigned long long), st));
+  GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)cgrid * sizeof(double), st));
+  GLR_CUDA(cudaMemsetAsync(xa, 0, a_acc, st));
   const uint64_t W = (uint64_t)kBandTiles;
   const unsigned r = (unsigned)srank, g = (unsigned)sworld;
   // the filter's shift/signed forms and cleared-miss leftovers assume an
   // ideal angle >= 2^-100; below it the FP64 sign kernel (mode 1) runs
   const int filter_ok = (!with_angle || ideal >= 0x1p-100) ? 1 : 0;
+  const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
   if (with_angle) {
     cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
@@ -1970,10 +2132,19 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
         filter_ok, cc, cd);
     GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
-    cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
-        chunk, r, g, ideal, filter_ok, cc, xa);
-    GLR_LAUNCHED("cross_filter_kernel<angle>");
+    for (uint64_t sb = ubeg; sb < uend; sb += seg_len) {
+      const uint64_t se = uend - sb < seg_len ? uend : sb + seg_len;
+      const uint64_t nbits = (se - sb) * kFSlices;
+      GLR_CUDA(cudaMemsetAsync(fix, 0, (size_t)((nbits + 31) / 32) * 4, st));
+      cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, se,
+          chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
+      GLR_LAUNCHED("cross_filter_kernel<angle>");
+      cross_fixup_kernel<<<xgrid, kFixThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, nbits,
+          ideal, kappa, filter_ok, fix, xa + (size_t)cgrid * kAccWords);
+      GLR_LAUNCHED("cross_fixup_kernel");
+    }
     adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                  d_list, U, T, W, ubeg, uend, chunk, r, g, ideal,
                                                  filter_ok, ac, ad);
@@ -1989,14 +2160,15 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     GLR_LAUNCHED("cross_pairs_kernel<general>");
     cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
         rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
-        chunk, r, g, 0.0, filter_ok, cc, xa);
+        chunk, r, g, 0.0, 0.0, filter_ok, cc, xa, nullptr);
     GLR_LAUNCHED("cross_filter_kernel");
     adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                   d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
                                                   filter_ok, ac, ad);
     GLR_LAUNCHED("adj_kernel");
   }
-  cross_finalize_kernel<<<1, 1024, 0, st>>>(cc, cd, xa, cgrid, ac, ad, agrid, d_out);
+  cross_finalize_kernel<<<1, 1024, 0, st>>>(cc, cd, xa, cgrid, cgrid + xgrid, ac, ad, agrid,
+                                            d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
   return GLR_OK;
 }
