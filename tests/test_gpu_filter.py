@@ -125,8 +125,50 @@ def lattice_c5_like(seed=8, n=3000, m=6000):
     return xy, _random_pairs(rng, n, m)
 
 
+def tight_clusters(seed=9, clusters=24, per=300):
+    """Clusters that fill whole tiles with tight per-unit thresholds (small
+    box D, long edges L ~ 2D): packed near-parallel long edges, near-collinear
+    chains with T-junctions, pencils of lines at 1e-7 rad through one point,
+    and crossing fans -- the unit threshold, not the global bound, decides
+    every pair inside them (tests/test_filter_bound.py checks the same
+    families with exact rationals)."""
+    rng = np.random.default_rng(seed)
+    segs = []
+    for c in range(clusters):
+        off = rng.uniform(0.05, 0.9, 2)
+        D = float(10.0 ** rng.uniform(-6, -2))
+        kind = c % 4
+        for _ in range(per):
+            if kind == 0:
+                y = rng.uniform(0, D)
+                segs.append((off + [0, y], off + [D, y + rng.normal(scale=D * 1e-6)]))
+            elif kind == 1:
+                d = np.array([0.6, 0.8])
+                s0, s1 = np.sort(rng.uniform(0, D, 2))
+                nrm = np.array([-0.8, 0.6]) * rng.normal(scale=D * 1e-9)
+                segs.append((off + s0 * d + nrm, off + s1 * d))
+            elif kind == 2:
+                ang = rng.normal(scale=1e-7)
+                v = np.array([math.cos(ang), math.sin(ang)]) * D / 2
+                q = off + rng.normal(scale=D * 1e-9, size=2)
+                segs.append((q - v, q + v))
+            else:
+                if rng.random() < 0.5:
+                    y = rng.uniform(0, D)
+                    segs.append((off + [0, y], off + [D, y + rng.uniform(-D, D) * 1e-3]))
+                else:
+                    x = rng.uniform(0, D)
+                    segs.append((off + [x, -D * 0.1], off + [x + rng.uniform(-D, D), D * 1.1]))
+    pts = np.array([p for sgm in segs for p in sgm], dtype=np.float64)
+    xy, inv = np.unique(pts, axis=0, return_inverse=True)
+    pairs = inv.reshape(-1, 2)
+    pairs = pairs[pairs[:, 0] != pairs[:, 1]]
+    return xy, pairs
+
+
 CASES = {f.__name__: f for f in (near_collinear, exact_lattice, far_offset, mixed_scales,
-                                  short_edges, hubs, coincident, lattice_c5_like)}
+                                  short_edges, hubs, coincident, lattice_c5_like,
+                                  tight_clusters)}
 
 
 def _run(dg, mode, ideal):
