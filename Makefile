@@ -19,7 +19,7 @@ $(BUILD)/%.o: paper_2411_09809_b200/csrc/%.cu $(HDR)
 
 $(LIB): $(OBJ)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -ldl
 	cat $(BUILD)/*.ptxas.log > $(LIBDIR)/ptxas.log
 
 oracle:

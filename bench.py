@@ -43,6 +43,10 @@ CONFIG = 5
 FP64_PER_PAIR_EC = 18      # DADD/DMUL of the reference predicate
 FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
 FP64_PER_PAIR_NC = 5
+# occlusion_filter_kernel hot block (tools/sass_loop.py, 4 j x 8 i = 32 pairs):
+# 154 SASS; FMA pipe: 48 FADD2 + 16 FMUL2 + 16 FFMA2 + 8 FADD = 168 lane-ops
+OCC_SASS_PER_PAIR = 154 / 32
+OCC_FMA_PER_PAIR = 168 / 32
 # The default pair kernel (certified FP32 filter) per pair:
 # 8 FFMA + 2 FMUL on the FP32 FMA pipe (issued as packed pairs) and, fused
 # with E_ca over theta-ordered edges, 2 DADD on the FP64 pipe (|theta_j -
@@ -187,6 +191,19 @@ def run_reference(args, world, rank):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _occ_roofline(rate, sm_mhz):
+    """Occlusion pass against its two compute ceilings per GPU: the FP32 FMA
+    pipe (OCC_FMA_PER_PAIR lane-ops per pair at 128 lanes/clk/SM) and issue
+    slots (OCC_SASS_PER_PAIR instructions per pair, 4 schedulers x 32 lanes)."""
+    fma_peak = FMA_LANES_PER_CLK_SM * 148 * sm_mhz * 1e6 / OCC_FMA_PER_PAIR
+    issue_peak = 4 * 32 * 148 * sm_mhz * 1e6 / OCC_SASS_PER_PAIR
+    return {"bound": "fp32-fma", "achieved": rate, "peak": fma_peak, "unit": "pairs/s",
+            "frac": rate / fma_peak, "fma_lane_ops_per_pair": OCC_FMA_PER_PAIR,
+            "issue_bound": {"sass_per_pair": OCC_SASS_PER_PAIR, "pairs_per_s": issue_peak,
+                            "frac": rate / issue_peak},
+            "kernel": "occlusion_filter_kernel"}
 
 
 def _config_desc(g, p, world):
@@ -444,6 +461,7 @@ def main():
                           "tflops": FP64_PER_PAIR_NC * P_V / world / (occ_ms * 1e-3) / 1e12,
                           "vs_fp64_peak_at_max_clock": FP64_PER_PAIR_NC * P_V / world
                           / (occ_ms * 1e-3) / (64 * 148 * 1965e6)},
+                      "roofline": _occ_roofline(P_V / world / (occ_ms * 1e-3), sm_mhz),
                       "culled": {"value": P_V / (occ_culled_ms * 1e-3), "unit": "pairs/s",
                                  "ms_per_step": occ_culled_ms, "candidate_units": occ_units,
                                  "dense_units": M.occlusion_units(n),
@@ -492,8 +510,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 3 * 8,
-                "strategy": "auto (what edge_crossing_angle(g) runs: the culled plan on C5; "
-                            "value is the dense pass)"},
+                "strategy": "auto: what edge_crossing_angle(g) runs -- on C5 the culled plan "
+                            "(plan build included); the line's top-level value is the dense "
+                            "theta-ordered pass, device-resident"},
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -41,6 +41,7 @@ enum {
   GLR_OK = 0,
   GLR_EARG = 1,       /* invalid argument (ParameterError / InputError side) */
   GLR_ECUDA = 2,      /* CUDA runtime error */
+  GLR_ENCCL = 3,      /* NCCL unavailable or failed (collective entry points) */
   GLR_EINVARIANT = 4, /* internal consistency check failed (InvariantError) */
   GLR_EFALLBACK = 8,  /* reserved (earlier loaders deferred to Python with it) */
   GLR_EPARSE = 16     /* loaders: malformed input, see glr_parse_status() */
@@ -81,6 +82,13 @@ int glr_crossing_tile(void);
  * consecutive j-tiles (within a band: rows ti below the band first, then the
  * band's own triangle), so concurrently running CTAs share j-tiles in L2. */
 int glr_crossing_band(void);
+
+/* Units per chunk of interleaved sharding for a unit range of `span` units
+ * over `world` ranks (glr_crossing_pairs_interleaved): a function of span,
+ * world and compile-time constants only -- never of the device -- so every
+ * rank cuts the same chunks; rank r owns the chunks whose index is r mod
+ * world, i.e. unit u of [b, e) belongs to rank ((u - b) / chunk) % world. */
+uint64_t glr_crossing_chunk(uint64_t span, int world);
 
 /* Number of edge tile-pair units for m edges: T(T+1)/2. */
 uint64_t glr_crossing_units(int64_t m);
@@ -315,6 +323,27 @@ int glr_crossing_set_mode(void *d_records, int mode, void *stream);
 /* Number of kernel launches issued by this thread since the last call
  * (counter is reset by the call). */
 uint64_t glr_take_launch_count(void);
+
+/* ---- combining shards -------------------------------
+ * The partials of disjoint unit ranges add up; these entry points sum them
+ * across GPUs with NCCL (opened with dlopen on first use; GLR_ENCCL when it
+ * is missing).  Replaces the torch.distributed all_reduce of
+ * paper_2411_09809_b200/sharding.py for hosts without Python. */
+
+/* One process, ndev GPUs: d_bufs[i] (count float64 on devices[i]) are summed
+ * in place over all i.  Communicators are created once per device list and
+ * cached; synchronous on return. */
+int glr_allreduce_sum_f64(int ndev, const int *devices, double **d_bufs, int count);
+
+/* One process per GPU: rank 0 creates the id (glr_nccl_id_bytes() bytes) and
+ * the host hands it to every rank; each rank then creates its communicator on
+ * its current device.  The allreduce is in place and asynchronous on
+ * `stream`. */
+int glr_nccl_id_bytes(void);
+int glr_nccl_unique_id(void *id_out);
+int glr_nccl_comm_init(const void *id, int rank, int world, void **comm_out);
+int glr_allreduce_sum_f64_comm(void *comm, double *d_buf, int count, void *stream);
+int glr_nccl_comm_destroy(void *comm);
 
 #ifdef __cplusplus
 }

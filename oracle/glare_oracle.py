@@ -324,6 +324,42 @@ def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int, band=
     return total, dev
 
 
+# Interleaved ownership of the crossing pass's units across ranks (restates
+# csrc/crossing.cu chunk_for and the chunk loop of the pair kernels: rank r
+# of `world` takes the chunks ch = r, r + world, r + 2 world, ...).  The
+# build-time constants are the library's defaults: 148 SMs (B200) x 4 CTAs
+# per SM as the reference CTA count, chunks of at most 256 units.
+CHUNK_CTA_REF = 148 * 4
+CHUNK_MAX = 256
+
+
+def interleaved_chunk(span: int, world: int) -> int:
+    if span == 0 or world < 1:
+        return 1
+    c = span // (min(span, CHUNK_CTA_REF) * 8 * world)
+    return max(1, min(CHUNK_MAX, c))
+
+
+def interleaved_owner(u: int, ubeg: int, chunk: int, world: int) -> int:
+    return ((u - ubeg) // chunk) % world
+
+
+def crossing_scan_interleaved(xy, edges, ideal, tile: int, rank: int, world: int, band=None):
+    """(count, dev_sum) of the units rank `rank` owns under interleaved chunk
+    ownership of the whole unit space [0, T(T+1)/2)."""
+    m = len(edges)
+    T = max(1, -(-m // tile))
+    U = T * (T + 1) // 2
+    chunk = interleaved_chunk(U, world)
+    total, dev = 0, 0.0
+    for ch in range(rank, -(-U // chunk), world):
+        b, e = ch * chunk, min(U, (ch + 1) * chunk)
+        c, d = crossing_scan_units(xy, edges, ideal, tile, b, e, band)
+        total += c
+        dev += d
+    return total, dev
+
+
 def node_occlusion_units(xy, r, tile: int, ubeg: int, uend: int) -> int:
     """Occluding pairs restricted to vertex tile-pair units [ubeg, uend)."""
     n = len(xy)

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("GLARE_B200_LIB") or os.path.join(_HERE, "_lib", "libg
 GLR_OK = 0
 GLR_EARG = 1
 GLR_ECUDA = 2
+GLR_ENCCL = 3
 GLR_EINVARIANT = 4
 GLR_EFALLBACK = 8
 GLR_EPARSE = 16
@@ -35,6 +36,14 @@ SIGNATURES = {
     ),
     "glr_crossing_tile": (_c.c_int, []),
     "glr_crossing_band": (_c.c_int, []),
+    "glr_crossing_chunk": (_c.c_uint64, [_c.c_uint64, _c.c_int]),
+    "glr_allreduce_sum_f64": (
+        _c.c_int, [_c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_void_p), _c.c_int]),
+    "glr_nccl_id_bytes": (_c.c_int, []),
+    "glr_nccl_unique_id": (_c.c_int, [_c.c_void_p]),
+    "glr_nccl_comm_init": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_void_p)]),
+    "glr_allreduce_sum_f64_comm": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_int, _c.c_void_p]),
+    "glr_nccl_comm_destroy": (_c.c_int, [_c.c_void_p]),
     "glr_crossing_units": (_c.c_uint64, [_c.c_int64]),
     "glr_crossing_records_bytes": (_c.c_size_t, [_c.c_int64, _c.c_int64]),
     "glr_crossing_prepare": (

@@ -2047,6 +2047,20 @@ int crossing_prepare(const double *d_xy, int64_t n, const int64_t *d_edges, int6
   return GLR_OK;
 }
 
+// Chunk of interleaved ownership: >= 8 chunks per CTA of every rank, <=
+// kMaxChunk units per chunk (each chunk reloads its i-tile, so longer chunks
+// mean less L2/DRAM traffic).  A function of the whole range, the rank count
+// and constants only (not of this device's SM count), so all ranks cut the
+// same chunks (glr_crossing_chunk).
+uint64_t chunk_for(uint64_t span, int sworld) {
+  const uint64_t cta_ref = (uint64_t)kNumSmB200 * kMinBlocks;
+  if (span == 0 || sworld < 1) return 1;
+  uint64_t chunk = span / ((span < cta_ref ? span : cta_ref) * 8 * (uint64_t)sworld);
+  if (chunk > (uint64_t)kMaxChunk) chunk = (uint64_t)kMaxChunk;
+  if (chunk < 1) chunk = 1;
+  return chunk;
+}
+
 int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                    const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
                    int srank, int sworld, double *d_out, cudaStream_t st) {
@@ -2084,14 +2098,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   const int cgrid = grid > fgrid ? grid : fgrid;  // CTA partial slots
   const int agrid = sm_count() * 8;
   const int xgrid = with_angle ? sm_count() * 4 : 0;  // cross_fixup_kernel CTAs
-  // chunk: >= 8 chunks per CTA of every rank, <= kMaxChunk units per chunk
-  // (each chunk reloads its i-tile, so longer chunks mean less L2/DRAM
-  // traffic).  A function of the whole range, the rank count and constants
-  // only (not of this device's SM count), so all ranks cut the same chunks.
-  const uint64_t cta_ref = (uint64_t)kNumSmB200 * kMinBlocks;
-  uint64_t chunk = span / ((span < cta_ref ? span : cta_ref) * 8 * (uint64_t)sworld);
-  if (chunk > (uint64_t)kMaxChunk) chunk = (uint64_t)kMaxChunk;
-  if (chunk < 1) chunk = 1;
+  const uint64_t chunk = chunk_for(span, sworld);
   // The angle pass runs in unit segments of at most kMaxSegUnits whose
   // offsets are multiples of chunk * world (so chunk ownership is the one of
   // the whole range); each segment's warp-slices have one bit in the fixup
@@ -2234,6 +2241,8 @@ extern "C" {
 int glr_crossing_tile(void) { return glr::kTile; }
 
 int glr_crossing_band(void) { return glr::kBandTiles; }
+
+uint64_t glr_crossing_chunk(uint64_t span, int world) { return glr::chunk_for(span, world); }
 
 int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m, double beta,
                               double *d_w, void *stream) {

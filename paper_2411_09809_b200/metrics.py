@@ -218,9 +218,12 @@ class CrossingRecords:
     the candidate tile pairs.  ``order="theta"`` makes dense records hold the
     edges ordered by direction (glr_theta_sort_edges), which lets the fused
     E_c + E_ca pass evaluate the angle deviation with one FP64 operation per
-    pair in almost every unit; ``"input"`` keeps the caller's order (unit
-    ranges then match the oracle's unit-range restatement).  Results never
-    depend on the order."""
+    pair in almost every unit; ``"input"`` keeps the caller's order with
+    ``strategy="dense"`` (unit ranges then match the oracle's unit-range
+    restatement).  When ``"auto"`` builds the culled plan and then prefers the
+    dense pass, input order reuses the Morton-ordered records (one prologue);
+    theta order prepares its own (the Morton order is needed to decide, the
+    direction order to run).  Results never depend on the order."""
 
     ORDERS = ("input", "theta")
 
@@ -242,6 +245,11 @@ class CrossingRecords:
             lst = _candidates(L.glr_crossing_candidates, _ptr(self.buf), self.n, self.m)
             if strategy == "culled" or len(lst) <= CROSS_CULL_FRACTION * crossing_units(self.m):
                 self.list = lst
+                return
+            if order == "input":
+                # auto chose the dense pass: results never depend on the edge
+                # order, so the Morton-ordered records serve it as they are
+                # (no second prologue)
                 return
         if order == "theta" and self.m >= 2:
             es = torch.empty_like(dg.edges)

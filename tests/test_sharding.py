@@ -1,7 +1,10 @@
 """Multi-rank path on CPU: world-size-2 gloo process group running the same
-shard plan and allreduce code the NCCL ranks run (paper_2411_09809_b200/
-sharding.py); per-rank partials come from the oracle's unit-range
-restatement (the CUDA kernels' contract, checked against them in
+ownership rules and allreduce code the NCCL ranks run (paper_2411_09809_b200/
+sharding.py): interleaved chunk ownership of the crossing units (the rule
+production uses, crossing.cu chunk_for, restated in oracle/glare_oracle.py
+and checked against the library's glr_crossing_chunk here) and contiguous
+ranges of the occlusion units.  Per-rank partials come from the oracle's
+unit-range restatement (the CUDA kernels' contract, checked against them in
 tests/test_gpu_parity.py)."""
 
 from __future__ import annotations
@@ -18,7 +21,8 @@ import torch.multiprocessing as mp
 from paper_2411_09809_b200 import sharding
 
 IDEAL = 7.0 * np.pi / 18.0
-TILE_E = 512
+TILE_E = 256   # glr_crossing_tile()
+BAND = 2048    # glr_crossing_band()
 TILE_V = 1024
 
 
@@ -42,10 +46,8 @@ def _worker(rank, world, port, q):
         from oracle import glare_oracle as O
 
         g = graph_from(cases.lattice_stress)
-        Te = -(-g.num_edges // TILE_E)
         Tv = -(-g.num_vertices // TILE_V)
-        b, e = sharding.shard_range(Te * (Te + 1) // 2, rank, world)
-        c, d = O.crossing_scan_units(g.xy, g.edges, IDEAL, TILE_E, b, e)
+        c, d = O.crossing_scan_interleaved(g.xy, g.edges, IDEAL, TILE_E, rank, world, BAND)
         bv, ev = sharding.shard_range(Tv * (Tv + 1) // 2, rank, world)
         occ = O.node_occlusion_units(g.xy, 1.0, TILE_V, bv, ev)
         buf = torch.tensor([float(c), d, float(occ)], dtype=torch.float64)
@@ -111,3 +113,27 @@ def test_balanced_triangle_and_weighted_ranges():
         cuts = [sharding.weighted_range(lst_w, r, 4) for r in range(4)]
         assert cuts[0][0] == 0 and cuts[-1][1] == 50
         assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+
+
+def test_interleaved_chunk_matches_library():
+    """The oracle's restatement of the chunk rule equals the library's
+    (glr_crossing_chunk: host code, no GPU needed), and chunks of every rank
+    tile the unit space exactly once."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import _lib
+
+    lib = _lib.host_lib()
+    assert lib.glr_crossing_tile() == TILE_E and lib.glr_crossing_band() == BAND
+    rng = np.random.default_rng(1)
+    spans = [1, 2, 591, 592, 593, 4735, 4736, 9473, 122_078_125, 66_337_020, 2 ** 40]
+    spans += [int(x) for x in rng.integers(1, 10 ** 9, 40)]
+    for span in spans:
+        for world in (1, 2, 3, 4, 7, 8, 16):
+            assert lib.glr_crossing_chunk(span, world) == O.interleaved_chunk(span, world)
+    for span in (1, 7, 300, 5000, 70_001):
+        for world in (1, 2, 3, 8):
+            chunk = O.interleaved_chunk(span, world)
+            owners = [O.interleaved_owner(u, 0, chunk, world) for u in range(span)]
+            counts = np.bincount(owners, minlength=world)
+            assert counts.sum() == span
+            assert counts.max() - counts.min() <= chunk
