@@ -324,6 +324,35 @@ def crossing_scan_units(xy, edges, ideal, tile: int, ubeg: int, uend: int, band=
     return total, dev
 
 
+def crossing_scan_tiles(xy, edges, ideal, tile: int, tile_pairs):
+    """(count, dev_sum) over explicit tile pairs (ti, tj), ti <= tj, of the
+    edge sequence `edges` (pairs j > i only when ti == tj) -- the unit of the
+    culled candidate lists and of any edge order the kernels use."""
+    m = len(edges)
+    e0, e1 = edges[:, 0], edges[:, 1]
+    ax, ay, bx, by = xy[e0, 0], xy[e0, 1], xy[e1, 0], xy[e1, 1]
+    xmin, xmax = np.minimum(ax, bx), np.maximum(ax, bx)
+    ymin, ymax = np.minimum(ay, by), np.maximum(ay, by)
+    theta = axis_angles(ax, ay, bx, by) if ideal is not None else None
+    total, dev = 0, 0.0
+    for ti, tj in tile_pairs:
+        I = np.arange(ti * tile, min(m, (ti + 1) * tile))[:, None]
+        J = np.arange(tj * tile, min(m, (tj + 1) * tile))[None, :]
+        if I.size == 0 or J.size == 0:
+            continue
+        ok = J > I
+        ok &= (xmax[J] >= xmin[I]) & (xmax[I] >= xmin[J]) & (ymax[J] >= ymin[I]) & (ymax[I] >= ymin[J])
+        ok &= (e0[I] != e0[J]) & (e0[I] != e1[J]) & (e1[I] != e0[J]) & (e1[I] != e1[J])
+        ii, jj = np.nonzero(ok)
+        ii = I[ii, 0]
+        jj = J[0, jj]
+        hit = straddle_mask(ax[ii], ay[ii], bx[ii], by[ii], ax[jj], ay[jj], bx[jj], by[jj])
+        total += int(np.count_nonzero(hit))
+        if ideal is not None and np.any(hit):
+            dev += float(np.sum(np.abs(ideal - crossing_angles(theta[ii[hit]], theta[jj[hit]]))))
+    return total, dev
+
+
 # Interleaved ownership of the crossing pass's units across ranks (restates
 # csrc/crossing.cu chunk_for and the chunk loop of the pair kernels: rank r
 # of `world` takes the chunks ch = r, r + world, r + 2 world, ...).  The

@@ -976,6 +976,68 @@ __device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj
   }
 }
 
+// The same M for NJ consecutive j-edges at once, computed operation by
+// operation across the block (GLR_XMB): consecutive FFMA2s then share an
+// operand in the same slot (the i-edge line constants across j-edges, the
+// j-edge line constants across i-groups), which the operand reuse cache
+// serves without register-file reads -- the kernel is bound by register
+// reads (tools/rf_model.py, profiles/r02_rfbench.txt).  Identical roundings.
+template <bool DIAG, bool FOLD, int NJ>
+__device__ __forceinline__ void filter_mb(const FIRegs &R, unsigned jaddr, int jj0, int islot,
+                                          uint64_t T2, float (&M)[NJ][kFK]) {
+  float4 q0[NJ], q1[NJ];
+#pragma unroll
+  for (int q = 0; q < NJ; ++q) {
+    q0[q] = lds_f4(jaddr + (jj0 + q) * (unsigned)sizeof(JRec));
+    q1[q] = lds_f4(jaddr + (jj0 + q) * (unsigned)sizeof(JRec) + 16);
+  }
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) {
+    uint64_t c1[NJ], c2[NJ], c3[NJ], c4[NJ];
+    // i-line at the j-endpoints: nsaby_g, nska_g shared by 2 NJ FFMA2s
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) c1[q] = f2_fma(R.nsaby[g], f2_bcast(q0[q].x), R.nska[g]);
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) c2[q] = f2_fma(R.nsaby[g], f2_bcast(q0[q].z), R.nska[g]);
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) c1[q] = f2_fma(R.sabx[g], f2_bcast(q0[q].y), c1[q]);
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) c2[q] = f2_fma(R.sabx[g], f2_bcast(q0[q].w), c2[q]);
+    // j-line at the i-endpoints: (nscdy, nskc) shared by c3/c4 of a j-edge
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      c3[q] = f2_fma(f2_bcast(q1[q].y), R.ax[g], f2_bcast(q1[q].z));
+      c4[q] = f2_fma(f2_bcast(q1[q].y), R.bx[g], f2_bcast(q1[q].z));
+    }
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      c3[q] = f2_fma(f2_bcast(q1[q].x), R.ay[g], c3[q]);
+      c4[q] = f2_fma(f2_bcast(q1[q].x), R.by[g], c4[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NJ; ++q) {
+      const uint64_t p12 = FOLD ? f2_fma(c1[q], c2[q], T2) : f2_mul(c1[q], c2[q]);
+      const uint64_t p34 = FOLD ? f2_fma(c3[q], c4[q], T2) : f2_mul(c3[q], c4[q]);
+      if (FOLD) {
+        M[q][2 * g] =
+            __int_as_float(max(__float_as_int(f2_lo(p12)), __float_as_int(f2_lo(p34))));
+        M[q][2 * g + 1] =
+            __int_as_float(max(__float_as_int(f2_hi(p12)), __float_as_int(f2_hi(p34))));
+      } else {
+        M[q][2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
+        M[q][2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
+      }
+    }
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int q = 0; q < NJ; ++q)
+#pragma unroll
+      for (int k = 0; k < kFK; ++k)
+        if (!(jj0 + q > islot + 32 * k)) M[q][k] = FOLD ? 4.0f : 2.0f;
+  }
+}
+
 // Uncertain pairs are not evaluated where they are found: each warp queues
 // them in shared memory (16-bit entry = tile slot of the i-edge << 8 | j slot) and
 // evaluates the queue with all 32 lanes at once (exact_pair's FP64 records
@@ -1021,10 +1083,10 @@ __device__ unsigned long long g_fstats[2];
 // (angle_dev_fast_signed), 2 the signed form (unit_shift), 3 the reference's
 // per-pair formula (angle_dev: cross_fixup_kernel); the count-only kernel
 // uses 0.
-template <bool ANGLE, bool DIAG, int NJ, int AM>
+template <bool ANGLE, bool DIAG, int NJ, int AM, bool T1 = false>
 __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)[kFK],
                                              unsigned jaddr,
-                                             unsigned thaddr, int jj0, int islot, float thr,
+                                             unsigned thaddr, int jj0, int islot, float thr_u,
                                              unsigned (&cnt)[kFK], double (&dev)[kFK],
                                              double (&A2)[2], double ideal, double kappa,
                                              const EdgeRec *__restrict__ rec,
@@ -1034,6 +1096,10 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
                                              unsigned &qc) {
   constexpr bool SIGNED = ANGLE && AM == 2;
   constexpr bool FOLD = !ANGLE || SIGNED;
+  // T1: the unit's threshold is the global bound 1 (every unit of a
+  // domain-spanning tile order): a compile-time constant, so the FOLD
+  // products take it as an immediate (one register read less per FFMA2)
+  const float thr = T1 ? 1.0f : thr_u;
   const uint64_t T2 = f2_bcast(thr);
   // FOLD: uncertain <=> M in [+0, 2t] <=> M's bits <= 2t's bits (unsigned: a
   // negative M, a certain hit, lies above every non-negative float), so the
@@ -1041,10 +1107,18 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
   const unsigned vbits = __float_as_uint(2.0f * thr);
   unsigned mmin = 0xffffffffu;
   bool any = false;
+#ifdef GLR_XMB
+  float MB[NJ][kFK];
+  filter_mb<DIAG, FOLD, NJ>(R, jaddr, jj0, islot, T2, MB);
+#endif
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
+#ifdef GLR_XMB
+    float (&M)[kFK] = MB[q];
+#else
     float M[kFK];
     filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
+#endif
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
     if (SIGNED) {
       // hits are M's sign bits: C_k += hit (LEA.HI), h = hits on this j-edge,
@@ -1530,10 +1604,25 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else if (ANGLE && am == 2) {
+      if (thr == 1.0f) {
 #pragma unroll 1
-      for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
-        filter_block<ANGLE, false, kFilterBlockSigned, 2>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
-                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
+        for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
+          filter_block<ANGLE, false, kFilterBlockSigned, 2, true>(
+              R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa, rec, ids, theta, ibase,
+              jbase, wq, qn, qc);
+      } else {
+#pragma unroll 1
+        for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
+          filter_block<ANGLE, false, kFilterBlockSigned, 2>(R, th, jr, jth, jj, islot, thr, cnt,
+                                                            dev, A2, ideal, kappa, rec, ids, theta,
+                                                            ibase, jbase, wq, qn, qc);
+      }
+    } else if (!ANGLE && thr == 1.0f) {
+#pragma unroll 1
+      for (int jj = 0; jj < kTile; jj += kNJ)
+        filter_block<ANGLE, false, kNJ, 0, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                                 ideal, kappa, rec, ids, theta, ibase, jbase, wq,
+                                                 qn, qc);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kNJ)
