@@ -169,7 +169,7 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
  * (crossing.cu unit_shift), and skip units of two tiles of one hub's edges
  * (every pair shares the hub).  Results do not depend on the order. */
 #ifndef GLR_HUB_DEGREE_DEFAULT
-#define GLR_HUB_DEGREE_DEFAULT 1024
+#define GLR_HUB_DEGREE_DEFAULT 4096  /* C5 sweep: 1024 4634 ms, 4096 4543, 8192 4570, none 4823 (profiles/r02_hub_sweep.txt) */
 #endif
 int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                          int64_t m, int64_t hub_degree, int64_t *d_edges_out, void *stream);

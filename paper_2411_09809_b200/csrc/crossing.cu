@@ -200,12 +200,36 @@ struct __align__(16) FTile {
 };
 static_assert(sizeof(FTile) == (size_t)kTile * 36, "FTile must be 36 B per edge");
 
-// The same record in the j role, one edge per 32 B: (cx, cy, dx, dy) and
-// (scdx, -scdy, -skc, 0); read by all lanes of a warp at once (broadcast).
+// The same record in the j role, 32 B per edge, stored by PAIRS of
+// consecutive edges (2p, 2p+1) so that the j-endpoint coordinates of the two
+// are adjacent floats (one packed register pair each, see filter_m2):
+//   [cx0 cx1 cy0 cy1] [dx0 dx1 dy0 dy1] [scdx0 -scdy0 -skc0 scdx1]
+//   [-scdy1 -skc1 0 0]
+// read by all lanes of a warp at once (broadcast).
 struct __align__(16) JRec {
   float4 c;
   float4 k;
 };
+struct __align__(16) JPair {
+  float4 cxy, dxy, k0, k1;
+};
+static_assert(sizeof(JPair) == 2 * sizeof(JRec), "a j pair is two records");
+__device__ inline void jrec_store(JRec *jrec, int64_t e, float ax, float ay, float bx, float by,
+                                  float sabx, float nsaby, float nska) {
+  float *w = reinterpret_cast<float *>(jrec + (e & ~1ll));
+  const int h = (int)(e & 1);
+  w[0 + h] = ax; w[2 + h] = ay; w[4 + h] = bx; w[6 + h] = by;
+  if (h == 0) {
+    w[8] = sabx; w[9] = nsaby; w[10] = nska;
+  } else {
+    w[11] = sabx; w[12] = nsaby; w[13] = nska; w[14] = 0.0f; w[15] = 0.0f;
+  }
+}
+__device__ inline float4 jrec_points(const JRec *jrec, int64_t e) {  // (ax, ay, bx, by)
+  const float *w = reinterpret_cast<const float *>(jrec + (e & ~1ll));
+  const int h = (int)(e & 1);
+  return make_float4(w[0 + h], w[2 + h], w[4 + h], w[6 + h]);
+}
 
 // Per tile: box of its edges' scaled FP32 endpoints and the largest L =
 // |abx| + |aby|; a unit's two boxes bound |p - a| for all its pairs, which
@@ -457,10 +481,8 @@ __global__ void frec_kernel(int64_t m, int64_t m_pad, RecView rv, const double *
 #pragma unroll
     for (int k = 0; k < kFFields; ++k) reinterpret_cast<float *>(&t.v[k][P])[h] = f[k];
     t.theta[slot] = theta;
-    JRec j;
-    j.c = make_float4(f[kFAx], f[kFAy], f[kFBx], f[kFBy]);
-    j.k = make_float4(f[kFSabx], f[kFNsaby], f[kFNska], 0.0f);
-    rv.jrec[e] = j;
+    jrec_store(rv.jrec, e, f[kFAx], f[kFAy], f[kFBx], f[kFBy], f[kFSabx], f[kFNsaby],
+               f[kFNska]);
   }
 }
 
@@ -479,11 +501,11 @@ __global__ void __launch_bounds__(kTile) tile_fbox_kernel(int64_t m, RecView rv)
   float xlo = INFINITY, xhi = -INFINITY, ylo = INFINITY, yhi = -INFINITY, l = 0.0f;
   float tlo = INFINITY, thi = -INFINITY;
   if (e < m) {
-    const JRec j = rv.jrec[e];
-    xlo = fminf(j.c.x, j.c.z); xhi = fmaxf(j.c.x, j.c.z);
-    ylo = fminf(j.c.y, j.c.w); yhi = fmaxf(j.c.y, j.c.w);
+    const float4 j = jrec_points(rv.jrec, e);
+    xlo = fminf(j.x, j.z); xhi = fmaxf(j.x, j.z);
+    ylo = fminf(j.y, j.w); yhi = fmaxf(j.y, j.w);
     // L of the FP32 direction (exact float differences, rounded up)
-    l = __fadd_ru(fabsf(__fsub_rn(j.c.z, j.c.x)), fabsf(__fsub_rn(j.c.w, j.c.y)));
+    l = __fadd_ru(fabsf(__fsub_rn(j.z, j.x)), fabsf(__fsub_rn(j.w, j.y)));
     const double th = rv.theta[e];
     tlo = __double2float_rd(th);
     thi = __double2float_ru(th);
@@ -905,9 +927,9 @@ __device__ __forceinline__ double exact_pair(const EdgeRec *__restrict__ rec,
   return ANGLE ? angle_dev(theta[ei], theta[ej], ideal) : 0.0;
 }
 
-// M_k = max(P12, P34) of one j-edge (shared memory) against the thread's K
+// M_k = max(P12, P34) of a j-edge (shared memory) against the thread's K
 // i-edges; masked pairs of a diagonal tile get M = 2 (certain miss).
-// Per pair: 8 FFMA + 2 FMUL, issued as packed pairs over two i-edges.
+// Per pair: 8 FFMA + 2 FMUL/FFMA, issued as packed pairs (filter_m2).
 // Shared-memory loads by 32-bit shared address (the stage base is computed
 // once per unit, so the block loop carries no generic-to-shared conversions).
 // volatile: never hoisted above the stage's mbarrier wait.
@@ -937,104 +959,66 @@ __device__ __forceinline__ double lds_f64(unsigned addr) {
 // diagonal tile get M = 4 (t <= 1).  The fused kernel keeps FMUL2 products
 // (its SEL needs a predicate anyway, and the third FFMA2 operand cost it
 // 5%: 5.34 vs 5.08 s on C5).
+// M of a PAIR of j-edges (jj, jj+1; jj even) against the lane's kFK i-edges,
+// M2[h][k] for j-edge jj + h.  Mixed packing (the kernel is bound by
+// register-file reads, tools/rf_model.py): c1, c2 (the i-edge's line at the
+// two j-endpoints) are packed over the two j-edges -- the j coordinates are
+// a register pair of the JPair layout and the i-line constants scalars (4
+// reads instead of 5 in the inner FFMA2) -- while c3, c4 (the j-edge's line
+// at the i-endpoints) stay packed over the lane's i-edge pair with the
+// j-line constants as scalars.  The max of P12 and P34 is taken per 32-bit
+// half, so the two packings meet there.  Identical roundings to filter_m.
 template <bool DIAG, bool FOLD>
-__device__ __forceinline__ void filter_m(const FIRegs &R, unsigned jaddr, int jj, int islot,
-                                         uint64_t T2, float (&M)[kFK]) {
-  const float4 q0 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec));       // cx cy dx dy
-  const float4 q1 = lds_f4(jaddr + jj * (unsigned)sizeof(JRec) + 16);  // scdx -scdy -skc
-  const uint64_t CX = f2_bcast(q0.x), CY = f2_bcast(q0.y);
-  const uint64_t DX = f2_bcast(q0.z), DY = f2_bcast(q0.w);
-  const uint64_t SCDX = f2_bcast(q1.x), NSCDY = f2_bcast(q1.y), NSKC = f2_bcast(q1.z);
+__device__ __forceinline__ void filter_m2(const FIRegs &R, unsigned jaddr, int jj, int islot,
+                                          uint64_t T2, float (&M2)[2][kFK]) {
+  const unsigned pa = jaddr + (unsigned)jj * (unsigned)sizeof(JRec);
+  const float4 a0 = lds_f4(pa);       // cx0 cx1 cy0 cy1
+  const float4 a1 = lds_f4(pa + 16);  // dx0 dx1 dy0 dy1
+  const float4 a2 = lds_f4(pa + 32);  // scdx0 -scdy0 -skc0 scdx1
+  const float4 a3 = lds_f4(pa + 48);  // -scdy1 -skc1 0 0
+  const uint64_t CX = f2_pack(a0.x, a0.y), CY = f2_pack(a0.z, a0.w);
+  const uint64_t DX = f2_pack(a1.x, a1.y), DY = f2_pack(a1.z, a1.w);
+  const float scdx[2] = {a2.x, a2.w}, nscdy[2] = {a2.y, a3.x}, nskc[2] = {a2.z, a3.y};
 #pragma unroll
   for (int g = 0; g < kGroups; ++g) {
-    // c1 = ab x (c - a), c2 = ab x (d - a), c3 = cd x (a - c), c4 = cd x (b - c)
-    const uint64_t c1 = f2_fma(R.sabx[g], CY, f2_fma(R.nsaby[g], CX, R.nska[g]));
-    const uint64_t c2 = f2_fma(R.sabx[g], DY, f2_fma(R.nsaby[g], DX, R.nska[g]));
-    const uint64_t c3 = f2_fma(SCDX, R.ay[g], f2_fma(NSCDY, R.ax[g], NSKC));
-    const uint64_t c4 = f2_fma(SCDX, R.by[g], f2_fma(NSCDY, R.bx[g], NSKC));
-    const uint64_t p12 = FOLD ? f2_fma(c1, c2, T2) : f2_mul(c1, c2);
-    const uint64_t p34 = FOLD ? f2_fma(c3, c4, T2) : f2_mul(c3, c4);
-#ifndef GLR_XFMNMX
-    if (FOLD) {
-      // the signed-integer maximum of the bit patterns (ALU pipe; FMNMX
-      // competes with FFMA2): it equals max(P12, P34) when either is
-      // non-negative, and is negative (sign bit set) when both are -- all
-      // FOLD's hit (sign bit) and uncertain (bits in [+0, 2t]) tests read
-      M[2 * g] = __int_as_float(max(__float_as_int(f2_lo(p12)), __float_as_int(f2_lo(p34))));
-      M[2 * g + 1] =
-          __int_as_float(max(__float_as_int(f2_hi(p12)), __float_as_int(f2_hi(p34))));
-      continue;
-    }
-#endif
-    M[2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
-    M[2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
-  }
-  if (DIAG) {
+    uint64_t p12[2], p34[2];
 #pragma unroll
-    for (int k = 0; k < kFK; ++k)
-      if (!(jj > islot + 32 * k)) M[k] = FOLD ? 4.0f : 2.0f;
-  }
-}
-
-// The same M for NJ consecutive j-edges at once, computed operation by
-// operation across the block (GLR_XMB): consecutive FFMA2s then share an
-// operand in the same slot (the i-edge line constants across j-edges, the
-// j-edge line constants across i-groups), which the operand reuse cache
-// serves without register-file reads -- the kernel is bound by register
-// reads (tools/rf_model.py, profiles/r02_rfbench.txt).  Identical roundings.
-template <bool DIAG, bool FOLD, int NJ>
-__device__ __forceinline__ void filter_mb(const FIRegs &R, unsigned jaddr, int jj0, int islot,
-                                          uint64_t T2, float (&M)[NJ][kFK]) {
-  float4 q0[NJ], q1[NJ];
-#pragma unroll
-  for (int q = 0; q < NJ; ++q) {
-    q0[q] = lds_f4(jaddr + (jj0 + q) * (unsigned)sizeof(JRec));
-    q1[q] = lds_f4(jaddr + (jj0 + q) * (unsigned)sizeof(JRec) + 16);
-  }
-#pragma unroll
-  for (int g = 0; g < kGroups; ++g) {
-    uint64_t c1[NJ], c2[NJ], c3[NJ], c4[NJ];
-    // i-line at the j-endpoints: nsaby_g, nska_g shared by 2 NJ FFMA2s
-#pragma unroll
-    for (int q = 0; q < NJ; ++q) c1[q] = f2_fma(R.nsaby[g], f2_bcast(q0[q].x), R.nska[g]);
-#pragma unroll
-    for (int q = 0; q < NJ; ++q) c2[q] = f2_fma(R.nsaby[g], f2_bcast(q0[q].z), R.nska[g]);
-#pragma unroll
-    for (int q = 0; q < NJ; ++q) c1[q] = f2_fma(R.sabx[g], f2_bcast(q0[q].y), c1[q]);
-#pragma unroll
-    for (int q = 0; q < NJ; ++q) c2[q] = f2_fma(R.sabx[g], f2_bcast(q0[q].w), c2[q]);
-    // j-line at the i-endpoints: (nscdy, nskc) shared by c3/c4 of a j-edge
-#pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-      c3[q] = f2_fma(f2_bcast(q1[q].y), R.ax[g], f2_bcast(q1[q].z));
-      c4[q] = f2_fma(f2_bcast(q1[q].y), R.bx[g], f2_bcast(q1[q].z));
+    for (int h = 0; h < 2; ++h) {  // i-edge 2g + h: its line over (j0, j1)
+      const float sx = h ? f2_hi(R.sabx[g]) : f2_lo(R.sabx[g]);
+      const float ny = h ? f2_hi(R.nsaby[g]) : f2_lo(R.nsaby[g]);
+      const float nk = h ? f2_hi(R.nska[g]) : f2_lo(R.nska[g]);
+      // c1 = ab x (c - a), c2 = ab x (d - a): fma(sabx, y, fma(-saby, x, -ska))
+      const uint64_t c1 = f2_fma(f2_bcast(sx), CY, f2_fma(f2_bcast(ny), CX, f2_bcast(nk)));
+      const uint64_t c2 = f2_fma(f2_bcast(sx), DY, f2_fma(f2_bcast(ny), DX, f2_bcast(nk)));
+      p12[h] = FOLD ? f2_fma(c1, c2, T2) : f2_mul(c1, c2);
     }
 #pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-      c3[q] = f2_fma(f2_bcast(q1[q].x), R.ay[g], c3[q]);
-      c4[q] = f2_fma(f2_bcast(q1[q].x), R.by[g], c4[q]);
+    for (int q = 0; q < 2; ++q) {  // j-edge q: its line over the i-pair
+      // c3 = cd x (a - c), c4 = cd x (b - c)
+      const uint64_t c3 =
+          f2_fma(f2_bcast(scdx[q]), R.ay[g], f2_fma(f2_bcast(nscdy[q]), R.ax[g], f2_bcast(nskc[q])));
+      const uint64_t c4 =
+          f2_fma(f2_bcast(scdx[q]), R.by[g], f2_fma(f2_bcast(nscdy[q]), R.bx[g], f2_bcast(nskc[q])));
+      p34[q] = FOLD ? f2_fma(c3, c4, T2) : f2_mul(c3, c4);
     }
+    // (i_h, j_q): p12[h] half q, p34[q] half h
 #pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-      const uint64_t p12 = FOLD ? f2_fma(c1[q], c2[q], T2) : f2_mul(c1[q], c2[q]);
-      const uint64_t p34 = FOLD ? f2_fma(c3[q], c4[q], T2) : f2_mul(c3[q], c4[q]);
-      if (FOLD) {
-        M[q][2 * g] =
-            __int_as_float(max(__float_as_int(f2_lo(p12)), __float_as_int(f2_lo(p34))));
-        M[q][2 * g + 1] =
-            __int_as_float(max(__float_as_int(f2_hi(p12)), __float_as_int(f2_hi(p34))));
-      } else {
-        M[q][2 * g] = fmaxf(f2_lo(p12), f2_lo(p34));
-        M[q][2 * g + 1] = fmaxf(f2_hi(p12), f2_hi(p34));
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float a = q ? f2_hi(p12[h]) : f2_lo(p12[h]);
+        const float b = h ? f2_hi(p34[q]) : f2_lo(p34[q]);
+        M2[q][2 * g + h] = FOLD ? __int_as_float(max(__float_as_int(a), __float_as_int(b)))
+                                : fmaxf(a, b);
       }
     }
   }
   if (DIAG) {
 #pragma unroll
-    for (int q = 0; q < NJ; ++q)
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int k = 0; k < kFK; ++k)
-        if (!(jj0 + q > islot + 32 * k)) M[q][k] = FOLD ? 4.0f : 2.0f;
+        if (!(jj + q > islot + 32 * k)) M2[q][k] = FOLD ? 4.0f : 2.0f;
   }
 }
 
@@ -1107,18 +1091,15 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
   const unsigned vbits = __float_as_uint(2.0f * thr);
   unsigned mmin = 0xffffffffu;
   bool any = false;
-#ifdef GLR_XMB
+  static_assert(NJ % 2 == 0, "j-edges come in pairs (filter_m2)");
   float MB[NJ][kFK];
-  filter_mb<DIAG, FOLD, NJ>(R, jaddr, jj0, islot, T2, MB);
-#endif
+#pragma unroll
+  for (int q = 0; q < NJ; q += 2)
+    filter_m2<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2,
+                          *reinterpret_cast<float (*)[2][kFK]>(&MB[q][0]));
 #pragma unroll
   for (int q = 0; q < NJ; ++q) {
-#ifdef GLR_XMB
     float (&M)[kFK] = MB[q];
-#else
-    float M[kFK];
-    filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
-#endif
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
     if (SIGNED) {
       // hits are M's sign bits: C_k += hit (LEA.HI), h = hits on this j-edge,
@@ -1179,14 +1160,16 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     // and bit order (deterministic), and the path has no vote per pair
     unsigned U = 0;
 #pragma unroll
-    for (int q = 0; q < NJ; ++q) {
-      float M[kFK];
-      filter_m<DIAG, FOLD>(R, jaddr, jj0 + q, islot, T2, M);
+    for (int q2 = 0; q2 < NJ; q2 += 2) {
+      float M2[2][kFK];
+      filter_m2<DIAG, FOLD>(R, jaddr, jj0 + q2, islot, T2, M2);
 #pragma unroll
-      for (int k = 0; k < kFK; ++k) {
-        const bool u = FOLD ? __float_as_uint(M[k]) <= vbits : fabsf(M[k]) <= thr;
-        U |= (u ? 1u : 0u) << (q * kFK + k);
-      }
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < kFK; ++k) {
+          const bool u = FOLD ? __float_as_uint(M2[h][k]) <= vbits : fabsf(M2[h][k]) <= thr;
+          U |= (u ? 1u : 0u) << ((q2 + h) * kFK + k);
+        }
     }
     const unsigned lane = (unsigned)islot & 31u;
     const unsigned n = __popc(U);
