@@ -54,16 +54,25 @@ OCC_FMA_PER_PAIR = 168 / 32
 # difference, ~1e-4 of them on C5, take 4).
 FMA_PER_PAIR = 10
 # SASS instructions per pair of the hot block of cross_filter_kernel<angle>
-# in classified units (201 per 16 pairs, tools/sass_loop.py): the issue-slot
-# bound is 4 schedulers x 32 lanes x 148 SMs x clock / this.
-SASS_PER_PAIR = 201 / 16
+# in classified units with the capped threshold (159 per 16 pairs,
+# tools/sass_loop.py / tools/rf_model.py): the issue-slot bound is
+# 4 schedulers x 32 lanes x 148 SMs x clock / this.
+SASS_PER_PAIR = 159 / 16
+# Register-file operand reads per pair of the same block (477 per 16 pairs,
+# tools/rf_model.py), and the measured cost of one 32-bit vector-register
+# read per scheduler (0.56 cycles: FFMA2 P-S-P 2.75 cycles, FMUL2 P-P 2.2,
+# +LEA.HI +1.3, profiles/r02_rfbench.txt).  The model predicts the measured
+# per-pair time of the crossing filter (within 2% with the 23% of
+# instructions outside the hot block) and of the occlusion filter (3%).
+RF_READS_PER_PAIR = 477 / 16
+RF_CYCLES_PER_READ = 0.56
+OCC_RF_READS_PER_PAIR = 424 / 32
 FP64_PER_PAIR_FILTER_ECA = 2
 FMA_LANES_PER_CLK_SM = 128   # measured 124 (FFMA2/FMUL2/FADD2, profiles/r01_packed.txt)
 FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)
 # Bytes the pair kernel must read at least once per launch: i-role filter
 # record 36 B + j-role record 32 B + theta 8 B per edge.
 REC_BYTES_PER_EDGE = 76
-C5_DRAM_BYTES_PER_LAUNCH = 250_230_000_000 + 185_480_000   # profiles/r01_dram_c5_filter_v2.txt
 CPU_SAMPLE_EDGES = 120_000
 CPU_SAMPLE_SEED = 99
 
@@ -193,6 +202,25 @@ def run_reference(args, world, rank):
     return 0
 
 
+def _rf_bound(rate, sm_mhz, reads_per_pair):
+    peak = 4 * 148 * sm_mhz * 1e6 * 32 / (reads_per_pair * RF_CYCLES_PER_READ)
+    return {"reads_per_pair": reads_per_pair, "cycles_per_read": RF_CYCLES_PER_READ,
+            "pairs_per_s": peak, "frac": rate / peak,
+            "source": "tools/rf_model.py on the hot block; profiles/r02_rfbench.txt"}
+
+
+def _dram_bytes():
+    """DRAM read+write bytes of one full C5 fused launch (ncu), if profiled."""
+    path = os.path.join(REPO, "profiles", "r02_dram_c5.txt")
+    try:
+        with open(path) as f:
+            vals = [float(line.split("=")[1].split()[0]) * (1e9 if "Gbyte" in line else 1e6)
+                    for line in f if "dram__bytes_" in line and "=" in line]
+        return sum(vals) if vals else None
+    except (OSError, ValueError, IndexError):
+        return None
+
+
 def _occ_roofline(rate, sm_mhz):
     """Occlusion pass against its two compute ceilings per GPU: the FP32 FMA
     pipe (OCC_FMA_PER_PAIR lane-ops per pair at 128 lanes/clk/SM) and issue
@@ -203,6 +231,7 @@ def _occ_roofline(rate, sm_mhz):
             "frac": rate / fma_peak, "fma_lane_ops_per_pair": OCC_FMA_PER_PAIR,
             "issue_bound": {"sass_per_pair": OCC_SASS_PER_PAIR, "pairs_per_s": issue_peak,
                             "frac": rate / issue_peak},
+            "rf_read_bound": _rf_bound(rate, sm_mhz, OCC_RF_READS_PER_PAIR),
             "kernel": "occlusion_filter_kernel"}
 
 
@@ -499,13 +528,15 @@ def main():
                                          / fp64_peak_run},
                      # DRAM read+write bytes of one full-C5 launch from ncu
                      # (profiles/r01_dram_c5_filter.txt); per-rank share for N>1.
-                     "traffic": C5_DRAM_BYTES_PER_LAUNCH / world,
+                     "traffic": (_dram_bytes() / world) if _dram_bytes() else None,
                      "traffic_unit": "bytes/launch (dram__bytes_read+write, ncu)",
-                     # the binding resource per ncu (FMA pipe ~49% busy): issue slots
                      "issue_bound": {"sass_per_pair": SASS_PER_PAIR,
                                      "pairs_per_s": 4 * 32 * 148 * sm_mhz * 1e6 / SASS_PER_PAIR,
                                      "frac": pair_rate / (4 * 32 * 148 * sm_mhz * 1e6
                                                           / SASS_PER_PAIR)},
+                     # the resource that binds (K2): register-file
+                     # operand reads, RF_CYCLES_PER_READ scheduler cycles each
+                     "rf_read_bound": _rf_bound(pair_rate, sm_mhz, RF_READS_PER_PAIR),
                      "algorithmic_bytes": REC_BYTES_PER_EDGE * m},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
