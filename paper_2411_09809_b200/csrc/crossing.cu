@@ -1042,8 +1042,15 @@ __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned q
   for (unsigned b = 0; b < qn; b += 32) {
     if (b + lane < qn) {
       const unsigned ent = wq[b + lane];  // i slot << 8 | j slot
-      const double t = exact_pair<ANGLE>(rec, ids, theta, ibase + (ent >> 8),
-                                         jbase + (ent & 255u), ideal);
+      const int64_t ei = ibase + (ent >> 8), ej = jbase + (ent & 255u);
+#ifndef GLR_XNOIDCHECK
+      // a shared vertex index: never counted (exact.py:205-210), and most
+      // uncertain pairs are such pairs (an exact cross product is 0) -- skip
+      // exact_pair's random record loads for them
+      const int2 ia = ids[ei], ic = ids[ej];
+      if (ia.x == ic.x || ia.x == ic.y || ia.y == ic.x || ia.y == ic.y) continue;
+#endif
+      const double t = exact_pair<ANGLE>(rec, ids, theta, ei, ej, ideal);
       if (t >= 0.0) {
         cnt += 1u;
         if (ANGLE) dev = __dadd_rn(dev, t);
@@ -1159,6 +1166,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     // the lanes' entries by a warp prefix sum: positions depend only on lane
     // and bit order (deterministic), and the path has no vote per pair
     unsigned U = 0;
+#ifdef GLR_XREFILTER
 #pragma unroll
     for (int q2 = 0; q2 < NJ; q2 += 2) {
       float M2[2][kFK];
@@ -1171,6 +1179,29 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
           U |= (u ? 1u : 0u) << ((q2 + h) * kFK + k);
         }
     }
+#else
+    // the block's M values are still live: no re-filter
+#pragma unroll
+    for (int q = 0; q < NJ; ++q)
+#pragma unroll
+      for (int k = 0; k < kFK; ++k) {
+        const bool u = FOLD ? __float_as_uint(MB[q][k]) <= vbits : fabsf(MB[q][k]) <= thr;
+        U |= (u ? 1u : 0u) << (q * kFK + k);
+      }
+#endif
+#ifdef GLR_XIDCHECK_PLACE
+    // Pairs sharing a vertex index are never counted (exact.py:205-210) but
+    // are always uncertain (an exact cross product is 0): most of C5's
+    // uncertain pairs.  Drop them here from the ids (L1-resident: the
+    // slice's and the block's), so only genuine near-degenerate pairs reach
+    // exact_pair and its random 64 B record loads.
+    for (unsigned V = U; V != 0u; V &= V - 1u) {
+      const int b = __ffs(V) - 1;
+      const int2 a = ids[ibase + islot + 32 * (b % kFK)];
+      const int2 c = ids[jbase + jj0 + b / kFK];
+      if (a.x == c.x || a.x == c.y || a.y == c.x || a.y == c.y) U &= ~(1u << b);
+    }
+#endif
     const unsigned lane = (unsigned)islot & 31u;
     const unsigned n = __popc(U);
     unsigned incl = n;
