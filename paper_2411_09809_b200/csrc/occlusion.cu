@@ -470,6 +470,11 @@ int occlusion_run(const double *d_xy, int64_t n, double thr, const int2 *d_list,
     set_error("%s: invalid arguments", who);
     return GLR_EARG;
   }
+  if (n > ((int64_t)1 << 26) * 2) {  // the float64 count slot is exact below 2^53 pairs
+    set_error("%s: n=%lld vertices: n(n-1)/2 reaches 2^53, counts would round", who,
+              (long long)n);
+    return GLR_EARG;
+  }
   const uint64_t T = (uint64_t)(pad_vertices(n < 1 ? 1 : n) / kTile);
   const uint64_t U = d_list != nullptr ? list_len : tri_units(T);
   if (ubeg > uend || uend > U) {
