@@ -44,9 +44,9 @@ FP64_PER_PAIR_EC = 18      # DADD/DMUL of the reference predicate (SURVEY.md 8(d
 FP64_PER_PAIR_ECA = 22     # + 4 DADD of the fused crossing-angle deviation
 FP64_PER_PAIR_NC = 5
 # occlusion_filter_kernel hot block (tools/sass_loop.py, 4 j x 8 i = 32 pairs):
-# 154 SASS; FMA pipe: 48 FADD2 + 16 FMUL2 + 16 FFMA2 + 8 FADD = 168 lane-ops
-OCC_SASS_PER_PAIR = 154 / 32
-OCC_FMA_PER_PAIR = 168 / 32
+# 123 SASS; FMA pipe: 32 FADD2 + 32 FFMA2 = 128 lane-ops
+OCC_SASS_PER_PAIR = 123 / 32
+OCC_FMA_PER_PAIR = 128 / 32
 # The default pair kernel (certified FP32 filter) per pair:
 # 8 FFMA + 2 FMUL on the FP32 FMA pipe (issued as packed pairs) and, fused
 # with E_ca over theta-ordered edges, 2 DADD on the FP64 pipe (|theta_j -
@@ -66,7 +66,7 @@ SASS_PER_PAIR = 159 / 16
 # instructions outside the hot block) and of the occlusion filter (3%).
 RF_READS_PER_PAIR = 477 / 16
 RF_CYCLES_PER_READ = 0.56
-OCC_RF_READS_PER_PAIR = 424 / 32
+OCC_RF_READS_PER_PAIR = 371 / 32
 FP64_PER_PAIR_FILTER_ECA = 2
 FMA_LANES_PER_CLK_SM = 128   # measured 124 (FFMA2/FMUL2/FADD2, profiles/r01_packed.txt)
 FP64_LANES_PER_CLK_SM = 64   # measured 61.7 (profiles/r01_pipes.txt)

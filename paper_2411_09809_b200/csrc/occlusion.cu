@@ -196,15 +196,33 @@ occ_header_kernel(const double2 *__restrict__ xy, int64_t n, double thr, OccHead
   *h = H;
 }
 
-__global__ void occ_scale_kernel(const double2 *__restrict__ xy, int64_t n,
-                                 const OccHeader *__restrict__ h, float2 *__restrict__ sxy) {
+// Scaled FP32 coordinates twice: sxy[v] (the j role, staged per unit in
+// shared memory) and, for the i role, NEGATED and packed per thread so that
+// one 128-bit load gives a thread's i-vertex pair (v0, v1 = v0 + kThreads)
+// as two register pairs (-x0, -x1 | -y0, -y1): nip[(tile*kK/2 + g)*kThreads
+// + t] for tile slot t + 2g kThreads.  Pads (v >= n, up to the tile end):
+// i side -3e38 (negated +3e38), so every difference with a pad overflows to
+// infinity.
+constexpr float kOccPad = 3.0e38f;
+__global__ void occ_scale_kernel(const double2 *__restrict__ xy, int64_t n, int64_t n_pad,
+                                 const OccHeader *__restrict__ h, float2 *__restrict__ sxy,
+                                 float *__restrict__ nip) {
   if (!h->use) return;
   const double x0 = h->x0, y0 = h->y0, sc = h->sc;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_pad;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const double2 p = xy[v];
-    sxy[v] = make_float2(__double2float_rn(__dmul_rn(__dsub_rn(p.x, x0), sc)),
-                         __double2float_rn(__dmul_rn(__dsub_rn(p.y, y0), sc)));
+    float x = kOccPad, y = kOccPad;
+    if (v < n) {
+      const double2 p = xy[v];
+      x = __double2float_rn(__dmul_rn(__dsub_rn(p.x, x0), sc));
+      y = __double2float_rn(__dmul_rn(__dsub_rn(p.y, y0), sc));
+      sxy[v] = make_float2(x, y);
+    }
+    const int64_t tile = v / kTile;
+    const int slot = (int)(v % kTile), t = slot % kThreads, k = slot / kThreads;
+    float *q = nip + 4 * ((tile * (kK / 2) + k / 2) * kThreads + t);
+    q[k & 1] = -x;
+    q[2 + (k & 1)] = -y;
   }
 }
 
@@ -228,6 +246,11 @@ __device__ __forceinline__ uint64_t o2_sub(uint64_t a, uint64_t b) {
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ uint64_t o2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ uint64_t o2_mul(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -241,65 +264,70 @@ __device__ __forceinline__ uint64_t o2_fma(uint64_t a, uint64_t b, uint64_t c) {
 
 constexpr int kOccFBlock = 4;  // j-vertices per filter block (one warp vote)
 
-// S of one j against the thread's K i-vertices; masked diagonal pairs -> +inf
+// The threshold folded into the products (default): per pair
+//   d = RN(dY dY + RN(dX dX - t_lo))
+// (two FFMA2 per two pairs instead of FMUL2 + FFMA2 + FADD2: the filter is
+// bound by register-file reads, tools/rf_model.py).  The sign bit of d is
+// the exact pre-rounding value's sign, so d < 0 certifies occlusion and
+// d > RU(t_hi - t_lo) certifies non-occlusion with the same t_lo / t_hi as
+// the unfolded test (K3: the two roundings stay within 2^-23
+// max(S, t_lo), the budget the band already allots them;
+// tests/test_filter_bound.py checks it with exact rationals).  Masked
+// diagonal pairs -> +inf.
 template <bool DIAG>
-__device__ __forceinline__ void occ_s(const uint64_t (&X)[kK / 2], const uint64_t (&Y)[kK / 2],
-                                      float2 pj, int jj, float (&S)[kK]) {
+__device__ __forceinline__ void occ_d(const uint64_t (&X)[kK / 2], const uint64_t (&Y)[kK / 2],
+                                      float2 pj, int jj, uint64_t NEGTLO2, float (&D)[kK]) {
   const uint64_t XJ = o2_pack(pj.x, pj.x), YJ = o2_pack(pj.y, pj.y);
 #pragma unroll
   for (int g = 0; g < kK / 2; ++g) {
-    const uint64_t dx = o2_sub(XJ, X[g]), dy = o2_sub(YJ, Y[g]);
-    const uint64_t s = o2_fma(dy, dy, o2_mul(dx, dx));
-    S[2 * g] = o2_lo(s);
-    S[2 * g + 1] = o2_hi(s);
+    // X, Y hold the NEGATED i coordinates: dx = xj + (-xi) = RN(xj - xi)
+    const uint64_t dx = o2_add(XJ, X[g]), dy = o2_add(YJ, Y[g]);
+    const uint64_t d = o2_fma(dy, dy, o2_fma(dx, dx, NEGTLO2));
+    D[2 * g] = o2_lo(d);
+    D[2 * g + 1] = o2_hi(d);
   }
   if (DIAG) {
 #pragma unroll
     for (int k = 0; k < kK; ++k)
-      if (!(jj > (int)threadIdx.x + k * kThreads)) S[k] = INFINITY;
+      if (!(jj > (int)threadIdx.x + k * kThreads)) D[k] = INFINITY;
   }
 }
 
 template <bool DIAG>
 __device__ __forceinline__ void occ_filter_block(const uint64_t (&X)[kK / 2],
                                                  const uint64_t (&Y)[kK / 2], const float2 *sj,
-                                                 int jj0, const OccHeader &H, uint64_t NTLO2,
+                                                 int jj0, const OccHeader &H,
                                                  unsigned vote_bits,
                                                  const double2 *__restrict__ xy, int64_t ibase,
                                                  int64_t jbase, int64_t n,
                                                  unsigned long long thr_bits,
                                                  unsigned (&cnt)[kK]) {
-  // min over the block of d = S - tlo viewed as unsigned: a non-negative
-  // float orders like its bit pattern and a negative one (certain hit) is
-  // above every non-negative, so one VIMNMX3 per two pairs finds whether any
-  // d lies in [0, RU(thi - tlo)] -- a superset of the uncertain band
+  // min over the block of d viewed as unsigned: a non-negative float orders
+  // like its bit pattern and a negative one (certain hit) is above every
+  // non-negative, so one VIMNMX3 per two pairs finds whether any d lies in
+  // [+0, RU(thi - tlo)], the uncertain band
   unsigned m = 0xffffffffu;
+  const uint64_t NEGTLO2 = o2_pack(-H.tlo, -H.tlo);
 #pragma unroll
   for (int q = 0; q < kOccFBlock; ++q) {
-    float S[kK];
-    occ_s<DIAG>(X, Y, sj[jj0 + q], jj0 + q, S);
+    float D[kK];
+    occ_d<DIAG>(X, Y, sj[jj0 + q], jj0 + q, NEGTLO2, D);
 #pragma unroll
-    for (int g = 0; g < kK / 2; ++g) {
-      // d = S - tlo (packed): S < tlo exactly when d's sign bit is set (RN
-      // keeps the sign of the difference; d is +0 when S == tlo)
-      const uint64_t d = o2_sub(o2_pack(S[2 * g], S[2 * g + 1]), NTLO2);
-      const unsigned dlo = __float_as_uint(o2_lo(d)), dhi = __float_as_uint(o2_hi(d));
-      cnt[2 * g] += dlo >> 31;
-      cnt[2 * g + 1] += dhi >> 31;
-      // uncertain band [tlo, thi] => RN(S - tlo) in [+0, RN(thi - tlo)] (RN is
-      // monotone and S - tlo = +0 at S = tlo)
-      m = min(m, min(dlo, dhi));
+    for (int k = 0; k < kK; ++k) {
+      const unsigned b = __float_as_uint(D[k]);
+      cnt[k] += b >> 31;  // certain hit: the sign bit
+      m = min(m, b);      // uncertain: bits in [+0, RU(thi - tlo)]
     }
   }
   if (__any_sync(0xffffffffu, m <= vote_bits)) {
 #pragma unroll 1
     for (int q = 0; q < kOccFBlock; ++q) {
-      float S[kK];
-      occ_s<DIAG>(X, Y, sj[jj0 + q], jj0 + q, S);
+      float D[kK];
+      occ_d<DIAG>(X, Y, sj[jj0 + q], jj0 + q, NEGTLO2, D);
       const int64_t vj = jbase + jj0 + q;
 #pragma unroll
       for (int k = 0; k < kK; ++k) {
-        if (S[k] >= H.tlo && S[k] <= H.thi) {  // uncertain: the reference's FP64 test
+        if (__float_as_uint(D[k]) <= vote_bits) {  // uncertain: the reference's FP64 test
           const int64_t vi = ibase + threadIdx.x + k * kThreads;
           if (vi < n && vj < n) {
             const double2 a = xy[vi], b = xy[vj];
@@ -311,25 +339,26 @@ __device__ __forceinline__ void occ_filter_block(const uint64_t (&X)[kK / 2],
       }
     }
   }
+
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict__ sxy,
+                        const float4 *__restrict__ nip,
                         const OccHeader *__restrict__ hdr, int64_t n,
                         const int2 *__restrict__ ulist, uint64_t T, uint64_t ubeg, uint64_t uend,
                         unsigned long long thr_bits, unsigned long long *__restrict__ cta_cnt) {
   if (!hdr->use) return;
   const OccHeader H = *hdr;
   // packed constant tlo; vote bound = the band width rounded up, as bits
-  const uint64_t NTLO2 = o2_pack(H.tlo, H.tlo);
   const unsigned vote_bits = __float_as_uint(__fsub_ru(H.thi, H.tlo));
   __shared__ __align__(16) float2 sj[kTile];
   __shared__ unsigned long long red[kThreads / 32];
   const uint64_t span = uend - ubeg;
   const uint64_t b = ubeg + span * blockIdx.x / gridDim.x;
   const uint64_t e = ubeg + span * (blockIdx.x + 1) / gridDim.x;
-  // pads: i side +3e38, j side -3e38: differences overflow to +-inf, S = inf
-  const float PADF = 3.0e38f;
+  // pads: i side +3e38 (nip), j side -3e38: differences overflow, d = inf
+  const float PADF = kOccPad;
   unsigned long long total = 0;
   uint64_t X[kK / 2], Y[kK / 2];
   uint64_t ti = 0, tj = 0, cur = ~0ull;
@@ -343,12 +372,11 @@ occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict
     if (ti != cur) {
 #pragma unroll
       for (int g = 0; g < kK / 2; ++g) {
-        const int64_t v0 = (int64_t)ti * kTile + threadIdx.x + (2 * g) * kThreads;
-        const int64_t v1 = v0 + kThreads;
-        const float2 p0 = v0 < n ? sxy[v0] : make_float2(PADF, PADF);
-        const float2 p1 = v1 < n ? sxy[v1] : make_float2(PADF, PADF);
-        X[g] = o2_pack(p0.x, p1.x);
-        Y[g] = o2_pack(p0.y, p1.y);
+        // the negated i coordinates (exact), so the pair loop adds with no
+        // per-iteration negation
+        const float4 q = nip[((int64_t)ti * (kK / 2) + g) * kThreads + threadIdx.x];
+        X[g] = o2_pack(q.x, q.y);
+        Y[g] = o2_pack(q.z, q.w);
       }
       cur = ti;
     }
@@ -364,12 +392,12 @@ occlusion_filter_kernel(const double2 *__restrict__ xy, const float2 *__restrict
     const int64_t ibase = (int64_t)ti * kTile, jbase = (int64_t)tj * kTile;
     if (ti == tj) {
       for (int jj = 0; jj < kTile; jj += kOccFBlock)
-        occ_filter_block<true>(X, Y, sj, jj, H, NTLO2, vote_bits, xy, ibase, jbase, n,
+        occ_filter_block<true>(X, Y, sj, jj, H, vote_bits, xy, ibase, jbase, n,
                                thr_bits, cnt);
     } else {
 #pragma unroll 1
       for (int jj = 0; jj < kTile; jj += kOccFBlock)
-        occ_filter_block<false>(X, Y, sj, jj, H, NTLO2, vote_bits, xy, ibase, jbase, n,
+        occ_filter_block<false>(X, Y, sj, jj, H, vote_bits, xy, ibase, jbase, n,
                                 thr_bits, cnt);
     }
     unsigned c = 0;
@@ -491,22 +519,26 @@ int occlusion_run(const double *d_xy, int64_t n, double thr, const int2 *d_list,
   const int grid = (int)g;
   const size_t a_cta = ((size_t)grid * sizeof(unsigned long long) + 255) & ~(size_t)255;
   const size_t a_hdr = 256;
+  const int64_t n_pad = (int64_t)T * kTile;
   const size_t a_sxy = ((size_t)n * sizeof(float2) + 255) & ~(size_t)255;
-  Scratch scr(a_cta + a_hdr + (use_filter ? a_sxy : 0), st);
+  const size_t a_nip = ((size_t)n_pad * sizeof(float2) + 255) & ~(size_t)255;
+  Scratch scr(a_cta + a_hdr + (use_filter ? a_sxy + a_nip : 0), st);
   GLR_CUDA(scr.err);
   unsigned long long *cta = scr.as<unsigned long long>();
   OccHeader *hdr = reinterpret_cast<OccHeader *>(scr.as<char>() + a_cta);
   float2 *sxy = reinterpret_cast<float2 *>(scr.as<char>() + a_cta + a_hdr);
+  float *nip = reinterpret_cast<float *>(scr.as<char>() + a_cta + a_hdr + a_sxy);
   unsigned long long thr_bits;
   memcpy(&thr_bits, &thr, sizeof(thr));
   const double2 *xy = reinterpret_cast<const double2 *>(d_xy);
   if (use_filter) {
     occ_header_kernel<<<1, 1024, 0, st>>>(xy, n, thr, hdr);
     GLR_LAUNCHED("occ_header_kernel");
-    occ_scale_kernel<<<occ_blocks(n), 128, 0, st>>>(xy, n, hdr, sxy);
+    occ_scale_kernel<<<occ_blocks(n_pad), 128, 0, st>>>(xy, n, n_pad, hdr, sxy, nip);
     GLR_LAUNCHED("occ_scale_kernel");
-    occlusion_filter_kernel<<<grid, kThreads, 0, st>>>(xy, sxy, hdr, n, d_list, T, ubeg, uend,
-                                                       thr_bits, cta);
+    occlusion_filter_kernel<<<grid, kThreads, 0, st>>>(
+        xy, sxy, reinterpret_cast<const float4 *>(nip), hdr, n, d_list, T, ubeg, uend, thr_bits,
+        cta);
     GLR_LAUNCHED("occlusion_filter_kernel");
   }
   occlusion_pairs_kernel<<<grid, kThreads, 0, st>>>(xy, n, d_list, T, ubeg, uend, thr_bits,

@@ -434,9 +434,11 @@ def _occ_header(xy: np.ndarray, thr: float):
 
 
 def test_occlusion_band_certifies():
-    """S~ = RN(RN(dY dY) ... ) of the packed filter: S~ < T_lo must be an
+    """S~ = RN(dY dY + RN(dX dX)) of the packed filter: S~ < T_lo must be an
     occluding pair of the reference (FP64 dx*dx + dy*dy < (2r)^2, strict),
-    S~ > T_hi a non-occluding one; exact ties and near-ties included."""
+    S~ > T_hi a non-occluding one; and the folded form the kernel runs,
+    d = RN(dY dY + RN(dX dX - T_lo)): d < 0 occluding, d > RU(T_hi - T_lo)
+    not.  Exact ties and near-ties included."""
     rng = np.random.default_rng(17)
     checked = {"hit": 0, "miss": 0, "uncertain": 0}
     for trial in range(12):
@@ -475,8 +477,20 @@ def test_occlusion_band_certifies():
                     checked["miss"] += 1
                 else:
                     checked["uncertain"] += 1
+                # the folded evaluation the kernel runs (occlusion.cu occ_d):
+                # d = RN(dY dY + RN(dX dX - tlo)); hit <=> the pre-rounding
+                # value is negative (d's sign bit); miss <=> d > RU(thi - tlo)
+                e = rn32(dX * dX - Fr(tlo))
+                w = dY * dY + e
+                dfold = rn32(w)
+                if w < 0:
+                    assert ref, ("fold", trial, i, j)
+                    checked["fold_hit"] = checked.get("fold_hit", 0) + 1
+                elif dfold > Fr(ru32(thi - tlo)):
+                    assert not ref, ("fold", trial, i, j)
                 # the error bound the band is built from
                 St = Fr(dx * dx + dy * dy) * Fr(sc) * Fr(sc)
                 if St < Fr(8 * T):
                     assert abs(S - St) <= Fr(_occ_E(float(St))), (trial, i, j)
     assert checked["hit"] > 50 and checked["miss"] > 1000 and checked["uncertain"] > 0, checked
+    assert checked["fold_hit"] >= checked["hit"] // 2, checked
