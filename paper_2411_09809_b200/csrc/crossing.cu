@@ -90,6 +90,15 @@ constexpr int kFilterBlockCount = GLR_XFBLOCK_C;  // same for the count-only ker
 #define GLR_XFBLOCK_S 4
 #endif
 constexpr int kFilterBlockSigned = GLR_XFBLOCK_S;  // same for signed units
+// unroll of the j-block loops over a tile (signed units / count-only, t = 1)
+#ifndef GLR_XJUNROLL_S
+#define GLR_XJUNROLL_S 1
+#endif
+#ifndef GLR_XJUNROLL_C
+#define GLR_XJUNROLL_C 1
+#endif
+constexpr int kJUnrollS = GLR_XJUNROLL_S;
+constexpr int kJUnrollC = GLR_XJUNROLL_C;
 // CTAs per SM of the filter kernel (fused 4 -> <= 128 registers, count-only
 // 5 -> <= 102, with kFK = 4):
 // tools/c5_time.py and tools/config_bench.py, profiles/r01_variants_filter.txt
@@ -1619,7 +1628,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else if (ANGLE && am == 2) {
       if (thr == 1.0f) {
-#pragma unroll 1
+#pragma unroll kJUnrollS
         for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
           filter_block<ANGLE, false, kFilterBlockSigned, 2, true>(
               R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa, rec, ids, theta, ibase,
@@ -1632,7 +1641,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                                                             ibase, jbase, wq, qn, qc);
       }
     } else if (!ANGLE && thr == 1.0f) {
-#pragma unroll 1
+#pragma unroll kJUnrollC
       for (int jj = 0; jj < kTile; jj += kNJ)
         filter_block<ANGLE, false, kNJ, 0, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
                                                  ideal, kappa, rec, ids, theta, ibase, jbase, wq,
