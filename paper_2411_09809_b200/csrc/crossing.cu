@@ -1038,7 +1038,14 @@ __device__ __forceinline__ void filter_m2(const FIRegs &R, unsigned jaddr, int j
 // of the slice, or when the queue is full.  Results go to the lane's
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
+#ifndef GLR_XNOLANEQ
+// per-lane queues (GLR_XNOLANEQ: one warp queue with prefix-sum placement):
+// kLQ entries per lane, lane-minor (entry i of lane l at i * 32 + l)
+constexpr unsigned kLQ = 24;  // 32 x 24 x 2 B per warp: the fused kernel stays under 48 KB static smem
+constexpr unsigned kQCap = 32 * kLQ;
+#else
 constexpr unsigned kQCap = GLR_XFBLOCK_S > 4 ? 32 * GLR_XFBLOCK_S * 4 : 512;  // per warp (>= 32 lanes x NJ x kFK)
+#endif
 static_assert(kTile <= 256, "queue entries hold 8-bit tile slots");
 template <bool ANGLE>
 __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
@@ -1068,6 +1075,32 @@ __device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned q
   }
   __syncwarp();
 }
+
+#ifndef GLR_XNOLANEQ
+// The lane's own queue entries, in insertion order (no cross-lane traffic:
+// lanes drain independently, sums stay deterministic).
+template <bool ANGLE>
+__device__ __forceinline__ void drain_lane(const unsigned short *wq, unsigned qn, unsigned lane,
+                                           const EdgeRec *__restrict__ rec,
+                                           const int2 *__restrict__ ids,
+                                           const double *__restrict__ theta, int64_t ibase,
+                                           int64_t jbase, double ideal, unsigned &cnt,
+                                           double &dev) {
+  for (unsigned i = 0; i < qn; ++i) {
+    const unsigned ent = wq[i * 32 + lane];  // i slot << 8 | j slot
+    const int64_t ei = ibase + (ent >> 8), ej = jbase + (ent & 255u);
+#ifndef GLR_XNOIDCHECK
+    const int2 ia = ids[ei], ic = ids[ej];
+    if (ia.x == ic.x || ia.x == ic.y || ia.y == ic.x || ia.y == ic.y) continue;
+#endif
+    const double t = exact_pair<ANGLE>(rec, ids, theta, ei, ej, ideal);
+    if (t >= 0.0) {
+      cnt += 1u;
+      if (ANGLE) dev = __dadd_rn(dev, t);
+    }
+  }
+}
+#endif
 
 // NJ consecutive j-edges against the thread's K i-edges.  Certain hits are
 // counted (and their angle deviations summed) with predicated adds; one
@@ -1212,6 +1245,23 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     }
 #endif
     const unsigned lane = (unsigned)islot & 31u;
+#ifndef GLR_XNOLANEQ
+    // per-lane queue: no prefix sum; drain the lane's entries when this
+    // block's could overflow them
+    if (qn + __popc(U) > kLQ) {
+      drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
+                        SIGNED ? qc : cnt[0], dev[0]);
+      qn = 0;
+    }
+    while (U != 0u) {
+      const int b = __ffs(U) - 1;
+      U &= U - 1u;
+      wq[qn * 32u + lane] = (unsigned short)(((unsigned)(islot + 32 * (b % kFK)) << 8) |
+                                            (unsigned)(jj0 + b / kFK));
+      ++qn;
+    }
+    return;
+#endif
     const unsigned n = __popc(U);
     unsigned incl = n;
 #pragma unroll
@@ -1670,9 +1720,15 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // stage is released)
     if (qn != 0) {
       if (ANGLE && am == 2)
+#ifndef GLR_XNOLANEQ
+        drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
+      else
+        drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+#else
         drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
       else
         drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+#endif
     }
     unsigned c = qc;
 #pragma unroll
@@ -1812,7 +1868,11 @@ cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                                                      jbase, wq, qn, qc);
       }
       if (qn != 0)
+#ifndef GLR_XNOLANEQ
+        drain_lane<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+#else
         drain_queue<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+#endif
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
