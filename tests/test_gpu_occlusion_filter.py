@@ -35,6 +35,15 @@ def _random(seed, n, kind):
         xy = rng.integers(0, 200, (n, 2)).astype(np.float64)
     elif kind == "offset":
         xy = 2.0 ** 40 + rng.integers(0, 300, (n, 2)).astype(np.float64) * 0.25
+    elif kind == "ring":
+        # pairs at distance 2r (r = 0.75 here) scaled by 1 +- k 2^-52 and by
+        # 1 +- 2^-24 (the FP32 resolution), in random directions, around
+        # random centres at an offset: every folded-test band case
+        c = 1000.0 + rng.uniform(0, 50, (n // 2, 2))
+        ang = rng.uniform(0, 2 * np.pi, n // 2)
+        f = 1.0 + rng.choice([0, 1, -1, 2, -2, 2 ** 28, -(2 ** 28)], n // 2) * 2.0 ** -52
+        d = 1.5 * f
+        xy = np.concatenate([c, c + d[:, None] * np.stack([np.cos(ang), np.sin(ang)], 1)])
     elif kind == "cluster":
         xy = np.concatenate([rng.uniform(0, 1e-6, (n // 2, 2)), rng.uniform(0, 10, (n - n // 2, 2))])
     else:
@@ -42,7 +51,7 @@ def _random(seed, n, kind):
     return LayoutGraph(np.arange(n), xy, np.empty((0, 2), dtype=np.int64))
 
 
-@pytest.mark.parametrize("kind,r", [("lattice", 1.0), ("lattice", 2.5), ("offset", 0.5),
+@pytest.mark.parametrize("kind,r", [("lattice", 1.0), ("lattice", 2.5), ("offset", 0.5), ("ring", 0.75),
                                     ("cluster", 1e-7), ("cluster", 0.3), ("uniform", 0.7),
                                     ("uniform", 1e-9), ("uniform", 1e9)])
 @pytest.mark.parametrize("strategy", ["dense", "culled"])
