@@ -1038,45 +1038,12 @@ __device__ __forceinline__ void filter_m2(const FIRegs &R, unsigned jaddr, int j
 // of the slice, or when the queue is full.  Results go to the lane's
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
-#ifndef GLR_XNOLANEQ
-// per-lane queues (GLR_XNOLANEQ: one warp queue with prefix-sum placement):
-// kLQ entries per lane, lane-minor (entry i of lane l at i * 32 + l)
-constexpr unsigned kLQ = 24;  // 32 x 24 x 2 B per warp: the fused kernel stays under 48 KB static smem
+// per-lane queues of uncertain pairs: kLQ entries per lane, lane-minor
+// (entry i of lane l at i * 32 + l); 32 x 24 x 2 B per warp keeps the fused
+// kernel under 48 KB of static shared memory
+constexpr unsigned kLQ = 24;
 constexpr unsigned kQCap = 32 * kLQ;
-#else
-constexpr unsigned kQCap = GLR_XFBLOCK_S > 4 ? 32 * GLR_XFBLOCK_S * 4 : 512;  // per warp (>= 32 lanes x NJ x kFK)
-#endif
 static_assert(kTile <= 256, "queue entries hold 8-bit tile slots");
-template <bool ANGLE>
-__device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
-                                         const EdgeRec *__restrict__ rec,
-                                         const int2 *__restrict__ ids,
-                                         const double *__restrict__ theta, int64_t ibase,
-                                         int64_t jbase, double ideal, unsigned &cnt,
-                                         double &dev) {
-  __syncwarp();
-  for (unsigned b = 0; b < qn; b += 32) {
-    if (b + lane < qn) {
-      const unsigned ent = wq[b + lane];  // i slot << 8 | j slot
-      const int64_t ei = ibase + (ent >> 8), ej = jbase + (ent & 255u);
-#ifndef GLR_XNOIDCHECK
-      // a shared vertex index: never counted (exact.py:205-210), and most
-      // uncertain pairs are such pairs (an exact cross product is 0) -- skip
-      // exact_pair's random record loads for them
-      const int2 ia = ids[ei], ic = ids[ej];
-      if (ia.x == ic.x || ia.x == ic.y || ia.y == ic.x || ia.y == ic.y) continue;
-#endif
-      const double t = exact_pair<ANGLE>(rec, ids, theta, ei, ej, ideal);
-      if (t >= 0.0) {
-        cnt += 1u;
-        if (ANGLE) dev = __dadd_rn(dev, t);
-      }
-    }
-  }
-  __syncwarp();
-}
-
-#ifndef GLR_XNOLANEQ
 // The lane's own queue entries, in insertion order (no cross-lane traffic:
 // lanes drain independently, sums stay deterministic).
 template <bool ANGLE>
@@ -1100,7 +1067,6 @@ __device__ __forceinline__ void drain_lane(const unsigned short *wq, unsigned qn
     }
   }
 }
-#endif
 
 // NJ consecutive j-edges against the thread's K i-edges.  Certain hits are
 // counted (and their angle deviations summed) with predicated adds; one
@@ -1204,25 +1170,10 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     }
   }
   if (__any_sync(0xffffffffu, FOLD ? mmin <= vbits : any)) {
-    // re-filter the block into a per-lane mask (bit q*kFK + k), then place
-    // the lanes' entries by a warp prefix sum: positions depend only on lane
-    // and bit order (deterministic), and the path has no vote per pair
+    // the block's M values (still live) into a per-lane mask of its
+    // uncertain pairs (bit q*kFK + k), appended to the lane's own queue in
+    // bit order: positions depend only on the lane's history (deterministic)
     unsigned U = 0;
-#ifdef GLR_XREFILTER
-#pragma unroll
-    for (int q2 = 0; q2 < NJ; q2 += 2) {
-      float M2[2][kFK];
-      filter_m2<DIAG, FOLD>(R, jaddr, jj0 + q2, islot, T2, M2);
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < kFK; ++k) {
-          const bool u = FOLD ? __float_as_uint(M2[h][k]) <= vbits : fabsf(M2[h][k]) <= thr;
-          U |= (u ? 1u : 0u) << ((q2 + h) * kFK + k);
-        }
-    }
-#else
-    // the block's M values are still live: no re-filter
 #pragma unroll
     for (int q = 0; q < NJ; ++q)
 #pragma unroll
@@ -1230,22 +1181,11 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         const bool u = FOLD ? __float_as_uint(MB[q][k]) <= vbits : fabsf(MB[q][k]) <= thr;
         U |= (u ? 1u : 0u) << (q * kFK + k);
       }
-#endif
-#ifdef GLR_XIDCHECK_PLACE
-    // Pairs sharing a vertex index are never counted (exact.py:205-210) but
-    // are always uncertain (an exact cross product is 0): most of C5's
-    // uncertain pairs.  Drop them here from the ids (L1-resident: the
-    // slice's and the block's), so only genuine near-degenerate pairs reach
-    // exact_pair and its random 64 B record loads.
-    for (unsigned V = U; V != 0u; V &= V - 1u) {
-      const int b = __ffs(V) - 1;
-      const int2 a = ids[ibase + islot + 32 * (b % kFK)];
-      const int2 c = ids[jbase + jj0 + b / kFK];
-      if (a.x == c.x || a.x == c.y || a.y == c.x || a.y == c.y) U &= ~(1u << b);
-    }
-#endif
     const unsigned lane = (unsigned)islot & 31u;
-#ifndef GLR_XNOLANEQ
+#ifdef GLR_XFSTATS
+    if (lane == 0) atomicAdd(&g_fstats[0], 1ull);
+    atomicAdd(&g_fstats[1], (unsigned long long)__popc(U));
+#endif
     // per-lane queue: no prefix sum; drain the lane's entries when this
     // block's could overflow them
     if (qn + __popc(U) > kLQ) {
@@ -1260,37 +1200,6 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
                                             (unsigned)(jj0 + b / kFK));
       ++qn;
     }
-    return;
-#endif
-    const unsigned n = __popc(U);
-    unsigned incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (unsigned)o) incl += v;
-    }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-#ifdef GLR_XFSTATS
-    if (lane == 0) {
-      atomicAdd(&g_fstats[0], 1ull);
-      atomicAdd(&g_fstats[1], (unsigned long long)total);
-    }
-#endif
-    if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
-      // queued hits: the signed form's C_k multiply x_k, so they count
-      // apart (qc); their deviations go to dev[0], unused by that form
-      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
-                         SIGNED ? qc : cnt[0], dev[0]);
-      qn = 0;
-    }
-    unsigned pos = qn + incl - n;
-    while (U != 0u) {
-      const int b = __ffs(U) - 1;
-      U &= U - 1u;
-      wq[pos++] = (unsigned short)(((unsigned)(islot + 32 * (b % kFK)) << 8) |
-                                   (unsigned)(jj0 + b / kFK));
-    }
-    qn += total;
   }
 }
 
@@ -1720,15 +1629,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // stage is released)
     if (qn != 0) {
       if (ANGLE && am == 2)
-#ifndef GLR_XNOLANEQ
         drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
       else
         drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
-#else
-        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
-      else
-        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
-#endif
     }
     unsigned c = qc;
 #pragma unroll
@@ -1868,11 +1771,7 @@ cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                                                      jbase, wq, qn, qc);
       }
       if (qn != 0)
-#ifndef GLR_XNOLANEQ
         drain_lane<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
-#else
-        drain_queue<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
-#endif
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
