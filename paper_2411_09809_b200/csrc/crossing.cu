@@ -1038,34 +1038,35 @@ __device__ __forceinline__ void filter_m2(const FIRegs &R, unsigned jaddr, int j
 // of the slice, or when the queue is full.  Results go to the lane's
 // cnt[0]/dev[0]: the queue order and the drain points depend only on the
 // slice, so sums stay deterministic.
-// per-lane queues of uncertain pairs: kLQ entries per lane, lane-minor
-// (entry i of lane l at i * 32 + l); 32 x 24 x 2 B per warp keeps the fused
-// kernel under 48 KB of static shared memory
-constexpr unsigned kLQ = 24;
-constexpr unsigned kQCap = 32 * kLQ;
+constexpr unsigned kQCap = GLR_XFBLOCK_S > 4 ? 32 * GLR_XFBLOCK_S * 4 : 512;  // per warp (>= 32 lanes x NJ x kFK)
 static_assert(kTile <= 256, "queue entries hold 8-bit tile slots");
-// The lane's own queue entries, in insertion order (no cross-lane traffic:
-// lanes drain independently, sums stay deterministic).
 template <bool ANGLE>
-__device__ __forceinline__ void drain_lane(const unsigned short *wq, unsigned qn, unsigned lane,
-                                           const EdgeRec *__restrict__ rec,
-                                           const int2 *__restrict__ ids,
-                                           const double *__restrict__ theta, int64_t ibase,
-                                           int64_t jbase, double ideal, unsigned &cnt,
-                                           double &dev) {
-  for (unsigned i = 0; i < qn; ++i) {
-    const unsigned ent = wq[i * 32 + lane];  // i slot << 8 | j slot
-    const int64_t ei = ibase + (ent >> 8), ej = jbase + (ent & 255u);
+__device__ __forceinline__ void drain_queue(const unsigned short *wq, unsigned qn, unsigned lane,
+                                         const EdgeRec *__restrict__ rec,
+                                         const int2 *__restrict__ ids,
+                                         const double *__restrict__ theta, int64_t ibase,
+                                         int64_t jbase, double ideal, unsigned &cnt,
+                                         double &dev) {
+  __syncwarp();
+  for (unsigned b = 0; b < qn; b += 32) {
+    if (b + lane < qn) {
+      const unsigned ent = wq[b + lane];  // i slot << 8 | j slot
+      const int64_t ei = ibase + (ent >> 8), ej = jbase + (ent & 255u);
 #ifndef GLR_XNOIDCHECK
-    const int2 ia = ids[ei], ic = ids[ej];
-    if (ia.x == ic.x || ia.x == ic.y || ia.y == ic.x || ia.y == ic.y) continue;
+      // a shared vertex index: never counted (exact.py:205-210), and most
+      // uncertain pairs are such pairs (an exact cross product is 0) -- skip
+      // exact_pair's random record loads for them
+      const int2 ia = ids[ei], ic = ids[ej];
+      if (ia.x == ic.x || ia.x == ic.y || ia.y == ic.x || ia.y == ic.y) continue;
 #endif
-    const double t = exact_pair<ANGLE>(rec, ids, theta, ei, ej, ideal);
-    if (t >= 0.0) {
-      cnt += 1u;
-      if (ANGLE) dev = __dadd_rn(dev, t);
+      const double t = exact_pair<ANGLE>(rec, ids, theta, ei, ej, ideal);
+      if (t >= 0.0) {
+        cnt += 1u;
+        if (ANGLE) dev = __dadd_rn(dev, t);
+      }
     }
   }
+  __syncwarp();
 }
 
 // NJ consecutive j-edges against the thread's K i-edges.  Certain hits are
@@ -1171,8 +1172,9 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
   }
   if (__any_sync(0xffffffffu, FOLD ? mmin <= vbits : any)) {
     // the block's M values (still live) into a per-lane mask of its
-    // uncertain pairs (bit q*kFK + k), appended to the lane's own queue in
-    // bit order: positions depend only on the lane's history (deterministic)
+    // uncertain pairs (bit q*kFK + k); a warp prefix sum places the lanes'
+    // entries: positions depend only on lane and bit order (deterministic),
+    // and the queue is drained by all 32 lanes at once
     unsigned U = 0;
 #pragma unroll
     for (int q = 0; q < NJ; ++q)
@@ -1182,24 +1184,35 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         U |= (u ? 1u : 0u) << (q * kFK + k);
       }
     const unsigned lane = (unsigned)islot & 31u;
+    const unsigned n = __popc(U);
+    unsigned incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
 #ifdef GLR_XFSTATS
-    if (lane == 0) atomicAdd(&g_fstats[0], 1ull);
-    atomicAdd(&g_fstats[1], (unsigned long long)__popc(U));
+    if (lane == 0) {
+      atomicAdd(&g_fstats[0], 1ull);
+      atomicAdd(&g_fstats[1], (unsigned long long)total);
+    }
 #endif
-    // per-lane queue: no prefix sum; drain the lane's entries when this
-    // block's could overflow them
-    if (qn + __popc(U) > kLQ) {
-      drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
-                        SIGNED ? qc : cnt[0], dev[0]);
+    if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
+      // queued hits: the signed form's C_k multiply x_k, so they count
+      // apart (qc); their deviations go to dev[0], unused by that form
+      drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
+                         SIGNED ? qc : cnt[0], dev[0]);
       qn = 0;
     }
+    unsigned pos = qn + incl - n;
     while (U != 0u) {
       const int b = __ffs(U) - 1;
       U &= U - 1u;
-      wq[qn * 32u + lane] = (unsigned short)(((unsigned)(islot + 32 * (b % kFK)) << 8) |
-                                            (unsigned)(jj0 + b / kFK));
-      ++qn;
+      wq[pos++] = (unsigned short)(((unsigned)(islot + 32 * (b % kFK)) << 8) |
+                                   (unsigned)(jj0 + b / kFK));
     }
+    qn += total;
   }
 }
 
@@ -1629,9 +1642,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // stage is released)
     if (qn != 0) {
       if (ANGLE && am == 2)
-        drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
+        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
       else
-        drain_lane<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
     }
     unsigned c = qc;
 #pragma unroll
@@ -1771,7 +1784,7 @@ cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                                                      jbase, wq, qn, qc);
       }
       if (qn != 0)
-        drain_lane<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
+        drain_queue<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
