@@ -1095,7 +1095,11 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
                                              int64_t jbase, unsigned short *wq, unsigned &qn,
                                              unsigned &qc) {
   constexpr bool SIGNED = ANGLE && AM == 2;
+#ifdef GLR_XGENNOFOLD
   constexpr bool FOLD = !ANGLE || SIGNED;
+#else
+  constexpr bool FOLD = true;  // every mode: the hit is M's sign bit
+#endif
   // T1: the unit's threshold is the global bound 1 (every unit of a
   // domain-spanning tile order): a compile-time constant, so the FOLD
   // products take it as an immediate (one register read less per FFMA2)
@@ -1155,14 +1159,25 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         // MOV or {0,1} multiplier per pair).
         double v = AM == 3 ? angle_dev_signed(th[k], thj, ideal)
                            : angle_dev_fast_signed(th[k], thj, kappa);
-        asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
-            "setp.lt.f32 p, %2, %3;\n\t"
-            "@p add.u32 %0, %0, 1;\n\t"
-            "mov.b64 {lo, hi}, %1;\n\t"
-            "selp.b32 hi, hi, 0, p;\n\t"
-            "mov.b64 %1, {lo, hi};\n\t}"
-            : "+r"(cnt[k % kCntAccAngle]), "+d"(v)
-            : "f"(M[k]), "f"(-thr));
+        if (FOLD) {  // hit <=> M's sign bit (an integer test: -0 is a hit)
+          asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
+              "setp.lt.s32 p, %2, 0;\n\t"
+              "@p add.u32 %0, %0, 1;\n\t"
+              "mov.b64 {lo, hi}, %1;\n\t"
+              "selp.b32 hi, hi, 0, p;\n\t"
+              "mov.b64 %1, {lo, hi};\n\t}"
+              : "+r"(cnt[k % kCntAccAngle]), "+d"(v)
+              : "r"(__float_as_int(M[k])));
+        } else {
+          asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
+              "setp.lt.f32 p, %2, %3;\n\t"
+              "@p add.u32 %0, %0, 1;\n\t"
+              "mov.b64 {lo, hi}, %1;\n\t"
+              "selp.b32 hi, hi, 0, p;\n\t"
+              "mov.b64 %1, {lo, hi};\n\t}"
+              : "+r"(cnt[k % kCntAccAngle]), "+d"(v)
+              : "f"(M[k]), "f"(-thr));
+        }
         dev[k % kDevAcc] = __dadd_rn(dev[k % kDevAcc], fabs(v));
       } else {
         // the sign bit of M is the hit (LEA.HI: one instruction)
@@ -1612,7 +1627,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                                                             dev, A2, ideal, kappa, rec, ids, theta,
                                                             ibase, jbase, wq, qn, qc);
       }
-    } else if (!ANGLE && thr == 1.0f) {
+    } else if (thr == 1.0f) {  // general units too: FOLD products with an immediate t
 #pragma unroll kJUnrollC
       for (int jj = 0; jj < kTile; jj += kNJ)
         filter_block<ANGLE, false, kNJ, 0, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
