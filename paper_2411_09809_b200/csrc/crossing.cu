@@ -180,15 +180,18 @@ constexpr int kFK = GLR_XFK;             // i-edges per lane in the filter kerne
 constexpr int kFGroups = kFK / 2;        // packed i-edge pairs per lane
 constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
 // independent hit counters / angle accumulators per lane (ILP vs registers;
-// one counter makes the count-only kernel 3% faster, profiles/r01_variants_filter.txt)
+// one counter makes the count-only kernel 3% faster, profiles/r01_variants_filter.txt;
+// in the fused kernel's general units 1 counter + 2 angle accumulators free
+// the registers ptxas otherwise shuffles with moves: C5 culled 2.96 -> 2.81 s,
+// dense 4.48 -> 4.45 s, profiles/r02_variants_acc.txt)
 #ifndef GLR_XFCNT_A
-#define GLR_XFCNT_A 4
+#define GLR_XFCNT_A 1
 #endif
 #ifndef GLR_XFCNT_C
 #define GLR_XFCNT_C 1
 #endif
 #ifndef GLR_XFDEV
-#define GLR_XFDEV 4
+#define GLR_XFDEV 2
 #endif
 constexpr int kCntAccAngle = GLR_XFCNT_A;
 constexpr int kCntAccCount = GLR_XFCNT_C;
