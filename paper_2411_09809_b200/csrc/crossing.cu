@@ -196,6 +196,11 @@ constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
 constexpr int kCntAccAngle = GLR_XFCNT_A;
 constexpr int kCntAccCount = GLR_XFCNT_C;
 constexpr int kDevAcc = GLR_XFDEV;
+#ifndef GLR_XA2
+#define GLR_XA2 2
+#endif
+constexpr int kA2 = GLR_XA2;  // signed units: alternating sum_j h_j theta_j accumulators (1 or 2)
+static_assert(kA2 == 1 || kA2 == 2, "kA2");
 static_assert(kFK % 2 == 0 && kFK <= 4 && kTile % (32 * kFK) == 0, "filter slice shape");
 
 __host__ __device__ inline int fslot(int slice, int k, int lane) {
@@ -1138,7 +1143,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
       unsigned h = b[0] >> 31;
 #pragma unroll
       for (int k = 1; k < kFK; ++k) h += b[k] >> 31;
-      A2[q & 1] = fma((double)h, thj, A2[q & 1]);
+      A2[q & (kA2 - 1)] = fma((double)h, thj, A2[q & (kA2 - 1)]);
       unsigned mq = b[0];
 #pragma unroll
       for (int k = 1; k < kFK; ++k) mq = min(mq, b[k]);
