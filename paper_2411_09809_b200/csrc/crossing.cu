@@ -824,19 +824,14 @@ __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
 }
 __device__ __forceinline__ uint64_t f2_bcast(float a) { return f2_pack(a, a); }
 __device__ __forceinline__ float f2_lo(uint64_t v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float lo;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(v));
   return lo;
 }
 __device__ __forceinline__ float f2_hi(uint64_t v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float hi;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(v));
   return hi;
-}
-__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
 }
 __device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
   uint64_t r;
@@ -1129,7 +1124,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
   for (int q = 0; q < NJ; ++q) {
     float (&M)[kFK] = MB[q];
     const double thj = ANGLE ? lds_f64(thaddr + (jj0 + q) * 8u) : 0.0;
-    if (SIGNED) {
+    if constexpr (SIGNED) {
       // hits are M's sign bits: C_k += hit (LEA.HI), h = hits on this j-edge,
       // A += h * theta_j (one DFMA per j-edge; unit_shift).  Short dependency
       // chains: pairwise hit sums, two alternating A accumulators, and the
@@ -1148,8 +1143,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
 #pragma unroll
       for (int k = 1; k < kFK; ++k) mq = min(mq, b[k]);
       mmin = q == 0 ? mq : min(mmin, mq);
-      continue;
-    }
+    } else {
 #pragma unroll
     for (int k = 0; k < kFK; ++k) {
       if (FOLD) {
@@ -1192,6 +1186,7 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         cnt[k % kCntAccCount] += __float_as_uint(M[k]) >> 31;
       }
     }
+    }  // not SIGNED
   }
   if (__any_sync(0xffffffffu, FOLD ? mmin <= vbits : any)) {
     // the block's M values (still live) into a per-lane mask of its

@@ -232,28 +232,18 @@ __device__ __forceinline__ uint64_t o2_pack(float lo, float hi) {
   return r;
 }
 __device__ __forceinline__ float o2_lo(uint64_t v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float lo;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(v));
   return lo;
 }
 __device__ __forceinline__ float o2_hi(uint64_t v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float hi;
+  asm("mov.b64 {_, %0}, %1;" : "=f"(hi) : "l"(v));
   return hi;
-}
-__device__ __forceinline__ uint64_t o2_sub(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
 }
 __device__ __forceinline__ uint64_t o2_add(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t o2_mul(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 __device__ __forceinline__ uint64_t o2_fma(uint64_t a, uint64_t b, uint64_t c) {
