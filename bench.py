@@ -373,7 +373,7 @@ def main():
         rec = M.CrossingRecords(dg, "culled")
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
         sharding.allreduce_partials(out[0:2])
-        units = rec.units
+        units = (rec.units, rec.n_mixed, rec.n_full)
         del rec
         return units
 
@@ -498,11 +498,14 @@ def main():
                                          "candidate tile pairs (incl. plan build)"}},
         "crossing_culled": {"metric": "edge-pair crossing tests/s (E_c+E_ca fused), culled plan",
                             "value": P_E / (cross_culled_ms * 1e-3), "unit": "pairs/s",
-                            "ms_per_step": cross_culled_ms, "candidate_units": cross_units,
+                            "ms_per_step": cross_culled_ms, "candidate_units": cross_units[0],
+                            "mixed_units": cross_units[1], "full_units": cross_units[2],
                             "dense_units": M.crossing_units(m),
-                            "note": "effective rate (m(m-1)/2 / time): same count and sum, 4-D "
-                                    "bbox Morton order + candidate tile pairs (incl. plan "
-                                    "build); the public API's strategy='auto' on C5"},
+                            "note": "effective rate (m(m-1)/2 / time): same count and sum, "
+                                    "(orientation, 4-D bbox Morton) order + classified tile "
+                                    "pairs -- certified-empty pairs dropped, certified-full "
+                                    "pairs counted without a predicate (incl. plan build); "
+                                    "the public API's strategy='auto' on C5"},
         "layout": layout,
         "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": peak_run,
                      "unit": "T lane-op/s (FP32 FFMA/FMUL on the FMA pipe)",

@@ -197,6 +197,34 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m,
                             uint64_t list_len, uint64_t unit_begin,
                             uint64_t unit_end, double *d_out, void *stream);
 
+/* Classified candidate tile pairs (the culled plan's list; replaces the
+ * per-pair work of exact.py:170-217 for whole tile pairs).  Every (ti <= tj)
+ * with overlapping tile rank boxes is certified, from per-tile boxes of the
+ * edges' two endpoints and an error bound on the reference's own FP64 cross
+ * products (admissible inputs only, see crossing.cu tile_class_kernel), as
+ *   - none: no pair can pass proper_intersection_mask (dropped),
+ *   - full: every pair passes it and shares no vertex, or
+ *   - mixed: anything else.
+ * d_list receives [mixed units | full units], each part row-major, as int2;
+ * h_counts[0] = mixed units, h_counts[1] = full units.  Synchronous; the list
+ * is written only when d_list != NULL and capacity >= both counts' sum. */
+int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
+                                       void *d_list, uint64_t capacity,
+                                       uint64_t *h_counts, void *stream);
+
+/* Units [unit_begin, unit_end) of a classified list (unit u = d_list[u]; u <
+ * mixed_len: the pair kernels; otherwise a full unit: na * nb crossings and
+ * the reference's per-pair deviation, or its closed form where the unit's
+ * theta ranges fix the formula's branch), under interleaved chunk ownership
+ * for rank of world (0 of 1: the whole range).  Partials over a disjoint
+ * cover of [0, mixed_len + full_len), or over all ranks, sum to the dense
+ * result. */
+int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m,
+                                  int with_angle, double ideal, const void *d_list,
+                                  uint64_t mixed_len, uint64_t full_len,
+                                  uint64_t unit_begin, uint64_t unit_end, int rank,
+                                  int world, double *d_out, void *stream);
+
 /* Candidate vertex tile pairs: (ti <= tj) whose tile boxes are closer than
  * reach = 2r on both axes (fl(gap) < reach); same protocol as
  * glr_crossing_candidates.  Pairs in skipped tile pairs provably fail the

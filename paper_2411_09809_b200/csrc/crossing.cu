@@ -2023,6 +2023,263 @@ tile_weight_kernel(const int *__restrict__ newc, double beta, double *__restrict
   }
 }
 
+// ---- classified candidate list: tile pairs certified to cross everywhere --
+//
+// The reference's predicate for a pair (a, b) x (c, d) needs c1, c2 (c and d
+// against line ab) to straddle zero and c3, c4 (a and b against line cd) to
+// straddle zero (geometry.py:62-79).  Name each edge's endpoints P (smaller
+// x, ties smaller y) and Q; the straddle tests do not depend on which
+// endpoint the reference calls a.  Per tile, PQBox bounds the P's and the
+// Q's of its real edges.  The exact orientation (Q - P) x (r - P) is affine
+// in each of the six coordinates separately, so over P-box x Q-box x r-box it
+// takes its extremes at box corners: evaluating the 16 (P, Q) corner lines
+// against the r-box (monotone in rx and ry) gives the exact range up to the
+// evaluation error.  Both the corner evaluation and the reference's own
+// fl(c) differ from the exact value by at most 2^-49 Ux Uy (four roundings
+// of u = 2^-53 on |dx dy| + |dy dx| <= 2 Ux Uy, Ux / Uy the extents of the
+// union of the four boxes), so a computed corner range beyond kClassMargin
+// Ux Uy = 2^-47 Ux Uy certifies the sign the reference computes for EVERY
+// pair of the unit:
+//   * "none": c and d strictly on one side of every line ab (or a and b of
+//     every line cd) -- no pair straddles, the unit is dropped;
+//   * "full": both straddles strictly certified for every pair -- every pair
+//     properly crosses, so the bboxes overlap and no vertex is shared (a
+//     shared vertex would make an exact orientation 0): the unit contributes
+//     na * nb crossings and the pairs' deviations (cross_full_kernel), with
+//     no per-pair predicate at all.
+// Only admissible inputs (finite, |coords| in [2^-160, 2^500], no overflow
+// or underflow in these products) are classified; otherwise every
+// overlapping unit stays "mixed".
+struct __align__(16) PQBox {
+  double px0, px1, py0, py1;  // P (smaller-x endpoint) box
+  double qx0, qx1, qy0, qy1;  // Q box
+};
+constexpr double kClassMargin = 0x1p-47;
+enum UnitClass { kUnitNone = 0, kUnitMixed = 1, kUnitFull = 2 };
+
+__global__ void __launch_bounds__(kTile) tile_pq_kernel(const EdgeRec *__restrict__ rec,
+                                                        int64_t m, PQBox *__restrict__ out) {
+  __shared__ double red[8][kTile / 32];
+  const int64_t e = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  // v[0..3]: -P.x, P.x, -P.y, P.y maxima; v[4..7] the same for Q
+  double v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = -INFINITY;
+  if (e < m) {
+    const EdgeRec &r = rec[e];
+    const bool pa = r.ax < r.bx || (r.ax == r.bx && r.ay <= r.by);
+    const double px = pa ? r.ax : r.bx, py = pa ? r.ay : r.by;
+    const double qx = pa ? r.bx : r.ax, qy = pa ? r.by : r.ay;
+    v[0] = -px; v[1] = px; v[2] = -py; v[3] = py;
+    v[4] = -qx; v[5] = qx; v[6] = -qy; v[7] = qy;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    for (int o = 16; o > 0; o >>= 1) v[i] = fmax(v[i], __shfl_down_sync(0xffffffffu, v[i], o));
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[i][threadIdx.x >> 5] = v[i];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double x = red[threadIdx.x][0];
+    for (int w = 1; w < kTile / 32; ++w) x = fmax(x, red[threadIdx.x][w]);
+    // even slots hold -min: negate back (an empty tile gets lo = +inf, hi = -inf)
+    reinterpret_cast<double *>(out + blockIdx.x)[threadIdx.x] = (threadIdx.x & 1) ? x : -x;
+  }
+}
+
+// Computed ranges of (Q - P) x (r - P) over the lines of L's edges, for r in
+// R's P-box (lo[0], hi[0]) and Q-box (lo[1], hi[1]).
+__device__ inline void orient_ranges(const PQBox &L, const PQBox &R, double (&lo)[2],
+                                     double (&hi)[2]) {
+  lo[0] = lo[1] = INFINITY;
+  hi[0] = hi[1] = -INFINITY;
+  const double rb[2][4] = {{R.px0, R.px1, R.py0, R.py1}, {R.qx0, R.qx1, R.qy0, R.qy1}};
+#pragma unroll 1
+  for (int c = 0; c < 16; ++c) {
+    const double px = (c & 1) ? L.px1 : L.px0, py = (c & 2) ? L.py1 : L.py0;
+    const double qx = (c & 4) ? L.qx1 : L.qx0, qy = (c & 8) ? L.qy1 : L.qy0;
+    const double a = __dsub_rn(qx, px), b = __dsub_rn(qy, py);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double t1a = __dmul_rn(a, __dsub_rn(rb[k][2], py));
+      const double t1b = __dmul_rn(a, __dsub_rn(rb[k][3], py));
+      const double t2a = __dmul_rn(b, __dsub_rn(rb[k][0], px));
+      const double t2b = __dmul_rn(b, __dsub_rn(rb[k][1], px));
+      lo[k] = fmin(lo[k], __dsub_rn(fmin(t1a, t1b), fmax(t2a, t2b)));
+      hi[k] = fmax(hi[k], __dsub_rn(fmax(t1a, t1b), fmin(t2a, t2b)));
+    }
+  }
+}
+
+__device__ inline int unit_class(const PQBox &A, const PQBox &B) {
+  const double x0 = fmin(fmin(A.px0, A.qx0), fmin(B.px0, B.qx0));
+  const double x1 = fmax(fmax(A.px1, A.qx1), fmax(B.px1, B.qx1));
+  const double y0 = fmin(fmin(A.py0, A.qy0), fmin(B.py0, B.qy0));
+  const double y1 = fmax(fmax(A.py1, A.qy1), fmax(B.py1, B.qy1));
+  // kClassMargin Ux Uy, rounded up by far more than the few ulps of the
+  // extents' own rounding; + 2^-1000 keeps it positive for flat boxes
+  const double thr = __dadd_ru(__dmul_ru(__dmul_ru(__dsub_ru(x1, x0), __dsub_ru(y1, y0)),
+                                         kClassMargin * (1.0 + 0x1p-20)),
+                               0x1p-1000);
+  double la[2], ha[2], lb[2], hb[2];
+  orient_ranges(A, B, la, ha);  // c, d against lines ab
+  orient_ranges(B, A, lb, hb);  // a, b against lines cd
+  const bool pa0 = la[0] > thr, na0 = ha[0] < -thr, pa1 = la[1] > thr, na1 = ha[1] < -thr;
+  const bool pb0 = lb[0] > thr, nb0 = hb[0] < -thr, pb1 = lb[1] > thr, nb1 = hb[1] < -thr;
+  if ((pa0 && pa1) || (na0 && na1) || (pb0 && pb1) || (nb0 && nb1)) return kUnitNone;
+  if (((pa0 && na1) || (na0 && pa1)) && ((pb0 && nb1) || (nb0 && pb1))) return kUnitFull;
+  return kUnitMixed;
+}
+
+// Row ti of the classified list: one CTA per row, tj = ti..T-1 in blocks of
+// kClassThreads, order-preserving compaction (warp ballots).  FILL == false
+// counts mixed / full units per row; FILL == true writes mixed units at
+// off_m[ti] and full units at off_m[T] + off_f[ti] (both parts row-major).
+constexpr int kClassThreads = 256;
+template <bool FILL>
+__global__ void __launch_bounds__(kClassThreads)
+tile_class_kernel(const RecHeader *__restrict__ hdr, const int4 *__restrict__ box,
+                  const PQBox *__restrict__ pq, int64_t T, unsigned long long *__restrict__ cnt_m,
+                  unsigned long long *__restrict__ cnt_f,
+                  const unsigned long long *__restrict__ off_m,
+                  const unsigned long long *__restrict__ off_f, int2 *__restrict__ list) {
+  constexpr int kWarps = kClassThreads / 32;
+  __shared__ unsigned wm[kWarps], wf[kWarps];
+  const int64_t ti = blockIdx.x;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool classify = hdr->admissible != 0;
+  const int4 a = box[ti];
+  const PQBox pa = pq[ti];
+  unsigned long long om = FILL ? off_m[ti] : 0ull, of = FILL ? off_m[T] + off_f[ti] : 0ull;
+  unsigned long long nm = 0, nf = 0;
+  for (int64_t base = ti; base < T; base += kClassThreads) {
+    const int64_t tj = base + threadIdx.x;
+    int c = kUnitNone;
+    if (tj < T && boxes_overlap(a, box[tj]))
+      c = (classify && tj != ti) ? unit_class(pa, pq[tj]) : kUnitMixed;
+    const unsigned bm = __ballot_sync(0xffffffffu, c == kUnitMixed);
+    const unsigned bf = __ballot_sync(0xffffffffu, c == kUnitFull);
+    if (lane == 0) {
+      wm[warp] = __popc(bm);
+      wf[warp] = __popc(bf);
+    }
+    __syncthreads();
+    unsigned pm = 0, pf = 0, tm = 0, tf = 0;
+#pragma unroll
+    for (unsigned w = 0; w < (unsigned)kWarps; ++w) {
+      if (w < warp) { pm += wm[w]; pf += wf[w]; }
+      tm += wm[w];
+      tf += wf[w];
+    }
+    if (FILL) {
+      const unsigned below = (1u << lane) - 1u;
+      if (c == kUnitMixed) list[om + pm + __popc(bm & below)] = make_int2((int)ti, (int)tj);
+      if (c == kUnitFull) list[of + pf + __popc(bf & below)] = make_int2((int)ti, (int)tj);
+    }
+    om += tm; of += tf; nm += tm; nf += tf;
+    __syncthreads();
+  }
+  if (!FILL && threadIdx.x == 0) {
+    cnt_m[ti] = nm;
+    cnt_f[ti] = nf;
+  }
+}
+
+// per tile: sum of theta over its real edges (fixed reduction tree)
+__global__ void __launch_bounds__(kTile) tile_theta_sum_kernel(const double *__restrict__ theta,
+                                                               int64_t m, double *__restrict__ ts) {
+  __shared__ double sh[kTile / 32];
+  const int64_t e = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  const double s = block_sum<kTile>(e < m ? theta[e] : 0.0, sh);
+  if (threadIdx.x == 0) ts[blockIdx.x] = s;
+}
+
+// Full units (every pair crosses, tile_class_kernel): na * nb crossings and
+// the deviation sum.  Units whose theta ranges give unit_shift's signed form
+// take it in closed form from the tiles' theta sums,
+//   sum_ij |theta_j - theta_i - s| = sigma (na sum_j theta_j - nb sum_i
+//   theta_i - na nb s),
+// (each term at least kSignMargin, so the cancellation costs < 1e-12
+// relative); the others evaluate the reference's per-pair formula
+// (angle_dev) for all na * nb pairs -- FP64 only, no predicate.  Same chunk
+// ownership as the pair kernels; the slice sums go to exact accumulators.
+constexpr int kFullThreads = kTile;  // thread t: i-edge t of the unit
+template <bool ANGLE>
+__global__ void __launch_bounds__(kFullThreads)
+cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ theta,
+                  const double *__restrict__ tsum, const int2 *__restrict__ flist, uint64_t fbeg,
+                  uint64_t fend, uint64_t chunk, unsigned srank, unsigned sworld, int64_t m,
+                  double ideal, unsigned long long *__restrict__ cta_cnt,
+                  unsigned long long *__restrict__ cta_acc) {
+  constexpr int kWarps = kFullThreads / 32;
+  __shared__ double sth[kTile];
+  __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
+  const unsigned lane = threadIdx.x & 31;
+  const int warp = (int)(threadIdx.x >> 5);
+  CtaUnits cu;
+  cu.ulist = flist; cu.T = 0; cu.W = 0; cu.ubeg = fbeg; cu.uend = fend; cu.chunk = chunk;
+  cu.nchunks = (fend - fbeg + chunk - 1) / chunk;
+  cu.step = (uint64_t)sworld * gridDim.x;
+  cu.ch0 = srank + (uint64_t)sworld * blockIdx.x;
+  if (ANGLE)
+    for (int i = threadIdx.x; i < kWarps * kAccWords; i += kFullThreads) (&wacc[0][0])[i] = 0;
+  __syncthreads();
+  const bool shift_ok = ANGLE && ideal >= 0x1p-100;
+  unsigned long long total = 0;
+  for (uint64_t uq = 0;; ++uq) {
+    uint64_t ti, tj;
+    if (!cu.at(uq, &ti, &tj)) break;
+    const int64_t ra = m - (int64_t)ti * kTile, rb = m - (int64_t)tj * kTile;
+    const int na = (int)(ra < kTile ? ra : kTile), nb = (int)(rb < kTile ? rb : kTile);
+    if (threadIdx.x == 0) total += (unsigned long long)na * (unsigned long long)nb;
+    if (!ANGLE) continue;
+    const TileBox bi = tbox[ti], bj = tbox[tj];
+    double sh = 0.0, sigma = 1.0;
+    if (shift_ok && unit_shift(bi, bj, ideal, &sh, &sigma) == 1) {
+      if (threadIdx.x == 0) {
+        const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)na, tsum[tj]),
+                                                     __dmul_rn((double)nb, tsum[ti])),
+                                           __dmul_rn((double)na * (double)nb, sh));
+        xacc_add(wacc[0], v > 0.0 ? v : 0.0);
+      }
+      continue;
+    }
+    __syncthreads();  // the previous unit's theta_j are consumed
+    sth[threadIdx.x] = theta[(int64_t)tj * kTile + threadIdx.x];
+    __syncthreads();
+    double d = 0.0;
+    if ((int)threadIdx.x < na) {
+      const double t = theta[(int64_t)ti * kTile + threadIdx.x];
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      int j = 0;
+      for (; j + 4 <= nb; j += 4) {
+        d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
+        d1 = __dadd_rn(d1, angle_dev(t, sth[j + 1], ideal));
+        d2 = __dadd_rn(d2, angle_dev(t, sth[j + 2], ideal));
+        d3 = __dadd_rn(d3, angle_dev(t, sth[j + 3], ideal));
+      }
+      for (; j < nb; ++j) d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
+      d = __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3));
+    }
+    for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
+    if (lane == 0) xacc_add(wacc[warp], d);
+  }
+  __shared__ unsigned long long acc_cnt;
+  if (threadIdx.x == 0) acc_cnt = total;
+  if (ANGLE && lane == 0) xacc_normalize(wacc[warp]);
+  __syncthreads();
+  if (threadIdx.x == 0) cta_cnt[blockIdx.x] += acc_cnt;
+  if (ANGLE) {
+    for (int i = threadIdx.x; i < kAccWords; i += kFullThreads) {
+      unsigned long long v = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
+      cta_acc[(size_t)blockIdx.x * kAccWords + i] += v;
+    }
+  }
+}
+
 int grid_for(uint64_t units, int per_sm = kMinBlocks) {
   uint64_t g = (uint64_t)sm_count() * per_sm;
   if (units < g) g = units;
@@ -2165,7 +2422,8 @@ uint64_t chunk_for(uint64_t span, int sworld) {
 
 int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                    const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
-                   int srank, int sworld, double *d_out, cudaStream_t st) {
+                   int srank, int sworld, double *d_out, cudaStream_t st,
+                   const int2 *d_full = nullptr, uint64_t fbeg = 0, uint64_t fend = 0) {
   if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0 || sworld < 1 || srank < 0 ||
       srank >= sworld) {
     set_error("glr_crossing_pairs: invalid arguments");
@@ -2188,12 +2446,20 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     set_error("glr_crossing_pairs: ideal angle must lie in (0, pi/2], got %g", ideal);
     return GLR_EARG;
   }
-  if (m < 2 || ubeg == uend) {
+  if (fbeg > fend || (fend > fbeg && d_full == nullptr)) {
+    set_error("glr_crossing_pairs: invalid full-unit range");
+    return GLR_EARG;
+  }
+  if (m < 2 || (ubeg == uend && fbeg == fend)) {
     GLR_CUDA(cudaMemsetAsync(d_out, 0, 2 * sizeof(double), st));
     return GLR_OK;
   }
   RecView rv = view(const_cast<void *>(d_records), n, m);
   const uint64_t span = uend - ubeg;
+  const uint64_t fspan = fend - fbeg;
+  // full units (cross_full_kernel): their own CTA slots after the pair kernels'
+  const int ggrid = fspan > 0 ? grid_for((fspan + sworld - 1) / sworld, 8) : 0;
+  const uint64_t fchunk = chunk_for(fspan, sworld);
   const int grid = grid_for((span + sworld - 1) / sworld);
   const int fgrid = grid_for((span + sworld - 1) / sworld,
                              with_angle ? kFilterMinBlocksAngle : kFilterMinBlocksCount);
@@ -2210,74 +2476,98 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   if (seg_len < seg_align) seg_len = seg_align;
   const uint64_t seg_max = span < seg_len ? span : seg_len;
   const size_t a_fix = with_angle ? al256((size_t)((seg_max * kFSlices + 31) / 32) * 4) : 0;
-  const size_t a_acc = (size_t)(cgrid + xgrid) * kAccWords * sizeof(unsigned long long);
-  Scratch scr((size_t)(cgrid + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc +
-                  a_fix + 256,
+  const int ncta = cgrid + ggrid;            // count / FP64 slots: pair kernels, full kernel
+  const int nacc = cgrid + xgrid + ggrid;    // exact accumulators: filter, fixup, full
+  const size_t a_acc = (size_t)nacc * kAccWords * sizeof(unsigned long long);
+  const size_t a_ts = (with_angle && fspan > 0) ? al256((size_t)(m_pad / kTile) * sizeof(double)) : 0;
+  Scratch scr((size_t)(ncta + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc +
+                  a_fix + a_ts + 512,
               st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
-  unsigned long long *ac = cc + cgrid;
+  unsigned long long *ac = cc + ncta;
   double *cd = reinterpret_cast<double *>(ac + agrid);
-  double *ad = cd + cgrid;
+  double *ad = cd + ncta;
   unsigned long long *xa = reinterpret_cast<unsigned long long *>(ad + agrid);
   unsigned *fix = reinterpret_cast<unsigned *>(
-      (reinterpret_cast<uintptr_t>(xa + (size_t)(cgrid + xgrid) * kAccWords) + 255) & ~(uintptr_t)255);
+      (reinterpret_cast<uintptr_t>(xa + (size_t)nacc * kAccWords) + 255) & ~(uintptr_t)255);
+  double *tsum = reinterpret_cast<double *>(
+      (reinterpret_cast<uintptr_t>(fix) + a_fix + 255) & ~(uintptr_t)255);
   // only the kernel of the records' mode writes its CTA slots
-  GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)cgrid * sizeof(unsigned long long), st));
-  GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)cgrid * sizeof(double), st));
+  GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)ncta * sizeof(unsigned long long), st));
+  GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)ncta * sizeof(double), st));
   GLR_CUDA(cudaMemsetAsync(xa, 0, a_acc, st));
-  const uint64_t W = (uint64_t)kBandTiles;
-  const unsigned r = (unsigned)srank, g = (unsigned)sworld;
-  // the filter's shift/signed forms and cleared-miss leftovers assume an
-  // ideal angle >= 2^-100; below it the FP64 sign kernel (mode 1) runs
-  const int filter_ok = (!with_angle || ideal >= 0x1p-100) ? 1 : 0;
-  const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
-  if (with_angle) {
-    cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
-        filter_ok, cc, cd);
-    GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
-    cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
-        filter_ok, cc, cd);
-    GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
-    for (uint64_t sb = ubeg; sb < uend; sb += seg_len) {
-      const uint64_t se = uend - sb < seg_len ? uend : sb + seg_len;
-      const uint64_t nbits = (se - sb) * kFSlices;
-      GLR_CUDA(cudaMemsetAsync(fix, 0, (size_t)((nbits + 31) / 32) * 4, st));
-      cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
-          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, se,
-          chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
-      GLR_LAUNCHED("cross_filter_kernel<angle>");
-      cross_fixup_kernel<<<xgrid, kFixThreads, 0, st>>>(
-          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, nbits,
-          ideal, kappa, filter_ok, fix, xa + (size_t)cgrid * kAccWords);
-      GLR_LAUNCHED("cross_fixup_kernel");
+  if (fspan > 0) {
+    if (with_angle) {
+      tile_theta_sum_kernel<<<(unsigned)(m_pad / kTile), kTile, 0, st>>>(rv.theta, m, tsum);
+      GLR_LAUNCHED("tile_theta_sum_kernel");
+      cross_full_kernel<true><<<ggrid, kFullThreads, 0, st>>>(
+          rv.tbox, rv.theta, tsum, d_full, fbeg, fend, fchunk, (unsigned)srank, (unsigned)sworld,
+          m, ideal, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
+      GLR_LAUNCHED("cross_full_kernel<angle>");
+    } else {
+      cross_full_kernel<false><<<ggrid, kFullThreads, 0, st>>>(
+          rv.tbox, rv.theta, nullptr, d_full, fbeg, fend, fchunk, (unsigned)srank,
+          (unsigned)sworld, m, 0.0, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
+      GLR_LAUNCHED("cross_full_kernel");
     }
-    adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
-                                                 d_list, U, T, W, ubeg, uend, chunk, r, g, ideal,
-                                                 filter_ok, ac, ad);
-    GLR_LAUNCHED("adj_kernel<angle>");
-  } else {
-    cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        filter_ok, cc, cd);
-    GLR_LAUNCHED("cross_pairs_kernel<fast>");
-    cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
-        filter_ok, cc, cd);
-    GLR_LAUNCHED("cross_pairs_kernel<general>");
-    cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
-        rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
-        chunk, r, g, 0.0, 0.0, filter_ok, cc, xa, nullptr);
-    GLR_LAUNCHED("cross_filter_kernel");
-    adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
-                                                  d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
-                                                  filter_ok, ac, ad);
-    GLR_LAUNCHED("adj_kernel");
   }
-  cross_finalize_kernel<<<1, 1024, 0, st>>>(cc, cd, xa, cgrid, cgrid + xgrid, ac, ad, agrid,
-                                            d_out);
+  if (span > 0) {
+    const uint64_t W = (uint64_t)kBandTiles;
+    const unsigned r = (unsigned)srank, g = (unsigned)sworld;
+    // the filter's shift/signed forms and cleared-miss leftovers assume an
+    // ideal angle >= 2^-100; below it the FP64 sign kernel (mode 1) runs
+    const int filter_ok = (!with_angle || ideal >= 0x1p-100) ? 1 : 0;
+    const double kappa = 1.5707963267948966 - ideal;  // host IEEE double
+    if (with_angle) {
+      cross_pairs_kernel<true, true><<<grid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
+          filter_ok, cc, cd);
+      GLR_LAUNCHED("cross_pairs_kernel<fast,angle>");
+      cross_pairs_kernel<false, true><<<grid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, ideal,
+          filter_ok, cc, cd);
+      GLR_LAUNCHED("cross_pairs_kernel<general,angle>");
+      for (uint64_t sb = ubeg; sb < uend; sb += seg_len) {
+        const uint64_t se = uend - sb < seg_len ? uend : sb + seg_len;
+        const uint64_t nbits = (se - sb) * kFSlices;
+        GLR_CUDA(cudaMemsetAsync(fix, 0, (size_t)((nbits + 31) / 32) * 4, st));
+        cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
+            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, se,
+            chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
+        GLR_LAUNCHED("cross_filter_kernel<angle>");
+        cross_fixup_kernel<<<xgrid, kFixThreads, 0, st>>>(
+            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, nbits,
+            ideal, kappa, filter_ok, fix, xa + (size_t)cgrid * kAccWords);
+        GLR_LAUNCHED("cross_fixup_kernel");
+      }
+      adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
+                                                   d_list, U, T, W, ubeg, uend, chunk, r, g, ideal,
+                                                   filter_ok, ac, ad);
+      GLR_LAUNCHED("adj_kernel<angle>");
+    } else {
+      cross_pairs_kernel<true, false><<<grid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+          filter_ok, cc, cd);
+      GLR_LAUNCHED("cross_pairs_kernel<fast>");
+      cross_pairs_kernel<false, false><<<grid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.theta, rv.ids, rv.newc, d_list, T, W, ubeg, uend, chunk, r, g, 0.0,
+          filter_ok, cc, cd);
+      GLR_LAUNCHED("cross_pairs_kernel<general>");
+      cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
+          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
+          chunk, r, g, 0.0, 0.0, filter_ok, cc, xa, nullptr);
+      GLR_LAUNCHED("cross_filter_kernel");
+      adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
+                                                    d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
+                                                    filter_ok, ac, ad);
+      GLR_LAUNCHED("adj_kernel");
+    }
+  } else {
+    GLR_CUDA(cudaMemsetAsync(ac, 0, (size_t)agrid * sizeof(unsigned long long), st));
+    GLR_CUDA(cudaMemsetAsync(ad, 0, (size_t)agrid * sizeof(double), st));
+  }
+  cross_finalize_kernel<<<1, 1024, 0, st>>>(cc, cd, xa, ncta, nacc, ac, ad, agrid, d_out);
   GLR_LAUNCHED("cross_finalize_kernel");
   return GLR_OK;
 }
@@ -2319,6 +2609,66 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
   if (d_list != nullptr && capacity >= total && total > 0) {
     tile_pairs_kernel<true><<<rb, 128, 0, st>>>(box, T, nullptr, offs, d_list);
     GLR_LAUNCHED("tile_pairs_kernel<fill>");
+  }
+  return GLR_OK;
+}
+
+// Classified candidate list (tile_class_kernel): [mixed units | full units],
+// each part row-major; none-certified units are dropped.
+int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, int2 *d_list,
+                                   uint64_t capacity, uint64_t *h_counts, cudaStream_t st) {
+  if (d_records == nullptr || h_counts == nullptr || m < 0 || n < 0) {
+    set_error("glr_crossing_candidates_classified: invalid arguments");
+    return GLR_EARG;
+  }
+  const int64_t m_pad = pad_edges(m < 1 ? 1 : m);
+  const int64_t T = m_pad / kTile;
+  RecView rv = view(const_cast<void *>(d_records), n, m);
+  size_t t_scan = 0;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (unsigned long long *)nullptr,
+                                         (unsigned long long *)nullptr, (int)(T + 1), st));
+  const size_t a_box = al256((size_t)T * sizeof(int4));
+  const size_t a_pq = al256((size_t)T * sizeof(PQBox));
+  const size_t a_cnt = al256((size_t)(T + 1) * sizeof(unsigned long long));
+  Scratch scr(a_box + a_pq + 4 * a_cnt + t_scan, st);
+  GLR_CUDA(scr.err);
+  char *p = scr.as<char>();
+  int4 *box = reinterpret_cast<int4 *>(p);
+  PQBox *pq = reinterpret_cast<PQBox *>(p + a_box);
+  p += a_box + a_pq;
+  unsigned long long *cnt_m = reinterpret_cast<unsigned long long *>(p);
+  unsigned long long *cnt_f = reinterpret_cast<unsigned long long *>(p + a_cnt);
+  unsigned long long *off_m = reinterpret_cast<unsigned long long *>(p + 2 * a_cnt);
+  unsigned long long *off_f = reinterpret_cast<unsigned long long *>(p + 3 * a_cnt);
+  void *tmp = p + 4 * a_cnt;
+  tile_box_kernel<<<(unsigned)T, kTile, 0, st>>>(rv.rec, box);
+  GLR_LAUNCHED("tile_box_kernel");
+  tile_pq_kernel<<<(unsigned)T, kTile, 0, st>>>(rv.rec, m, pq);
+  GLR_LAUNCHED("tile_pq_kernel");
+  GLR_CUDA(cudaMemsetAsync(cnt_m + T, 0, sizeof(unsigned long long), st));
+  GLR_CUDA(cudaMemsetAsync(cnt_f + T, 0, sizeof(unsigned long long), st));
+  tile_class_kernel<false><<<(unsigned)T, kClassThreads, 0, st>>>(rv.hdr, box, pq, T, cnt_m,
+                                                                   cnt_f, nullptr, nullptr,
+                                                                   nullptr);
+  GLR_LAUNCHED("tile_class_kernel<count>");
+  size_t tb = t_scan;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt_m, off_m, (int)(T + 1), st));
+  count_launch(2);
+  tb = t_scan;
+  GLR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt_f, off_f, (int)(T + 1), st));
+  count_launch(2);
+  unsigned long long tot[2] = {0, 0};
+  GLR_CUDA(cudaMemcpyAsync(&tot[0], off_m + T, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           st));
+  GLR_CUDA(cudaMemcpyAsync(&tot[1], off_f + T, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           st));
+  GLR_CUDA(cudaStreamSynchronize(st));
+  h_counts[0] = tot[0];
+  h_counts[1] = tot[1];
+  if (d_list != nullptr && capacity >= tot[0] + tot[1] && tot[0] + tot[1] > 0) {
+    tile_class_kernel<true><<<(unsigned)T, kClassThreads, 0, st>>>(rv.hdr, box, pq, T, nullptr,
+                                                                    nullptr, off_m, off_f, d_list);
+    GLR_LAUNCHED("tile_class_kernel<fill>");
   }
   return GLR_OK;
 }
@@ -2394,6 +2744,34 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m, int wit
   return glr::crossing_pairs(d_records, n, m, with_angle, ideal,
                              reinterpret_cast<const int2 *>(d_list), list_len, unit_begin,
                              unit_end, 0, 1, d_out, glr::as_stream(stream));
+}
+
+int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
+                                       void *d_list, uint64_t capacity, uint64_t *h_counts,
+                                       void *stream) {
+  return glr::crossing_candidates_classified(d_records, n, m, reinterpret_cast<int2 *>(d_list),
+                                             capacity, h_counts, glr::as_stream(stream));
+}
+
+int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m, int with_angle,
+                                  double ideal, const void *d_list, uint64_t mixed_len,
+                                  uint64_t full_len, uint64_t unit_begin, uint64_t unit_end,
+                                  int rank, int world, double *d_out, void *stream) {
+  const uint64_t U = mixed_len + full_len;
+  if ((d_list == nullptr && U > 0) || unit_begin > unit_end || unit_end > U || U < mixed_len) {
+    glr::set_error("glr_crossing_pairs_classified: unit range [%llu, %llu) outside [0, %llu)",
+                   (unsigned long long)unit_begin, (unsigned long long)unit_end,
+                   (unsigned long long)U);
+    return GLR_EARG;
+  }
+  const int2 *lst = reinterpret_cast<const int2 *>(d_list);
+  const uint64_t mb = unit_begin < mixed_len ? unit_begin : mixed_len;
+  const uint64_t me = unit_end < mixed_len ? unit_end : mixed_len;
+  const uint64_t fb = (unit_begin > mixed_len ? unit_begin : mixed_len) - mixed_len;
+  const uint64_t fe = (unit_end > mixed_len ? unit_end : mixed_len) - mixed_len;
+  return glr::crossing_pairs(d_records, n, m, with_angle, ideal, mixed_len ? lst : nullptr,
+                             mixed_len, mb, me, rank, world, d_out, glr::as_stream(stream),
+                             full_len ? lst + mixed_len : nullptr, fb, fe);
 }
 
 uint64_t glr_crossing_units(int64_t m) {

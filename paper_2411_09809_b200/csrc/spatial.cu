@@ -128,13 +128,41 @@ __device__ inline unsigned quant8(double v, double lo, double scale) {
   if (q > 255.0) q = 255.0;
   return (unsigned)q;
 }
-__global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
-                                     const longlong2 *__restrict__ e, int64_t m,
-                                     const unsigned long long *b, const int *__restrict__ deg,
-                                     int64_t hub_degree, unsigned long long *keys, int *idx) {
+// Sum over edges of the quantised bbox half-perimeter (|dx| + |dy| on the
+// 8-bit grid of the Morton code): integer atomics, so the order decision
+// below is deterministic.
+__global__ void edge_extent_kernel(const double2 *__restrict__ xy,
+                                   const longlong2 *__restrict__ e, int64_t m,
+                                   const unsigned long long *b, unsigned long long *lsum) {
   const double x0 = dunkey(b[0]), x1 = dunkey(b[1]), y0 = dunkey(b[2]), y1 = dunkey(b[3]);
   const double sx = (x1 > x0 && isfinite(x1 - x0)) ? 255.0 / (x1 - x0) : 0.0;
   const double sy = (y1 > y0 && isfinite(y1 - y0)) ? 255.0 / (y1 - y0) : 0.0;
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 uv = e[i];
+    const double2 p = xy[uv.x], q = xy[uv.y];
+    s += (unsigned long long)(quant8(fmax(p.x, q.x), x0, sx) - quant8(fmin(p.x, q.x), x0, sx)) +
+         (unsigned long long)(quant8(fmax(p.y, q.y), y0, sy) - quant8(fmin(p.y, q.y), y0, sy));
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(lsum, s);
+}
+
+// mean quantised half-perimeter (of 510) from which edges count as long
+#ifndef GLR_LONG_EDGE_EXTENT
+#define GLR_LONG_EDGE_EXTENT 16
+#endif
+
+__global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
+                                     const longlong2 *__restrict__ e, int64_t m,
+                                     const unsigned long long *b, const int *__restrict__ deg,
+                                     int64_t hub_degree, const unsigned long long *lsum,
+                                     unsigned long long *keys, int *idx) {
+  const double x0 = dunkey(b[0]), x1 = dunkey(b[1]), y0 = dunkey(b[2]), y1 = dunkey(b[3]);
+  const double sx = (x1 > x0 && isfinite(x1 - x0)) ? 255.0 / (x1 - x0) : 0.0;
+  const double sy = (y1 > y0 && isfinite(y1 - y0)) ? 255.0 / (y1 - y0) : 0.0;
+  const bool long_edges = *lsum >= (unsigned long long)GLR_LONG_EDGE_EXTENT * (unsigned long long)m;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
     const longlong2 uv = e[i];
@@ -149,10 +177,18 @@ __global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
     const long long hub = (du >= dv) ? uv.x : uv.y;
     const unsigned long long grp =
         ((du > dv ? du : dv) >= hub_degree) ? (unsigned long long)hub + 1ull : 0ull;
-    // orientation below the Morton code: on short-edge graphs a top-level
-    // split would give every region tiles of both orientations (C3 culled
-    // units 22,229 vs 11,688; C5 76.0M vs 73.3M, tools/cull_probe.py)
-    keys[i] = (grp << 33) | (mk << 1) | up;
+    // Long edges (mean bbox half-perimeter >= 1/32 of the grid's): the
+    // orientation goes ABOVE the Morton code, so a tile holds one diagonal
+    // orientation, its P (smaller-x) and Q endpoints form two compact boxes
+    // and its theta range is narrow -- what tile_class_kernel needs to
+    // certify whole units as crossing everywhere or nowhere, and what lets
+    // the angle pass use the signed form (unit_shift).  It costs a little
+    // bbox culling (C5: 55.7% vs 54.2% of the tile pairs remain), which the
+    // certified classes repay (C5: ~15% of the remaining units certified
+    // empty, ~10% full).  Short edges keep it below the Morton code: there a
+    // top-level split gives every region tiles of both orientations (C3
+    // culled units 22,229 vs 11,688).
+    keys[i] = long_edges ? ((grp << 33) | (up << 32) | mk) : ((grp << 33) | (mk << 1) | up);
     idx[i] = (int)i;
   }
 }
@@ -279,8 +315,12 @@ int keyed_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
     GLR_CUDA(cudaMemsetAsync(b + 3, 0x00, 8, st));
     bounds_kernel<<<grid_of(n), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), n, b);
     GLR_LAUNCHED("bounds_kernel");
+    GLR_CUDA(cudaMemsetAsync(b + 4, 0x00, 8, st));
+    edge_extent_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2, m,
+                                                   b, b + 4);
+    GLR_LAUNCHED("edge_extent_kernel");
     edge_box_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2,
-                                                     m, b, deg, hub_degree, keys, idx);
+                                                     m, b, deg, hub_degree, b + 4, keys, idx);
     GLR_LAUNCHED("edge_box_keys_kernel");
   } else {
     edge_theta_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy),

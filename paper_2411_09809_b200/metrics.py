@@ -50,6 +50,9 @@ CULL_FRACTION = 0.25      # auto (occlusion): cull when candidates <= this share
 # dense pass has the one-DADD angle in most units, the culled list does not,
 # but needs no band order); C5 keeps 54% of the tile pairs: 2.9 s vs 5.1 s
 CROSS_CULL_FRACTION = 0.75
+#: cost of a certified full unit (no predicate; closed form or FP64 deviations
+#: only) relative to a mixed one, for the auto decision and balanced shards
+FULL_UNIT_WEIGHT = 0.25
 AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
 # theta order: vertices of at least this degree get their own edge group
 # (glr_theta_sort_edges; 0 = the library default).  Tuning knob only.
@@ -119,6 +122,21 @@ def _check_strategy(strategy: str) -> str:
     if strategy not in STRATEGIES:
         raise ParameterError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
     return strategy
+
+
+def _classified_candidates(buf: torch.Tensor, n: int, m: int) -> tuple[torch.Tensor, int, int]:
+    """glr_crossing_candidates_classified: ([mixed | full] list, mixed, full)."""
+    L = _lib.lib()
+    counts = (ctypes.c_uint64 * 2)()
+    _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, None, 0, counts, _stream()),
+               "glr_crossing_candidates_classified")
+    mixed, full = int(counts[0]), int(counts[1])
+    lst = torch.empty((max(mixed + full, 1), 2), dtype=torch.int32, device=buf.device)
+    if mixed + full:
+        _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, _ptr(lst), mixed + full,
+                                                        counts, _stream()),
+                   "glr_crossing_candidates_classified")
+    return lst[:mixed + full], mixed, full
 
 
 def _candidates(fn, *args) -> torch.Tensor:
@@ -234,6 +252,7 @@ class CrossingRecords:
         self.m = dg.num_edges
         self.n = dg.num_vertices
         self.list = None
+        self.n_mixed = self.n_full = 0
         if strategy != "dense" and self.m >= 2 and (strategy == "culled"
                                                     or self.m >= AUTO_MIN_EDGES):
             L = _lib.lib()
@@ -242,9 +261,10 @@ class CrossingRecords:
                                                 _ptr(es), _stream()),
                        "glr_spatial_sort_edges")
             self._prepare(dg.xy, es)
-            lst = _candidates(L.glr_crossing_candidates, _ptr(self.buf), self.n, self.m)
-            if strategy == "culled" or len(lst) <= CROSS_CULL_FRACTION * crossing_units(self.m):
-                self.list = lst
+            lst, mixed, full = _classified_candidates(self.buf, self.n, self.m)
+            cost = mixed + FULL_UNIT_WEIGHT * full
+            if strategy == "culled" or cost <= CROSS_CULL_FRACTION * crossing_units(self.m):
+                self.list, self.n_mixed, self.n_full = lst, mixed, full
                 return
             if order == "input":
                 # auto chose the dense pass: results never depend on the edge
@@ -304,13 +324,19 @@ class CrossingRecords:
         ranks' partials sum exactly to the full (count, dev_sum)."""
         if out is None:
             out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
-        if self.culled and len(self.list) == 0:
-            return out.zero_()
+        if self.culled:
+            if len(self.list) == 0:
+                return out.zero_()
+            rc = _lib.lib().glr_crossing_pairs_classified(
+                _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
+                0.0 if ideal is None else float(ideal), _ptr(self.list), self.n_mixed,
+                self.n_full, 0, len(self.list), int(rank), int(world), _ptr(out), _stream())
+            _lib.check(rc, "glr_crossing_pairs_classified")
+            return out
         rc = _lib.lib().glr_crossing_pairs_interleaved(
             _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
-            0.0 if ideal is None else float(ideal),
-            _ptr(self.list) if self.culled else None, len(self.list) if self.culled else 0,
-            int(rank), int(world), _ptr(out), _stream())
+            0.0 if ideal is None else float(ideal), None, 0, int(rank), int(world), _ptr(out),
+            _stream())
         _lib.check(rc, "glr_crossing_pairs_interleaved")
         return out
 
@@ -338,6 +364,7 @@ class CrossingRecords:
             return sharding.triangle_range(w, rank, world, _lib.lib().glr_crossing_band())
         lst = self.list.cpu().numpy()
         unit_w = w[lst[:, 1]] * np.where(lst[:, 0] == lst[:, 1], 0.5, 1.0)
+        unit_w[self.n_mixed:] *= FULL_UNIT_WEIGHT
         return sharding.weighted_range(unit_w, rank, world)
 
     def partial(self, ideal: float | None, unit_begin: int, unit_end: int,
@@ -349,11 +376,11 @@ class CrossingRecords:
         angle = 0 if ideal is None else 1
         ideal_v = 0.0 if ideal is None else float(ideal)
         if self.culled:
-            rc = L.glr_crossing_pairs_list(_ptr(self.buf), self.n, self.m, angle, ideal_v,
-                                           _ptr(self.list) if len(self.list) else None,
-                                           len(self.list), int(unit_begin), int(unit_end),
-                                           _ptr(out), _stream())
-            _lib.check(rc, "glr_crossing_pairs_list")
+            rc = L.glr_crossing_pairs_classified(_ptr(self.buf), self.n, self.m, angle, ideal_v,
+                                                 _ptr(self.list) if len(self.list) else None,
+                                                 self.n_mixed, self.n_full, int(unit_begin),
+                                                 int(unit_end), 0, 1, _ptr(out), _stream())
+            _lib.check(rc, "glr_crossing_pairs_classified")
         else:
             rc = L.glr_crossing_pairs(_ptr(self.buf), self.n, self.m, angle, ideal_v,
                                       int(unit_begin), int(unit_end), _ptr(out), _stream())
