@@ -207,9 +207,12 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m,
  *   - mixed: anything else.
  * d_list receives [mixed units | full units], each part row-major, as int2;
  * h_counts[0] = mixed units, h_counts[1] = full units.  Synchronous; the list
- * is written only when d_list != NULL and capacity >= both counts' sum. */
+ * is written only when d_list != NULL and capacity >= both counts' sum.
+ * d_sub (optional, uint16 per list entry): for each mixed unit, bit
+ * s * 4 + q set when warp-slice s (128 i-edges) x j-quarter q (64 j-edges)
+ * is certified empty; the pair pass then skips it. */
 int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
-                                       void *d_list, uint64_t capacity,
+                                       void *d_list, void *d_sub, uint64_t capacity,
                                        uint64_t *h_counts, void *stream);
 
 /* Units [unit_begin, unit_end) of a classified list (unit u = d_list[u]; u <
@@ -221,7 +224,7 @@ int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t
  * result. */
 int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m,
                                   int with_angle, double ideal, const void *d_list,
-                                  uint64_t mixed_len, uint64_t full_len,
+                                  const void *d_sub, uint64_t mixed_len, uint64_t full_len,
                                   uint64_t unit_begin, uint64_t unit_end, int rank,
                                   int world, double *d_out, void *stream);
 

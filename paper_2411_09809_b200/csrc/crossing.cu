@@ -179,6 +179,14 @@ enum FField { kFAx, kFAy, kFBx, kFBy, kFSabx, kFNsaby, kFNska, kFFields };
 constexpr int kFK = GLR_XFK;             // i-edges per lane in the filter kernel
 constexpr int kFGroups = kFK / 2;        // packed i-edge pairs per lane
 constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
+// Sub-unit masks of the classified candidate list (tile_class_kernel): per
+// mixed unit, bit s * kSubQuarters + q marks warp-slice s x j-quarter q
+// (kSubJ consecutive j-edges) certified empty; the filter kernel skips it.
+constexpr int kSubQuarters = 4;
+constexpr int kSubJ = kTile / kSubQuarters;
+constexpr unsigned kSubQuarterMask = (1u << kSubQuarters) - 1u;
+static_assert(kFSlices * kSubQuarters <= 16, "sub-masks are 16 bits");
+static_assert((32 * kFK) % kSubJ == 0, "a warp slice is a whole number of sub-blocks");
 // independent hit counters / angle accumulators per lane (ILP vs registers;
 // one counter makes the count-only kernel 3% faster, profiles/r01_variants_filter.txt;
 // in the fused kernel's general units 1 counter + 2 angle accumulators free
@@ -1496,7 +1504,8 @@ __global__ void __launch_bounds__(kThreads,
 cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                     const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
                     const TileBox *__restrict__ tbox, const double *__restrict__ theta,
-                    const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
+                    const int2 *__restrict__ ids, const int2 *__restrict__ ulist,
+                    const unsigned short *__restrict__ usub, uint64_t T,
                     uint64_t W, uint64_t ubeg,
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double ideal,
                     double kappa, int filter_ok,
@@ -1577,6 +1586,9 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // both tiles are stars of one vertex: every pair shares it, and
     // exact.py:205 never counts such a pair -- the unit contributes nothing
     const bool star = bi.star >= 0 && bi.star == bj.star;
+    // j-quarters certified empty for this slice (tile_class_kernel sub-masks)
+    const unsigned skip =
+        usub != nullptr ? (unsigned)(usub[unit] >> (kSubQuarters * slice)) & kSubQuarterMask : 0u;
     double th[kFK];
     int am = 0;  // angle mode: 0 general (reference formula), 2 signed
     double sigma = 1.0;
@@ -1617,30 +1629,41 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else if (ANGLE && am == 2) {
-      if (thr == 1.0f) {
+      for (int q = 0; q < kSubQuarters; ++q) {
+        if (skip & (1u << q)) continue;
+        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+        if (thr == 1.0f) {
 #pragma unroll kJUnrollS
-        for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
-          filter_block<ANGLE, false, kFilterBlockSigned, 2, true>(
-              R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa, rec, ids, theta, ibase,
-              jbase, wq, qn, qc);
-      } else {
+          for (int jj = j0; jj < j1; jj += kFilterBlockSigned)
+            filter_block<ANGLE, false, kFilterBlockSigned, 2, true>(
+                R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa, rec, ids, theta, ibase,
+                jbase, wq, qn, qc);
+        } else {
 #pragma unroll 1
-        for (int jj = 0; jj < kTile; jj += kFilterBlockSigned)
-          filter_block<ANGLE, false, kFilterBlockSigned, 2>(R, th, jr, jth, jj, islot, thr, cnt,
-                                                            dev, A2, ideal, kappa, rec, ids, theta,
-                                                            ibase, jbase, wq, qn, qc);
+          for (int jj = j0; jj < j1; jj += kFilterBlockSigned)
+            filter_block<ANGLE, false, kFilterBlockSigned, 2>(R, th, jr, jth, jj, islot, thr, cnt,
+                                                              dev, A2, ideal, kappa, rec, ids,
+                                                              theta, ibase, jbase, wq, qn, qc);
+        }
       }
-    } else if (thr == 1.0f) {  // general units too: FOLD products with an immediate t
-#pragma unroll kJUnrollC
-      for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, 0, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
-                                                 ideal, kappa, rec, ids, theta, ibase, jbase, wq,
-                                                 qn, qc);
     } else {
+      for (int q = 0; q < kSubQuarters; ++q) {
+        if (skip & (1u << q)) continue;
+        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+        if (thr == 1.0f) {  // general units too: FOLD products with an immediate t
+#pragma unroll kJUnrollC
+          for (int jj = j0; jj < j1; jj += kNJ)
+            filter_block<ANGLE, false, kNJ, 0, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                                     ideal, kappa, rec, ids, theta, ibase, jbase,
+                                                     wq, qn, qc);
+        } else {
 #pragma unroll 1
-      for (int jj = 0; jj < kTile; jj += kNJ)
-        filter_block<ANGLE, false, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
-                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
+          for (int jj = j0; jj < j1; jj += kNJ)
+            filter_block<ANGLE, false, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                               ideal, kappa, rec, ids, theta, ibase, jbase, wq,
+                                               qn, qc);
+        }
+      }
     }
     // release the slice; the warp finishing the unit refills its stage
     __syncwarp();
@@ -2057,10 +2080,13 @@ struct __align__(16) PQBox {
 constexpr double kClassMargin = 0x1p-47;
 enum UnitClass { kUnitNone = 0, kUnitMixed = 1, kUnitFull = 2 };
 
-__global__ void __launch_bounds__(kTile) tile_pq_kernel(const EdgeRec *__restrict__ rec,
-                                                        int64_t m, PQBox *__restrict__ out) {
-  __shared__ double red[8][kTile / 32];
-  const int64_t e = (int64_t)blockIdx.x * kTile + threadIdx.x;
+// one CTA of NB threads per block of NB consecutive edges (NB = kTile:
+// tiles; NB = kSubJ: the sub-blocks of the sub-unit masks)
+template <int NB>
+__global__ void __launch_bounds__(NB) tile_pq_kernel(const EdgeRec *__restrict__ rec, int64_t m,
+                                                     PQBox *__restrict__ out) {
+  __shared__ double red[8][NB / 32];
+  const int64_t e = (int64_t)blockIdx.x * NB + threadIdx.x;
   // v[0..3]: -P.x, P.x, -P.y, P.y maxima; v[4..7] the same for Q
   double v[8];
 #pragma unroll
@@ -2082,7 +2108,7 @@ __global__ void __launch_bounds__(kTile) tile_pq_kernel(const EdgeRec *__restric
   __syncthreads();
   if (threadIdx.x < 8) {
     double x = red[threadIdx.x][0];
-    for (int w = 1; w < kTile / 32; ++w) x = fmax(x, red[threadIdx.x][w]);
+    for (int w = 1; w < NB / 32; ++w) x = fmax(x, red[threadIdx.x][w]);
     // even slots hold -min: negate back (an empty tile gets lo = +inf, hi = -inf)
     reinterpret_cast<double *>(out + blockIdx.x)[threadIdx.x] = (threadIdx.x & 1) ? x : -x;
   }
@@ -2112,6 +2138,15 @@ __device__ inline void orient_ranges(const PQBox &L, const PQBox &R, double (&lo
   }
 }
 
+__device__ inline PQBox pq_union(const PQBox &a, const PQBox &b) {
+  PQBox u;
+  u.px0 = fmin(a.px0, b.px0); u.px1 = fmax(a.px1, b.px1);
+  u.py0 = fmin(a.py0, b.py0); u.py1 = fmax(a.py1, b.py1);
+  u.qx0 = fmin(a.qx0, b.qx0); u.qx1 = fmax(a.qx1, b.qx1);
+  u.qy0 = fmin(a.qy0, b.qy0); u.qy1 = fmax(a.qy1, b.qy1);
+  return u;
+}
+
 __device__ inline int unit_class(const PQBox &A, const PQBox &B) {
   const double x0 = fmin(fmin(A.px0, A.qx0), fmin(B.px0, B.qx0));
   const double x1 = fmax(fmax(A.px1, A.qx1), fmax(B.px1, B.qx1));
@@ -2132,6 +2167,61 @@ __device__ inline int unit_class(const PQBox &A, const PQBox &B) {
   return kUnitMixed;
 }
 
+// "none" half of unit_class: B's endpoints strictly on one side of every line
+// of A (A-lines first; B-lines only when those do not decide).
+__device__ inline bool block_none(const PQBox &A, const PQBox &B) {
+  const double x0 = fmin(fmin(A.px0, A.qx0), fmin(B.px0, B.qx0));
+  const double x1 = fmax(fmax(A.px1, A.qx1), fmax(B.px1, B.qx1));
+  const double y0 = fmin(fmin(A.py0, A.qy0), fmin(B.py0, B.qy0));
+  const double y1 = fmax(fmax(A.py1, A.qy1), fmax(B.py1, B.qy1));
+  const double thr = __dadd_ru(__dmul_ru(__dmul_ru(__dsub_ru(x1, x0), __dsub_ru(y1, y0)),
+                                         kClassMargin * (1.0 + 0x1p-20)),
+                               0x1p-1000);
+  double lo[2], hi[2];
+  orient_ranges(A, B, lo, hi);
+  if ((lo[0] > thr && lo[1] > thr) || (hi[0] < -thr && hi[1] < -thr)) return true;
+  orient_ranges(B, A, lo, hi);
+  return (lo[0] > thr && lo[1] > thr) || (hi[0] < -thr && hi[1] < -thr);
+}
+
+// Sub-unit masks of the mixed part of a classified list: thread (u, bit)
+// tests warp-slice bit / kSubQuarters of tile ti against j-quarter
+// bit % kSubQuarters of tile tj (a sub-block without real edges is empty
+// too); the unit's bits are gathered with one ballot.  Diagonal units and
+// inadmissible inputs keep 0.
+constexpr int kSubBits = kFSlices * kSubQuarters;
+static_assert(32 % kSubBits == 0, "a warp covers whole units");
+__global__ void __launch_bounds__(256)
+sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list,
+                uint64_t mixed, const PQBox *__restrict__ pqs, unsigned short *__restrict__ sub) {
+  constexpr int kPer = kTile / kSubJ;             // sub-blocks per tile
+  constexpr int kSliceBlocks = 32 * kFK / kSubJ;  // sub-blocks per warp slice
+  const bool classify = hdr->admissible != 0;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t total = mixed * kSubBits;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
+       base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = base + threadIdx.x;
+    bool none = false;
+    uint64_t u = idx / kSubBits;
+    if (idx < total) {
+      const int2 p = list[u];
+      const int bit = (int)(idx % kSubBits);
+      if (classify && p.x != p.y) {
+        const int sl = bit / kSubQuarters, q = bit % kSubQuarters;
+        PQBox a = pqs[(int64_t)p.x * kPer + sl * kSliceBlocks];
+        for (int k = 1; k < kSliceBlocks; ++k)
+          a = pq_union(a, pqs[(int64_t)p.x * kPer + sl * kSliceBlocks + k]);
+        const PQBox b = pqs[(int64_t)p.y * kPer + q];
+        none = !(a.px0 <= a.px1) || !(b.px0 <= b.px1) || block_none(a, b);
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, none);
+    if (idx < total && lane % kSubBits == 0)
+      sub[u] = (unsigned short)((bal >> lane) & ((1u << kSubBits) - 1u));
+  }
+}
+
 // Row ti of the classified list: one CTA per row, tj = ti..T-1 in blocks of
 // kClassThreads, order-preserving compaction (warp ballots).  FILL == false
 // counts mixed / full units per row; FILL == true writes mixed units at
@@ -2140,8 +2230,8 @@ constexpr int kClassThreads = 256;
 template <bool FILL>
 __global__ void __launch_bounds__(kClassThreads)
 tile_class_kernel(const RecHeader *__restrict__ hdr, const int4 *__restrict__ box,
-                  const PQBox *__restrict__ pq, int64_t T, unsigned long long *__restrict__ cnt_m,
-                  unsigned long long *__restrict__ cnt_f,
+                  const PQBox *__restrict__ pq, int64_t T,
+                  unsigned long long *__restrict__ cnt_m, unsigned long long *__restrict__ cnt_f,
                   const unsigned long long *__restrict__ off_m,
                   const unsigned long long *__restrict__ off_f, int2 *__restrict__ list) {
   constexpr int kWarps = kClassThreads / 32;
@@ -2423,7 +2513,8 @@ uint64_t chunk_for(uint64_t span, int sworld) {
 int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, double ideal,
                    const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
                    int srank, int sworld, double *d_out, cudaStream_t st,
-                   const int2 *d_full = nullptr, uint64_t fbeg = 0, uint64_t fend = 0) {
+                   const int2 *d_full = nullptr, uint64_t fbeg = 0, uint64_t fend = 0,
+                   const unsigned short *d_sub = nullptr) {
   if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0 || sworld < 1 || srank < 0 ||
       srank >= sworld) {
     set_error("glr_crossing_pairs: invalid arguments");
@@ -2533,8 +2624,8 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
         const uint64_t nbits = (se - sb) * kFSlices;
         GLR_CUDA(cudaMemsetAsync(fix, 0, (size_t)((nbits + 31) / 32) * 4, st));
         cross_filter_kernel<true><<<fgrid, kThreads, 0, st>>>(
-            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, se,
-            chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
+            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, d_sub, T, W,
+            sb, se, chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
         GLR_LAUNCHED("cross_filter_kernel<angle>");
         cross_fixup_kernel<<<xgrid, kFixThreads, 0, st>>>(
             rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, nbits,
@@ -2555,8 +2646,8 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
           filter_ok, cc, cd);
       GLR_LAUNCHED("cross_pairs_kernel<general>");
       cross_filter_kernel<false><<<fgrid, kThreads, 0, st>>>(
-          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, ubeg, uend,
-          chunk, r, g, 0.0, 0.0, filter_ok, cc, xa, nullptr);
+          rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, d_sub, T, W, ubeg,
+          uend, chunk, r, g, 0.0, 0.0, filter_ok, cc, xa, nullptr);
       GLR_LAUNCHED("cross_filter_kernel");
       adj_kernel<false><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,
                                                     d_list, U, T, W, ubeg, uend, chunk, r, g, 0.0,
@@ -2616,7 +2707,8 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
 // Classified candidate list (tile_class_kernel): [mixed units | full units],
 // each part row-major; none-certified units are dropped.
 int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, int2 *d_list,
-                                   uint64_t capacity, uint64_t *h_counts, cudaStream_t st) {
+                                   unsigned short *d_sub, uint64_t capacity, uint64_t *h_counts,
+                                   cudaStream_t st) {
   if (d_records == nullptr || h_counts == nullptr || m < 0 || n < 0) {
     set_error("glr_crossing_candidates_classified: invalid arguments");
     return GLR_EARG;
@@ -2629,13 +2721,15 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
                                          (unsigned long long *)nullptr, (int)(T + 1), st));
   const size_t a_box = al256((size_t)T * sizeof(int4));
   const size_t a_pq = al256((size_t)T * sizeof(PQBox));
+  const size_t a_pqs = al256((size_t)(m_pad / kSubJ) * sizeof(PQBox));
   const size_t a_cnt = al256((size_t)(T + 1) * sizeof(unsigned long long));
-  Scratch scr(a_box + a_pq + 4 * a_cnt + t_scan, st);
+  Scratch scr(a_box + a_pq + a_pqs + 4 * a_cnt + t_scan, st);
   GLR_CUDA(scr.err);
   char *p = scr.as<char>();
   int4 *box = reinterpret_cast<int4 *>(p);
   PQBox *pq = reinterpret_cast<PQBox *>(p + a_box);
-  p += a_box + a_pq;
+  PQBox *pqs = reinterpret_cast<PQBox *>(p + a_box + a_pq);
+  p += a_box + a_pq + a_pqs;
   unsigned long long *cnt_m = reinterpret_cast<unsigned long long *>(p);
   unsigned long long *cnt_f = reinterpret_cast<unsigned long long *>(p + a_cnt);
   unsigned long long *off_m = reinterpret_cast<unsigned long long *>(p + 2 * a_cnt);
@@ -2643,7 +2737,7 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
   void *tmp = p + 4 * a_cnt;
   tile_box_kernel<<<(unsigned)T, kTile, 0, st>>>(rv.rec, box);
   GLR_LAUNCHED("tile_box_kernel");
-  tile_pq_kernel<<<(unsigned)T, kTile, 0, st>>>(rv.rec, m, pq);
+  tile_pq_kernel<kTile><<<(unsigned)T, kTile, 0, st>>>(rv.rec, m, pq);
   GLR_LAUNCHED("tile_pq_kernel");
   GLR_CUDA(cudaMemsetAsync(cnt_m + T, 0, sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(cnt_f + T, 0, sizeof(unsigned long long), st));
@@ -2669,6 +2763,16 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
     tile_class_kernel<true><<<(unsigned)T, kClassThreads, 0, st>>>(rv.hdr, box, pq, T, nullptr,
                                                                     nullptr, off_m, off_f, d_list);
     GLR_LAUNCHED("tile_class_kernel<fill>");
+    if (d_sub != nullptr) {
+      GLR_CUDA(cudaMemsetAsync(d_sub, 0, (size_t)(tot[0] + tot[1]) * sizeof(unsigned short), st));
+      if (tot[0] > 0) {
+        tile_pq_kernel<kSubJ><<<(unsigned)(m_pad / kSubJ), kSubJ, 0, st>>>(rv.rec, m, pqs);
+        GLR_LAUNCHED("tile_pq_kernel<sub>");
+        sub_mask_kernel<<<blocks_for((int64_t)(tot[0] * kSubBits), 256, 16), 256, 0, st>>>(
+            rv.hdr, d_list, tot[0], pqs, d_sub);
+        GLR_LAUNCHED("sub_mask_kernel");
+      }
+    }
   }
   return GLR_OK;
 }
@@ -2747,16 +2851,18 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m, int wit
 }
 
 int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
-                                       void *d_list, uint64_t capacity, uint64_t *h_counts,
-                                       void *stream) {
+                                       void *d_list, void *d_sub, uint64_t capacity,
+                                       uint64_t *h_counts, void *stream) {
   return glr::crossing_candidates_classified(d_records, n, m, reinterpret_cast<int2 *>(d_list),
-                                             capacity, h_counts, glr::as_stream(stream));
+                                             reinterpret_cast<unsigned short *>(d_sub), capacity,
+                                             h_counts, glr::as_stream(stream));
 }
 
 int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m, int with_angle,
-                                  double ideal, const void *d_list, uint64_t mixed_len,
-                                  uint64_t full_len, uint64_t unit_begin, uint64_t unit_end,
-                                  int rank, int world, double *d_out, void *stream) {
+                                  double ideal, const void *d_list, const void *d_sub,
+                                  uint64_t mixed_len, uint64_t full_len, uint64_t unit_begin,
+                                  uint64_t unit_end, int rank, int world, double *d_out,
+                                  void *stream) {
   const uint64_t U = mixed_len + full_len;
   if ((d_list == nullptr && U > 0) || unit_begin > unit_end || unit_end > U || U < mixed_len) {
     glr::set_error("glr_crossing_pairs_classified: unit range [%llu, %llu) outside [0, %llu)",
@@ -2771,7 +2877,8 @@ int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m, i
   const uint64_t fe = (unit_end > mixed_len ? unit_end : mixed_len) - mixed_len;
   return glr::crossing_pairs(d_records, n, m, with_angle, ideal, mixed_len ? lst : nullptr,
                              mixed_len, mb, me, rank, world, d_out, glr::as_stream(stream),
-                             full_len ? lst + mixed_len : nullptr, fb, fe);
+                             full_len ? lst + mixed_len : nullptr, fb, fe,
+                             reinterpret_cast<const unsigned short *>(d_sub));
 }
 
 uint64_t glr_crossing_units(int64_t m) {

@@ -124,19 +124,22 @@ def _check_strategy(strategy: str) -> str:
     return strategy
 
 
-def _classified_candidates(buf: torch.Tensor, n: int, m: int) -> tuple[torch.Tensor, int, int]:
-    """glr_crossing_candidates_classified: ([mixed | full] list, mixed, full)."""
+def _classified_candidates(buf: torch.Tensor, n: int, m: int):
+    """glr_crossing_candidates_classified: ([mixed | full] list, sub-unit
+    masks, mixed, full)."""
     L = _lib.lib()
     counts = (ctypes.c_uint64 * 2)()
-    _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, None, 0, counts, _stream()),
+    _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, None, None, 0, counts,
+                                                    _stream()),
                "glr_crossing_candidates_classified")
     mixed, full = int(counts[0]), int(counts[1])
     lst = torch.empty((max(mixed + full, 1), 2), dtype=torch.int32, device=buf.device)
+    sub = torch.zeros(max(mixed + full, 1), dtype=torch.int16, device=buf.device)
     if mixed + full:
-        _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, _ptr(lst), mixed + full,
-                                                        counts, _stream()),
+        _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, _ptr(lst), _ptr(sub),
+                                                        mixed + full, counts, _stream()),
                    "glr_crossing_candidates_classified")
-    return lst[:mixed + full], mixed, full
+    return lst[:mixed + full], sub, mixed, full
 
 
 def _candidates(fn, *args) -> torch.Tensor:
@@ -251,7 +254,7 @@ class CrossingRecords:
             raise ParameterError(f"order must be one of {self.ORDERS}, got {order!r}")
         self.m = dg.num_edges
         self.n = dg.num_vertices
-        self.list = None
+        self.list = self.sub = None
         self.n_mixed = self.n_full = 0
         if strategy != "dense" and self.m >= 2 and (strategy == "culled"
                                                     or self.m >= AUTO_MIN_EDGES):
@@ -261,10 +264,10 @@ class CrossingRecords:
                                                 _ptr(es), _stream()),
                        "glr_spatial_sort_edges")
             self._prepare(dg.xy, es)
-            lst, mixed, full = _classified_candidates(self.buf, self.n, self.m)
+            lst, sub, mixed, full = _classified_candidates(self.buf, self.n, self.m)
             cost = mixed + FULL_UNIT_WEIGHT * full
             if strategy == "culled" or cost <= CROSS_CULL_FRACTION * crossing_units(self.m):
-                self.list, self.n_mixed, self.n_full = lst, mixed, full
+                self.list, self.sub, self.n_mixed, self.n_full = lst, sub, mixed, full
                 return
             if order == "input":
                 # auto chose the dense pass: results never depend on the edge
@@ -295,6 +298,12 @@ class CrossingRecords:
     @property
     def units(self) -> int:
         return len(self.list) if self.culled else crossing_units(self.m)
+
+    #: skip the sub-unit blocks certified empty (tuning / cross-check knob)
+    use_sub_masks = True
+
+    def _sub_ptr(self):
+        return _ptr(self.sub) if self.use_sub_masks and len(self.list) else None
 
     #: pair-kernel modes (glr_crossing_fast_path / glr_crossing_set_mode)
     MODE_GENERAL, MODE_SIGN, MODE_FILTER = 0, 1, 2
@@ -329,8 +338,9 @@ class CrossingRecords:
                 return out.zero_()
             rc = _lib.lib().glr_crossing_pairs_classified(
                 _ptr(self.buf), self.n, self.m, 0 if ideal is None else 1,
-                0.0 if ideal is None else float(ideal), _ptr(self.list), self.n_mixed,
-                self.n_full, 0, len(self.list), int(rank), int(world), _ptr(out), _stream())
+                0.0 if ideal is None else float(ideal), _ptr(self.list), self._sub_ptr(),
+                self.n_mixed, self.n_full, 0, len(self.list), int(rank), int(world), _ptr(out),
+                _stream())
             _lib.check(rc, "glr_crossing_pairs_classified")
             return out
         rc = _lib.lib().glr_crossing_pairs_interleaved(
@@ -378,7 +388,8 @@ class CrossingRecords:
         if self.culled:
             rc = L.glr_crossing_pairs_classified(_ptr(self.buf), self.n, self.m, angle, ideal_v,
                                                  _ptr(self.list) if len(self.list) else None,
-                                                 self.n_mixed, self.n_full, int(unit_begin),
+                                                 self._sub_ptr(), self.n_mixed, self.n_full,
+                                                 int(unit_begin),
                                                  int(unit_end), 0, 1, _ptr(out), _stream())
             _lib.check(rc, "glr_crossing_pairs_classified")
         else:

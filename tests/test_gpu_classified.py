@@ -214,6 +214,55 @@ def test_classified_abi_ranges(gpu, plan):
     assert cs == int(c) and strict_close(ds, d)
     out = torch.empty(2, dtype=torch.float64, device="cuda")
     rc = L.glr_crossing_pairs_classified(rec.buf.data_ptr(), rec.n, rec.m, 1, IDEAL,
-                                         rec.list.data_ptr(), rec.n_mixed, rec.n_full, 0, U + 1,
-                                         0, 1, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                         rec.list.data_ptr(), rec.sub.data_ptr(), rec.n_mixed,
+                                         rec.n_full, 0, U + 1, 0, 1, out.data_ptr(),
+                                         torch.cuda.current_stream().cuda_stream)
     assert rc == _lib.GLR_EARG
+
+
+def test_sub_masks_sound(plan):
+    """Sub-unit masks: every (warp slice x j-quarter) block marked empty has no
+    crossing by the reference predicate, and the plan gives the same result
+    with the masks ignored."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import _lib
+
+    name, g, dg, rec, edges = plan
+    tile = _lib.lib().glr_crossing_tile()
+    slice_, quarter = 128, tile // 4
+    m = len(edges)
+    lst = rec.list.cpu().numpy()[:rec.n_mixed]
+    sub = rec.sub.cpu().numpy()[:rec.n_mixed].astype(np.int64) & 0xFFFF
+    marked = np.nonzero(sub)[0]
+    if name in ("chung_lu",):
+        assert len(marked) > 0
+    xy = g.xy
+    rng = np.random.default_rng(8)
+    for u in rng.choice(marked, min(40, len(marked)), replace=False) if len(marked) else []:
+        ti, tj = (int(v) for v in lst[u])
+        assert ti != tj
+        for bit in range(8):
+            if not (sub[u] >> bit) & 1:
+                continue
+            s, q = divmod(bit, 4)
+            I = np.arange(ti * tile + s * slice_, min(m, ti * tile + (s + 1) * slice_))
+            J = np.arange(tj * tile + q * quarter, min(m, tj * tile + (q + 1) * quarter))
+            if len(I) == 0 or len(J) == 0:
+                continue
+            ii, jj = np.meshgrid(I, J, indexing="ij")
+            ii, jj = ii.ravel(), jj.ravel()
+            a, b, c, d = xy[edges[ii, 0]], xy[edges[ii, 1]], xy[edges[jj, 0]], xy[edges[jj, 1]]
+            hit = O.straddle_mask(a[:, 0], a[:, 1], b[:, 0], b[:, 1], c[:, 0], c[:, 1], d[:, 0],
+                                  d[:, 1])
+            box = ((np.maximum(c[:, 0], d[:, 0]) >= np.minimum(a[:, 0], b[:, 0]))
+                   & (np.maximum(a[:, 0], b[:, 0]) >= np.minimum(c[:, 0], d[:, 0]))
+                   & (np.maximum(c[:, 1], d[:, 1]) >= np.minimum(a[:, 1], b[:, 1]))
+                   & (np.maximum(a[:, 1], b[:, 1]) >= np.minimum(c[:, 1], d[:, 1])))
+            assert not np.any(hit & box), (name, u, bit)
+    with_masks = rec.partial(IDEAL, 0, rec.units).tolist()
+    rec.use_sub_masks = False
+    try:
+        without = rec.partial(IDEAL, 0, rec.units).tolist()
+    finally:
+        rec.use_sub_masks = True
+    assert with_masks[0] == without[0] and strict_close(with_masks[1], without[1])

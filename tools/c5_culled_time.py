@@ -1,6 +1,6 @@
 """Time the culled C5 plan: build (box sort, prepare, classified candidates)
 and the fused E_c + E_ca pass over it, checked against the C5 golden:
-    python tools/c5_culled_time.py [reps]"""
+    python tools/c5_culled_time.py [reps] [alt]   (alt: odd reps ignore the sub-unit masks)"""
 import json
 import sys
 import time
@@ -19,6 +19,7 @@ for r in range(reps):
     torch.cuda.synchronize()
     t = time.perf_counter()
     rec = M.CrossingRecords(dg, "culled")
+    rec.use_sub_masks = r % 2 == 0 or len(sys.argv) < 3
     torch.cuda.synchronize()
     build = time.perf_counter() - t
     a, b = ev(), ev()
@@ -34,7 +35,7 @@ for r in range(reps):
     ec = a.elapsed_time(b)
     ok = int(c) == want["ec"] and int(c0) == want["ec"] and abs(d - want["dev"]) <= 1e-9 * want["dev"]
     print(json.dumps({"rep": r, "build_ms": round(build * 1e3, 1), "fused_ms": round(fused, 1),
-                      "ec_ms": round(ec, 1), "mixed": rec.n_mixed, "full": rec.n_full,
+                      "ec_ms": round(ec, 1), "sub_masks": rec.use_sub_masks, "mixed": rec.n_mixed, "full": rec.n_full,
                       "dense_units": M.crossing_units(g.num_edges), "count": int(c),
                       "dev": d, "golden_ok": ok}), flush=True)
     del rec
