@@ -1,0 +1,127 @@
+"""Edge orders for the classified culled plan, tried on the host: the edges
+are permuted in numpy, handed to the library in that order (no device sort),
+and the classified plan + fused pass are timed and checked against the C5
+golden.
+    python tools/kd_order_probe.py [variant ...]
+variants: lib (the library's own order), kd-cycle, kd-extent, kd-extent-nogrp"""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2411_09809_b200 import configs, metrics as M  # noqa: E402
+
+TILE = 256
+HUB = 16384
+
+
+def pq(xy, edges):
+    a, b = xy[edges[:, 0]], xy[edges[:, 1]]
+    pa = (a[:, 0] < b[:, 0]) | ((a[:, 0] == b[:, 0]) & (a[:, 1] <= b[:, 1]))
+    P = np.where(pa[:, None], a, b)
+    Q = np.where(pa[:, None], b, a)
+    return np.concatenate([P, Q], axis=1)  # px py qx qy
+
+
+def kd_order(xy, edges, rule, groups=True, hub=HUB):
+    m = len(edges)
+    c = pq(xy, edges)
+    ext = c.max(axis=0) - c.min(axis=0)
+    ext[ext == 0] = 1.0
+    cn = (c - c.min(axis=0)) / ext
+    up = ((c[:, 2] - c[:, 0]) * (c[:, 3] - c[:, 1]) >= 0).astype(np.int64)
+    deg = np.bincount(edges.ravel(), minlength=len(xy))
+    du, dv = deg[edges[:, 0]], deg[edges[:, 1]]
+    hubv = np.where(du >= dv, edges[:, 0], edges[:, 1])
+    grp = np.where(np.maximum(du, dv) >= hub, hubv + 1, 0) if groups else np.zeros(m, np.int64)
+    top = grp * 2 + up
+    perm = np.argsort(top, kind="stable")
+    tops = top[perm]
+    bounds = np.flatnonzero(np.diff(tops)) + 1
+    segs = list(zip(np.r_[0, bounds], np.r_[bounds, m]))
+    # recursion on position ranges, splits at tile boundaries
+    stack = [(int(s), int(e), 0) for s, e in segs]
+    while stack:
+        s, e, lvl = stack.pop()
+        t0 = -(-s // TILE)  # first tile boundary >= s
+        t1 = (e - 1) // TILE  # last tile boundary < e ... boundary positions t*TILE in (s, e)
+        lo = t0 if t0 * TILE > s else t0 + 1
+        if lo > t1:
+            continue
+        mid = (s + e) / 2
+        b = min(range(lo, t1 + 1), key=lambda t: abs(t * TILE - mid)) * TILE if t1 - lo < 8 else \
+            int(min(max(round(mid / TILE), lo), t1)) * TILE
+        idx = perm[s:e]
+        if rule == "cycle":
+            d = lvl % 4
+        else:
+            sub = cn[idx]
+            d = int(np.argmax(sub.max(axis=0) - sub.min(axis=0)))
+        k = b - s
+        part = np.argpartition(cn[idx, d], k - 1 if k > 0 else 0)
+        perm[s:e] = idx[part]
+        stack.append((s, b, lvl + 1))
+        stack.append((b, e, lvl + 1))
+    return perm
+
+
+def run(dg, g, p, es, want, label, reps=2):
+    for r in range(reps):
+        rec = M.CrossingRecords.__new__(M.CrossingRecords)
+        rec.m, rec.n = dg.num_edges, dg.num_vertices
+        rec.list = rec.sub = None
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        rec._prepare(dg.xy, es)
+        rec.list, rec.sub, rec.n_mixed, rec.n_full = M._classified_candidates(rec.buf, rec.n, rec.m)
+        torch.cuda.synchronize()
+        build = time.perf_counter() - t
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        c, d = rec.partial_interleaved(p["ideal"], 0, 1).tolist()
+        b.record()
+        torch.cuda.synchronize()
+        fused = a.elapsed_time(b)
+        a.record()
+        c0 = rec.partial_interleaved(None, 0, 1)[0].item()
+        b.record()
+        torch.cuda.synchronize()
+        ec = a.elapsed_time(b)
+        sub = rec.sub[:rec.n_mixed].to(torch.int32) & 0xFFFF
+        bits = sum(int(((sub >> k) & 1).sum().item()) for k in range(16))
+        ok = int(c) == want["ec"] and int(c0) == want["ec"] and abs(d - want["dev"]) <= 1e-9 * want["dev"]
+        print(json.dumps({"order": label, "rep": r, "prep_class_ms": round(build * 1e3, 1),
+                          "fused_ms": round(fused, 1), "ec_ms": round(ec, 1), "mixed": rec.n_mixed,
+                          "full": rec.n_full, "sub_bits_set": bits,
+                          "dense_units": M.crossing_units(g.num_edges), "golden_ok": ok}), flush=True)
+        del rec
+
+
+def main():
+    variants = sys.argv[1:] or ["lib", "kd-cycle", "kd-extent"]
+    want = json.load(open("tests/golden/golden.json"))["configs"]["C5"]
+    g, p = configs.config5()
+    dg = M.DeviceGraph.from_graph(g)
+    for v in variants:
+        if v == "lib":
+            rec = M.CrossingRecords(dg, "culled")
+            es = torch.empty_like(dg.edges)
+            from paper_2411_09809_b200 import _lib
+            _lib.check(_lib.lib().glr_spatial_sort_edges(M._ptr(dg.xy), dg.num_vertices,
+                                                         M._ptr(dg.edges), dg.num_edges, M._ptr(es),
+                                                         M._stream()), "sort")
+            del rec
+        else:
+            t = time.perf_counter()
+            perm = kd_order(g.xy, g.edges, "cycle" if "cycle" in v else "extent",
+                            groups="nogrp" not in v)
+            print(v, "host order s", round(time.perf_counter() - t, 1), flush=True)
+            es = torch.from_numpy(np.ascontiguousarray(g.edges[perm])).to(dg.edges.device)
+        run(dg, g, p, es, want, v)
+
+
+if __name__ == "__main__":
+    main()
