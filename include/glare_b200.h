@@ -151,12 +151,17 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
  * are compared.  Here whole tile pairs are skipped when their boxes are
  * disjoint (crossing) or farther apart than 2r (occlusion). */
 
-/* Writes to d_edges_out the edge list reordered by (hub group, 4-D Morton
- * code of the edge's bbox sides xmin, xmax, ymin, ymax, diagonal orientation)
- * -- rows unchanged, only their order; hub groups as in
- * glr_theta_sort_edges, for vertices of degree >= 16384.  The metrics do not depend on edge order; tiles
- * compact in all four sides let glr_crossing_candidates skip most tile
- * pairs of short-edge graphs and ~46% of them for long random edges. */
+/* Writes to d_edges_out the edge list in the culled plan's order -- rows
+ * unchanged, only their order; hub groups as in glr_theta_sort_edges, for
+ * vertices of degree >= 16384.  Short edges: (hub group, 4-D Morton code of
+ * the edge's bbox sides xmin, xmax, ymin, ymax, diagonal orientation).  Long
+ * edges (mean bbox half-perimeter >= 1/32 of the domain's): (hub group,
+ * diagonal orientation), then a balanced k-d tree over the endpoints (P.x,
+ * P.y, Q.x, Q.y) whose cells are the 256-edge tiles, 128-edge warp slices and
+ * 64-edge quarters (spatial.cu); one 8-byte read back decides between the
+ * two, so the call synchronises the stream.  The metrics do not depend on
+ * edge order (exact.py:145-222 visits every unordered pair once); compact
+ * tiles let glr_crossing_candidates* skip or certify most tile pairs. */
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                            int64_t m, int64_t *d_edges_out, void *stream);
 
@@ -173,6 +178,11 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
 #endif
 int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                          int64_t m, int64_t hub_degree, int64_t *d_edges_out, void *stream);
+
+/* Tuning / cross-check knob for glr_spatial_sort_edges: on = 0 keeps the
+ * Morton order for long edges too, 1 (default) the k-d order, < 0 only
+ * queries.  Returns the previous setting.  Results never depend on it. */
+int glr_spatial_set_kd(int on);
 
 /* Writes to d_xy_out the vertex positions reordered by Morton code (node
  * occlusion does not depend on vertex order). */

@@ -3,7 +3,7 @@ are permuted in numpy, handed to the library in that order (no device sort),
 and the classified plan + fused pass are timed and checked against the C5
 golden.
     python tools/kd_order_probe.py [variant ...]
-variants: lib (the library's own order), kd-cycle, kd-extent, kd-extent-nogrp"""
+variants: lib (the library's own order), lib-morton, kd-cycle, kd-extent[-nogrp][-leafN][-hubN]"""
 import json
 import sys
 import time
@@ -16,6 +16,7 @@ from paper_2411_09809_b200 import configs, metrics as M  # noqa: E402
 
 TILE = 256
 HUB = 16384
+LEAF = 64
 
 
 def pq(xy, edges):
@@ -46,14 +47,18 @@ def kd_order(xy, edges, rule, groups=True, hub=HUB):
     stack = [(int(s), int(e), 0) for s, e in segs]
     while stack:
         s, e, lvl = stack.pop()
-        t0 = -(-s // TILE)  # first tile boundary >= s
-        t1 = (e - 1) // TILE  # last tile boundary < e ... boundary positions t*TILE in (s, e)
-        lo = t0 if t0 * TILE > s else t0 + 1
-        if lo > t1:
+        b = None
+        for al in (TILE, 128, 64, 32, 16):
+            if al < LEAF:
+                break
+            lo = s // al + 1          # first boundary index with lo*al > s
+            hi = (e - 1) // al        # last boundary index with hi*al < e
+            if lo <= hi:
+                mid = (s + e) / 2
+                b = int(min(max(round(mid / al), lo), hi)) * al
+                break
+        if b is None:
             continue
-        mid = (s + e) / 2
-        b = min(range(lo, t1 + 1), key=lambda t: abs(t * TILE - mid)) * TILE if t1 - lo < 8 else \
-            int(min(max(round(mid / TILE), lo), t1)) * TILE
         idx = perm[s:e]
         if rule == "cycle":
             d = lvl % 4
@@ -106,18 +111,26 @@ def main():
     g, p = configs.config5()
     dg = M.DeviceGraph.from_graph(g)
     for v in variants:
-        if v == "lib":
-            rec = M.CrossingRecords(dg, "culled")
-            es = torch.empty_like(dg.edges)
+        if v.startswith("lib"):
             from paper_2411_09809_b200 import _lib
-            _lib.check(_lib.lib().glr_spatial_sort_edges(M._ptr(dg.xy), dg.num_vertices,
-                                                         M._ptr(dg.edges), dg.num_edges, M._ptr(es),
-                                                         M._stream()), "sort")
-            del rec
+            _lib.lib().glr_spatial_set_kd(0 if "morton" in v else 1)
+            es = torch.empty_like(dg.edges)
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                _lib.check(_lib.lib().glr_spatial_sort_edges(M._ptr(dg.xy), dg.num_vertices,
+                                                             M._ptr(dg.edges), dg.num_edges,
+                                                             M._ptr(es), M._stream()), "sort")
+                torch.cuda.synchronize()
+                print(v, "device sort ms", round(1e3 * (time.perf_counter() - t), 2), flush=True)
         else:
             t = time.perf_counter()
+            import re
+            global LEAF
+            mleaf, mhub = re.search(r"leaf(\d+)", v), re.search(r"hub(\d+)", v)
+            LEAF = int(mleaf.group(1)) if mleaf else 64
             perm = kd_order(g.xy, g.edges, "cycle" if "cycle" in v else "extent",
-                            groups="nogrp" not in v)
+                            groups="nogrp" not in v, hub=int(mhub.group(1)) if mhub else HUB)
             print(v, "host order s", round(time.perf_counter() - t, 1), flush=True)
             es = torch.from_numpy(np.ascontiguousarray(g.edges[perm])).to(dg.edges.device)
         run(dg, g, p, es, want, v)
