@@ -2147,6 +2147,14 @@ __device__ inline PQBox pq_union(const PQBox &a, const PQBox &b) {
   return u;
 }
 
+// The closed bboxes of A's edges and of B's edges are disjoint (P has the
+// smaller x, so the x-range is [px0, qx1]): every pair fails the reference's
+// closed-bbox test (exact.py:191-194) -- exact, plain double comparisons.
+__device__ inline bool pq_disjoint(const PQBox &A, const PQBox &B) {
+  return A.qx1 < B.px0 || B.qx1 < A.px0 || fmax(A.py1, A.qy1) < fmin(B.py0, B.qy0) ||
+         fmax(B.py1, B.qy1) < fmin(A.py0, A.qy0);
+}
+
 __device__ inline int unit_class(const PQBox &A, const PQBox &B) {
   const double x0 = fmin(fmin(A.px0, A.qx0), fmin(B.px0, B.qx0));
   const double x1 = fmax(fmax(A.px1, A.qx1), fmax(B.px1, B.qx1));
@@ -2213,7 +2221,7 @@ sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list
         for (int k = 1; k < kSliceBlocks; ++k)
           a = pq_union(a, pqs[(int64_t)p.x * kPer + sl * kSliceBlocks + k]);
         const PQBox b = pqs[(int64_t)p.y * kPer + q];
-        none = !(a.px0 <= a.px1) || !(b.px0 <= b.px1) || block_none(a, b);
+        none = !(a.px0 <= a.px1) || !(b.px0 <= b.px1) || pq_disjoint(a, b) || block_none(a, b);
       }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, none);

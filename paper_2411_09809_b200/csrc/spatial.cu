@@ -209,7 +209,14 @@ __global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
 // cell boundaries (C5: mean tile box side 0.079 of the domain vs 0.089-0.138,
 // mixed units 42.7M vs 50.5M, fused pass 2.07 -> 1.77 s).  Level-synchronous,
 // no host round trips: the range table lives on the device.
-constexpr int kKdLeaf = 64;
+#ifndef GLR_XTHREADS
+#define GLR_XTHREADS 128
+#endif
+#ifndef GLR_XK
+#define GLR_XK 2
+#endif
+constexpr int kKdTile = GLR_XTHREADS * GLR_XK;  // crossing.cu's kTile
+constexpr int kKdLeaf = kKdTile / 4;            // crossing.cu's kSubJ (j-quarter)
 // tuning / cross-check knob (glr_spatial_set_kd): 0 keeps the Morton order
 int &kd_flag() {
   static int f = 1;
@@ -386,7 +393,7 @@ kd_split_kernel(const int2 *__restrict__ rng, const int *__restrict__ nr,
         if (ext > best) { best = ext; dim = d; }
       }
       if (best > 0) {
-        for (int al = 256; al >= kKdLeaf; al >>= 1) {
+        for (int al = kKdTile; al >= kKdLeaf; al >>= 1) {
           const int lo = se.x / al + 1, hi = (se.y - 1) / al;
           if (lo <= hi) {
             long long bi = ((long long)se.x + se.y + al) / (2ll * al);
@@ -542,7 +549,7 @@ int vertex_sort(const double *d_xy, int64_t n, double *d_out, cudaStream_t st) {
 int kd_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
             int64_t hub_degree, const int *deg, const unsigned long long *b, int64_t *d_out,
             cudaStream_t st) {
-  const int64_t T = (m + 255) / 256;
+  const int64_t T = (m + kKdTile - 1) / kKdTile;
   int levels = 2;  // the 128 and 64 alignments below the tile
   while (levels < 40 && ((int64_t)1 << (levels - 2)) < T + 1) ++levels;
   // initial ranges: the runs of (hub group, orientation); at most two per
