@@ -218,12 +218,19 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m,
  * d_list receives [mixed units | full units], each part row-major, as int2;
  * h_counts[0] = mixed units, h_counts[1] = full units.  Synchronous; the list
  * is written only when d_list != NULL and capacity >= both counts' sum.
- * d_sub (optional, uint16 per list entry): for each mixed unit, bit
- * s * 4 + q set when warp-slice s (128 i-edges) x j-quarter q (64 j-edges)
- * is certified empty; the pair pass then skips it. */
+ * d_sub (optional, one mask of glr_crossing_sub_mask_bytes() bytes per list
+ * entry): for each mixed unit, block b = s * Q + q is warp-slice s (128
+ * i-edges) x j-quarter q (256 / Q j-edges, Q = glr_crossing_sub_quarters());
+ * bit b set: the block is certified empty, bit 2Q + b: certified full (the
+ * same two certificates, on the blocks' own endpoint boxes).  The pair pass
+ * skips both kinds and counts a full block as n_i * n_j crossings with the
+ * pairs' deviations (closed form or exact.py:217-221 per pair). */
 int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
                                        void *d_list, void *d_sub, uint64_t capacity,
                                        uint64_t *h_counts, void *stream);
+/* Layout of d_sub: bytes per mask (2, 4 or 8) and j-quarters per tile. */
+int glr_crossing_sub_mask_bytes(void);
+int glr_crossing_sub_quarters(void);
 
 /* Units [unit_begin, unit_end) of a classified list (unit u = d_list[u]; u <
  * mixed_len: the pair kernels; otherwise a full unit: na * nb crossings and

@@ -101,6 +101,8 @@ SIGNATURES = {
          _c.c_void_p],
     ),
     "glr_spatial_set_kd": (_c.c_int, [_c.c_int]),
+    "glr_crossing_sub_mask_bytes": (_c.c_int, []),
+    "glr_crossing_sub_quarters": (_c.c_int, []),
     "glr_spatial_sort_vertices": (
         _c.c_int, [_c.c_void_p, _c.c_int64, _c.c_void_p, _c.c_void_p]),
     "glr_crossing_candidates": (

@@ -179,14 +179,26 @@ enum FField { kFAx, kFAy, kFBx, kFBy, kFSabx, kFNsaby, kFNska, kFFields };
 constexpr int kFK = GLR_XFK;             // i-edges per lane in the filter kernel
 constexpr int kFGroups = kFK / 2;        // packed i-edge pairs per lane
 constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
-// Sub-unit masks of the classified candidate list (tile_class_kernel): per
-// mixed unit, bit s * kSubQuarters + q marks warp-slice s x j-quarter q
-// (kSubJ consecutive j-edges) certified empty; the filter kernel skips it.
-constexpr int kSubQuarters = 4;
+// Sub-unit masks of the classified candidate list (sub_mask_kernel): per
+// mixed unit, block s * kSubQuarters + q is warp-slice s x j-quarter q (kSubJ
+// consecutive j-edges).  Bit b of the mask: the block is certified empty;
+// bit kSubBits + b: certified full (every pair crosses).  The filter kernel
+// skips both kinds; cross_subfull_kernel counts the full ones.
+#ifndef GLR_XSUBQ
+#define GLR_XSUBQ 4
+#endif
+constexpr int kSubQuarters = GLR_XSUBQ;
 constexpr int kSubJ = kTile / kSubQuarters;
-constexpr unsigned kSubQuarterMask = (1u << kSubQuarters) - 1u;
-static_assert(kFSlices * kSubQuarters <= 16, "sub-masks are 16 bits");
+constexpr unsigned kSubQuarterMask = (kSubQuarters >= 32) ? 0xffffffffu : (1u << kSubQuarters) - 1u;
+constexpr int kSubBits = kFSlices * kSubQuarters;  // blocks per unit
+static_assert(2 * kSubBits <= 64 && 32 % kSubBits == 0, "sub-masks: none + full bits in <= 64");
 static_assert((32 * kFK) % kSubJ == 0, "a warp slice is a whole number of sub-blocks");
+static_assert(kSubJ % 4 == 0 && kSubJ >= 8, "j-quarters are whole filter blocks");
+template <int BITS> struct SubMaskOf { typedef uint64_t type; };
+template <> struct SubMaskOf<16> { typedef unsigned short type; };
+template <> struct SubMaskOf<8> { typedef unsigned short type; };
+template <> struct SubMaskOf<32> { typedef unsigned type; };
+typedef SubMaskOf<2 * kSubBits>::type SubMask;
 // independent hit counters / angle accumulators per lane (ILP vs registers;
 // one counter makes the count-only kernel 3% faster, profiles/r01_variants_filter.txt;
 // in the fused kernel's general units 1 counter + 2 angle accumulators free
@@ -899,12 +911,12 @@ __device__ inline void load_fi(FIRegs &R, const FTile *__restrict__ ftile, uint6
 // evaluates the reference's per-pair formula (angle_dev), so small
 // deviations are bit-identical to numpy's.
 constexpr double kSignMargin = 0x1p-8;
-__device__ inline int unit_shift(const TileBox &a, const TileBox &b, double ideal, double *s,
-                                 double *sigma) {
+__device__ inline int range_shift(float athlo, float athhi, float bthlo, float bthhi,
+                                  double ideal, double *s, double *sigma) {
   const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
   // float bounds are outward-rounded; their double differences are exact
   // or off by far less than kSignMargin
-  const double lo = (double)b.thlo - (double)a.thhi, hi = (double)b.thhi - (double)a.thlo;
+  const double lo = (double)bthlo - (double)athhi, hi = (double)bthhi - (double)athlo;
   if (!(lo <= hi)) return -1;  // empty tile
   double sh;
   if (lo >= 0.0 && hi <= HALF_PI) sh = ideal;
@@ -916,6 +928,10 @@ __device__ inline int unit_shift(const TileBox &a, const TileBox &b, double idea
   if (hi <= sh - kSignMargin) { *sigma = -1.0; return 1; }
   if (lo >= sh + kSignMargin) { *sigma = 1.0; return 1; }
   return 0;
+}
+__device__ inline int unit_shift(const TileBox &a, const TileBox &b, double ideal, double *s,
+                                 double *sigma) {
+  return range_shift(a.thlo, a.thhi, b.thlo, b.thhi, ideal, s, sigma);
 }
 
 // Exact reference predicate for one pair (general semantics: doubles
@@ -1505,7 +1521,7 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                     const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
                     const TileBox *__restrict__ tbox, const double *__restrict__ theta,
                     const int2 *__restrict__ ids, const int2 *__restrict__ ulist,
-                    const unsigned short *__restrict__ usub, uint64_t T,
+                    const SubMask *__restrict__ usub, uint64_t T,
                     uint64_t W, uint64_t ubeg,
                     uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld, double ideal,
                     double kappa, int filter_ok,
@@ -1586,9 +1602,12 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     // both tiles are stars of one vertex: every pair shares it, and
     // exact.py:205 never counts such a pair -- the unit contributes nothing
     const bool star = bi.star >= 0 && bi.star == bj.star;
-    // j-quarters certified empty for this slice (tile_class_kernel sub-masks)
-    const unsigned skip =
-        usub != nullptr ? (unsigned)(usub[unit] >> (kSubQuarters * slice)) & kSubQuarterMask : 0u;
+    // j-quarters certified empty or full for this slice (sub_mask_kernel)
+    unsigned skip = 0u;
+    if (usub != nullptr) {
+      const uint64_t sm = (uint64_t)usub[unit];
+      skip = (unsigned)((sm | (sm >> kSubBits)) >> (kSubQuarters * slice)) & kSubQuarterMask;
+    }
     double th[kFK];
     int am = 0;  // angle mode: 0 general (reference formula), 2 signed
     double sigma = 1.0;
@@ -2192,16 +2211,16 @@ __device__ inline bool block_none(const PQBox &A, const PQBox &B) {
   return (lo[0] > thr && lo[1] > thr) || (hi[0] < -thr && hi[1] < -thr);
 }
 
-// Sub-unit masks of the mixed part of a classified list: thread (u, bit)
-// tests warp-slice bit / kSubQuarters of tile ti against j-quarter
-// bit % kSubQuarters of tile tj (a sub-block without real edges is empty
-// too); the unit's bits are gathered with one ballot.  Diagonal units and
-// inadmissible inputs keep 0.
-constexpr int kSubBits = kFSlices * kSubQuarters;
+// Sub-unit masks of the mixed part of a classified list: thread (u, b)
+// classifies block b of unit u -- warp-slice b / kSubQuarters of tile ti
+// against j-quarter b % kSubQuarters of tile tj -- with unit_class on the
+// blocks' own endpoint boxes (a block without real edges, or with disjoint
+// closed bboxes, is empty too); the unit's bits are gathered with two
+// ballots.  Diagonal units and inadmissible inputs keep 0.
 static_assert(32 % kSubBits == 0, "a warp covers whole units");
 __global__ void __launch_bounds__(256)
 sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list,
-                uint64_t mixed, const PQBox *__restrict__ pqs, unsigned short *__restrict__ sub) {
+                uint64_t mixed, const PQBox *__restrict__ pqs, SubMask *__restrict__ sub) {
   constexpr int kPer = kTile / kSubJ;             // sub-blocks per tile
   constexpr int kSliceBlocks = 32 * kFK / kSubJ;  // sub-blocks per warp slice
   const bool classify = hdr->admissible != 0;
@@ -2210,7 +2229,7 @@ sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
        base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t idx = base + threadIdx.x;
-    bool none = false;
+    bool none = false, full = false;
     uint64_t u = idx / kSubBits;
     if (idx < total) {
       const int2 p = list[u];
@@ -2221,12 +2240,20 @@ sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list
         for (int k = 1; k < kSliceBlocks; ++k)
           a = pq_union(a, pqs[(int64_t)p.x * kPer + sl * kSliceBlocks + k]);
         const PQBox b = pqs[(int64_t)p.y * kPer + q];
-        none = !(a.px0 <= a.px1) || !(b.px0 <= b.px1) || pq_disjoint(a, b) || block_none(a, b);
+        none = !(a.px0 <= a.px1) || !(b.px0 <= b.px1) || pq_disjoint(a, b);
+        if (!none) {
+          const int c = unit_class(a, b);
+          none = c == kUnitNone;
+          full = c == kUnitFull;
+        }
       }
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, none);
-    if (idx < total && lane % kSubBits == 0)
-      sub[u] = (unsigned short)((bal >> lane) & ((1u << kSubBits) - 1u));
+    const unsigned bn = __ballot_sync(0xffffffffu, none);
+    const unsigned bf = __ballot_sync(0xffffffffu, full);
+    if (idx < total && lane % kSubBits == 0) {
+      const uint64_t mask = (1ull << kSubBits) - 1ull;
+      sub[u] = (SubMask)((((uint64_t)bn >> lane) & mask) | ((((uint64_t)bf >> lane) & mask) << kSubBits));
+    }
   }
 }
 
@@ -2370,6 +2397,174 @@ cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ t
   if (threadIdx.x == 0) cta_cnt[blockIdx.x] += acc_cnt;
   if (ANGLE) {
     for (int i = threadIdx.x; i < kAccWords; i += kFullThreads) {
+      unsigned long long v = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
+      cta_acc[(size_t)blockIdx.x * kAccWords + i] += v;
+    }
+  }
+}
+
+// Per kSubJ-block of edges: theta sum (fixed tree) and outward-rounded float
+// theta bounds of its real edges -- what cross_subfull_kernel needs for the
+// closed form of a certified-full block.
+struct SubStat {
+  double tsum;
+  float thlo, thhi;
+};
+__global__ void __launch_bounds__(kSubJ < 32 ? 32 : kSubJ)
+sub_stat_kernel(const double *__restrict__ theta, int64_t m, SubStat *__restrict__ out) {
+  // one warp per block when kSubJ < 32 would waste lanes: a CTA of
+  // max(kSubJ, 32) threads handles max(1, 32 / kSubJ) blocks
+  constexpr int kNT = kSubJ < 32 ? 32 : kSubJ;
+  constexpr int kPerCta = kNT / kSubJ;
+  __shared__ double sh[kNT / 32];
+  __shared__ float slo[kNT / 32], shi[kNT / 32];
+  const int64_t e = (int64_t)blockIdx.x * kNT + threadIdx.x;
+  double t = 0.0;
+  float lo = INFINITY, hi = -INFINITY;
+  if (e < m) {
+    t = theta[e];
+    lo = __double2float_rd(t);
+    hi = __double2float_ru(t);
+  }
+  constexpr int kW = kSubJ < 32 ? kSubJ : 32;  // lanes combined by shuffles
+  for (int o = kW / 2; o > 0; o >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, o, kW);
+    lo = fminf(lo, __shfl_down_sync(0xffffffffu, lo, o, kW));
+    hi = fmaxf(hi, __shfl_down_sync(0xffffffffu, hi, o, kW));
+  }
+  if (kSubJ <= 32) {
+    if (threadIdx.x % kSubJ == 0) {
+      SubStat r; r.tsum = t; r.thlo = lo; r.thhi = hi;
+      out[(int64_t)blockIdx.x * kPerCta + threadIdx.x / kSubJ] = r;
+    }
+  } else {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sh[w] = t; slo[w] = lo; shi[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < kNT / 32; ++i) {
+        t += sh[i];
+        lo = fminf(lo, slo[i]);
+        hi = fmaxf(hi, shi[i]);
+      }
+      SubStat r; r.tsum = t; r.thlo = lo; r.thhi = hi;
+      out[blockIdx.x] = r;
+    }
+  }
+}
+
+// Certified-full blocks of the mixed units (sub_mask_kernel's upper mask
+// bits): every pair of warp-slice s of tile ti and j-quarter q of tile tj
+// crosses properly, so the block contributes n_i * n_j crossings and its
+// pairs' deviations -- in closed form when the block's theta ranges give
+// range_shift's signed form (as cross_full_kernel does per unit), else by
+// the reference's per-pair formula (angle_dev), FP64 only.  One warp per
+// unit; lanes first scan 32 units' masks.  Units are owned by ranks in the
+// chunks of the pair kernels ((u - ubeg) / chunk mod world); runs only in
+// filter mode, like the kernel that skips these blocks.
+constexpr int kSubfullThreads = 256;
+template <bool ANGLE>
+__global__ void __launch_bounds__(kSubfullThreads)
+cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
+                     const int2 *__restrict__ ulist, const SubMask *__restrict__ usub,
+                     uint64_t ubeg, uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld,
+                     int64_t m, const double *__restrict__ theta,
+                     const SubStat *__restrict__ sstat, double ideal,
+                     unsigned long long *__restrict__ cta_cnt,
+                     unsigned long long *__restrict__ cta_acc) {
+  if (hdr->fast != kModeFilter || !filter_ok) return;
+  constexpr int kWarps = kSubfullThreads / 32;
+  constexpr int kSliceEdges = 32 * kFK;
+  constexpr int kSliceBlocks = kSliceEdges / kSubJ;
+  constexpr int kPer = kTile / kSubJ;
+  __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
+  __shared__ unsigned long long acc_cnt;
+  const unsigned lane = threadIdx.x & 31;
+  const int warp = (int)(threadIdx.x >> 5);
+  if (ANGLE)
+    for (int i = threadIdx.x; i < kWarps * kAccWords; i += kSubfullThreads) (&wacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) acc_cnt = 0;
+  __syncthreads();
+  const bool shift_ok = ANGLE && ideal >= 0x1p-100;
+  const uint64_t fullmask = (1ull << kSubBits) - 1ull;
+  unsigned long long total = 0;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t base = ubeg + ((uint64_t)blockIdx.x * kWarps + warp) * 32; base < uend;
+       base += nwarps * 32) {
+    const uint64_t mine = base + lane;
+    uint64_t fm = 0;
+    if (mine < uend && ((mine - ubeg) / chunk) % sworld == srank)
+      fm = ((uint64_t)usub[mine] >> kSubBits) & fullmask;
+    unsigned have = __ballot_sync(0xffffffffu, fm != 0);
+    while (have) {
+      const int src = __ffs(have) - 1;
+      have &= have - 1;
+      const uint64_t u = base + src;
+      uint64_t bits = __shfl_sync(0xffffffffu, fm, src);
+      const int2 p = ulist[u];
+      const int64_t ib = (int64_t)p.x * kTile, jb = (int64_t)p.y * kTile;
+      while (bits) {
+        const int b = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        const int sl = b / kSubQuarters, q = b % kSubQuarters;
+        const int64_t i0 = ib + (int64_t)sl * kSliceEdges, j0 = jb + (int64_t)q * kSubJ;
+        const int64_t ri = m - i0, rj = m - j0;
+        const int ni = (int)(ri < 0 ? 0 : ri < kSliceEdges ? ri : kSliceEdges);
+        const int nj = (int)(rj < 0 ? 0 : rj < kSubJ ? rj : kSubJ);
+        if (lane == 0) total += (unsigned long long)ni * (unsigned long long)nj;
+        if (!ANGLE || ni == 0 || nj == 0) continue;
+        const SubStat sj = sstat[(int64_t)p.y * kPer + q];
+        float ilo = INFINITY, ihi = -INFINITY;
+        double isum = 0.0;
+#pragma unroll
+        for (int k = 0; k < kSliceBlocks; ++k) {
+          const SubStat si = sstat[(int64_t)p.x * kPer + sl * kSliceBlocks + k];
+          ilo = fminf(ilo, si.thlo);
+          ihi = fmaxf(ihi, si.thhi);
+          isum = __dadd_rn(isum, si.tsum);
+        }
+        double sh = 0.0, sigma = 1.0;
+        if (shift_ok && range_shift(ilo, ihi, sj.thlo, sj.thhi, ideal, &sh, &sigma) == 1) {
+          if (lane == 0) {
+            const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)ni, sj.tsum),
+                                                         __dmul_rn((double)nj, isum)),
+                                               __dmul_rn((double)ni * (double)nj, sh));
+            xacc_add(wacc[warp], v > 0.0 ? v : 0.0);
+          }
+          continue;
+        }
+        // per-pair: lane l takes i-edges l, l + 32, ... of the slice
+        double d[kFK];
+        double ti[kFK];
+#pragma unroll
+        for (int k = 0; k < kFK; ++k) {
+          d[k] = 0.0;
+          ti[k] = (int)lane + 32 * k < ni ? theta[i0 + lane + 32 * k] : 0.0;
+        }
+        for (int j = 0; j < nj; ++j) {
+          const double tj = theta[j0 + j];
+#pragma unroll
+          for (int k = 0; k < kFK; ++k) d[k] = __dadd_rn(d[k], angle_dev(ti[k], tj, ideal));
+        }
+        double ds = 0.0;
+#pragma unroll
+        for (int k = 0; k < kFK; ++k)
+          if ((int)lane + 32 * k < ni) ds = __dadd_rn(ds, d[k]);
+        for (int o = 16; o > 0; o >>= 1) ds = __dadd_rn(ds, __shfl_down_sync(0xffffffffu, ds, o));
+        if (lane == 0) xacc_add(wacc[warp], ds);
+      }
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&acc_cnt, total);
+    if (ANGLE) xacc_normalize(wacc[warp]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cta_cnt[blockIdx.x] += acc_cnt;
+  if (ANGLE) {
+    for (int i = threadIdx.x; i < kAccWords; i += kSubfullThreads) {
       unsigned long long v = 0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) v += wacc[w][i];
@@ -2522,7 +2717,7 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
                    const int2 *d_list, uint64_t list_len, uint64_t ubeg, uint64_t uend,
                    int srank, int sworld, double *d_out, cudaStream_t st,
                    const int2 *d_full = nullptr, uint64_t fbeg = 0, uint64_t fend = 0,
-                   const unsigned short *d_sub = nullptr) {
+                   const SubMask *d_sub = nullptr) {
   if (d_records == nullptr || d_out == nullptr || m < 0 || n < 0 || sworld < 1 || srank < 0 ||
       srank >= sworld) {
     set_error("glr_crossing_pairs: invalid arguments");
@@ -2575,12 +2770,17 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   if (seg_len < seg_align) seg_len = seg_align;
   const uint64_t seg_max = span < seg_len ? span : seg_len;
   const size_t a_fix = with_angle ? al256((size_t)((seg_max * kFSlices + 31) / 32) * 4) : 0;
-  const int ncta = cgrid + ggrid;            // count / FP64 slots: pair kernels, full kernel
-  const int nacc = cgrid + xgrid + ggrid;    // exact accumulators: filter, fixup, full
+  // certified-full blocks of the mixed units (cross_subfull_kernel)
+  const int sgrid = (d_sub != nullptr && span > 0)
+                        ? blocks_for((int64_t)((span + sworld - 1) / sworld), kSubfullThreads, 8)
+                        : 0;
+  const int ncta = cgrid + ggrid + sgrid;          // count / FP64 slots: pair, full, sub-full
+  const int nacc = cgrid + xgrid + ggrid + sgrid;  // exact accumulators: filter, fixup, full, sub-full
   const size_t a_acc = (size_t)nacc * kAccWords * sizeof(unsigned long long);
   const size_t a_ts = (with_angle && fspan > 0) ? al256((size_t)(m_pad / kTile) * sizeof(double)) : 0;
+  const size_t a_ss = (with_angle && sgrid > 0) ? al256((size_t)(m_pad / kSubJ) * sizeof(SubStat)) : 0;
   Scratch scr((size_t)(ncta + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc +
-                  a_fix + a_ts + 512,
+                  a_fix + a_ts + a_ss + 768,
               st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
@@ -2592,6 +2792,8 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
       (reinterpret_cast<uintptr_t>(xa + (size_t)nacc * kAccWords) + 255) & ~(uintptr_t)255);
   double *tsum = reinterpret_cast<double *>(
       (reinterpret_cast<uintptr_t>(fix) + a_fix + 255) & ~(uintptr_t)255);
+  SubStat *sstat = reinterpret_cast<SubStat *>(
+      (reinterpret_cast<uintptr_t>(tsum) + a_ts + 255) & ~(uintptr_t)255);
   // only the kernel of the records' mode writes its CTA slots
   GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)ncta * sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)ncta * sizeof(double), st));
@@ -2609,6 +2811,26 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
           rv.tbox, rv.theta, nullptr, d_full, fbeg, fend, fchunk, (unsigned)srank,
           (unsigned)sworld, m, 0.0, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
       GLR_LAUNCHED("cross_full_kernel");
+    }
+  }
+  if (sgrid > 0) {
+    const uint64_t chunk_s = chunk_for(span, sworld);
+    const int filter_ok_s = (!with_angle || ideal >= 0x1p-100) ? 1 : 0;
+    unsigned long long *scc = cc + cgrid + ggrid;
+    unsigned long long *sxa = xa + (size_t)(cgrid + xgrid + ggrid) * kAccWords;
+    if (with_angle) {
+      constexpr int kNT = kSubJ < 32 ? 32 : kSubJ;
+      sub_stat_kernel<<<(unsigned)(m_pad / kNT), kNT, 0, st>>>(rv.theta, m, sstat);
+      GLR_LAUNCHED("sub_stat_kernel");
+      cross_subfull_kernel<true><<<sgrid, kSubfullThreads, 0, st>>>(
+          rv.hdr, filter_ok_s, d_list, d_sub, ubeg, uend, chunk_s, (unsigned)srank,
+          (unsigned)sworld, m, rv.theta, sstat, ideal, scc, sxa);
+      GLR_LAUNCHED("cross_subfull_kernel<angle>");
+    } else {
+      cross_subfull_kernel<false><<<sgrid, kSubfullThreads, 0, st>>>(
+          rv.hdr, filter_ok_s, d_list, d_sub, ubeg, uend, chunk_s, (unsigned)srank,
+          (unsigned)sworld, m, rv.theta, nullptr, 0.0, scc, sxa);
+      GLR_LAUNCHED("cross_subfull_kernel");
     }
   }
   if (span > 0) {
@@ -2715,7 +2937,7 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
 // Classified candidate list (tile_class_kernel): [mixed units | full units],
 // each part row-major; none-certified units are dropped.
 int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, int2 *d_list,
-                                   unsigned short *d_sub, uint64_t capacity, uint64_t *h_counts,
+                                   SubMask *d_sub, uint64_t capacity, uint64_t *h_counts,
                                    cudaStream_t st) {
   if (d_records == nullptr || h_counts == nullptr || m < 0 || n < 0) {
     set_error("glr_crossing_candidates_classified: invalid arguments");
@@ -2772,7 +2994,7 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
                                                                     nullptr, off_m, off_f, d_list);
     GLR_LAUNCHED("tile_class_kernel<fill>");
     if (d_sub != nullptr) {
-      GLR_CUDA(cudaMemsetAsync(d_sub, 0, (size_t)(tot[0] + tot[1]) * sizeof(unsigned short), st));
+      GLR_CUDA(cudaMemsetAsync(d_sub, 0, (size_t)(tot[0] + tot[1]) * sizeof(SubMask), st));
       if (tot[0] > 0) {
         tile_pq_kernel<kSubJ><<<(unsigned)(m_pad / kSubJ), kSubJ, 0, st>>>(rv.rec, m, pqs);
         GLR_LAUNCHED("tile_pq_kernel<sub>");
@@ -2803,6 +3025,10 @@ extern "C" int glr_debug_fstats(unsigned long long *h, int reset) {
 extern "C" {
 
 int glr_crossing_tile(void) { return glr::kTile; }
+
+int glr_crossing_sub_mask_bytes(void) { return (int)sizeof(glr::SubMask); }
+
+int glr_crossing_sub_quarters(void) { return glr::kSubQuarters; }
 
 int glr_crossing_band(void) { return glr::kBandTiles; }
 
@@ -2862,7 +3088,7 @@ int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t
                                        void *d_list, void *d_sub, uint64_t capacity,
                                        uint64_t *h_counts, void *stream) {
   return glr::crossing_candidates_classified(d_records, n, m, reinterpret_cast<int2 *>(d_list),
-                                             reinterpret_cast<unsigned short *>(d_sub), capacity,
+                                             reinterpret_cast<glr::SubMask *>(d_sub), capacity,
                                              h_counts, glr::as_stream(stream));
 }
 
@@ -2886,7 +3112,7 @@ int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m, i
   return glr::crossing_pairs(d_records, n, m, with_angle, ideal, mixed_len ? lst : nullptr,
                              mixed_len, mb, me, rank, world, d_out, glr::as_stream(stream),
                              full_len ? lst + mixed_len : nullptr, fb, fe,
-                             reinterpret_cast<const unsigned short *>(d_sub));
+                             reinterpret_cast<const glr::SubMask *>(d_sub));
 }
 
 uint64_t glr_crossing_units(int64_t m) {

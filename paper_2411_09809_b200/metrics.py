@@ -134,7 +134,8 @@ def _classified_candidates(buf: torch.Tensor, n: int, m: int):
                "glr_crossing_candidates_classified")
     mixed, full = int(counts[0]), int(counts[1])
     lst = torch.empty((max(mixed + full, 1), 2), dtype=torch.int32, device=buf.device)
-    sub = torch.zeros(max(mixed + full, 1), dtype=torch.int16, device=buf.device)
+    sub_dtype = {2: torch.int16, 4: torch.int32, 8: torch.int64}[L.glr_crossing_sub_mask_bytes()]
+    sub = torch.zeros(max(mixed + full, 1), dtype=sub_dtype, device=buf.device)
     if mixed + full:
         _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, _ptr(lst), _ptr(sub),
                                                         mixed + full, counts, _stream()),

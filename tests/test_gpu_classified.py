@@ -266,3 +266,55 @@ def test_sub_masks_sound(plan):
     finally:
         rec.use_sub_masks = True
     assert with_masks[0] == without[0] and strict_close(with_masks[1], without[1])
+
+
+def test_sub_full_blocks_cross_everywhere(plan):
+    """Sub-unit masks, upper bits: every (warp slice x j-quarter) block marked
+    full has all its pairs crossing by the reference predicate (bboxes
+    overlapping, no shared vertex), and a plan restricted to such units gives
+    the oracle's count and deviation sum for them."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import _lib
+
+    name, g, dg, rec, edges = plan
+    L = _lib.lib()
+    tile, Q = L.glr_crossing_tile(), L.glr_crossing_sub_quarters()
+    slice_, quarter = 128, tile // Q
+    nb = (tile // slice_) * Q
+    m = len(edges)
+    lst = rec.list.cpu().numpy()[:rec.n_mixed]
+    sub = rec.sub.cpu().numpy()[:rec.n_mixed].astype(np.int64)
+    fullbits = (sub >> nb) & ((1 << nb) - 1)
+    assert not np.any(fullbits & sub & ((1 << nb) - 1)), "a block is both empty and full"
+    marked = np.nonzero(fullbits)[0]
+    if name in ("chung_lu", "bundles"):
+        assert len(marked) > 0, name
+    xy = g.xy
+    rng = np.random.default_rng(9)
+    for u in rng.choice(marked, min(30, len(marked)), replace=False) if len(marked) else []:
+        ti, tj = (int(v) for v in lst[u])
+        assert ti != tj
+        for bit in range(nb):
+            if not (fullbits[u] >> bit) & 1:
+                continue
+            s, q = divmod(bit, Q)
+            I = np.arange(ti * tile + s * slice_, min(m, ti * tile + (s + 1) * slice_))
+            J = np.arange(tj * tile + q * quarter, min(m, tj * tile + (q + 1) * quarter))
+            assert len(I) and len(J)
+            ii, jj = np.meshgrid(I, J, indexing="ij")
+            ii, jj = ii.ravel(), jj.ravel()
+            a, b, c, d = xy[edges[ii, 0]], xy[edges[ii, 1]], xy[edges[jj, 0]], xy[edges[jj, 1]]
+            hit = O.straddle_mask(a[:, 0], a[:, 1], b[:, 0], b[:, 1], c[:, 0], c[:, 1], d[:, 0],
+                                  d[:, 1])
+            box = ((np.maximum(c[:, 0], d[:, 0]) >= np.minimum(a[:, 0], b[:, 0]))
+                   & (np.maximum(a[:, 0], b[:, 0]) >= np.minimum(c[:, 0], d[:, 0]))
+                   & (np.maximum(c[:, 1], d[:, 1]) >= np.minimum(a[:, 1], b[:, 1]))
+                   & (np.maximum(a[:, 1], b[:, 1]) >= np.minimum(c[:, 1], d[:, 1])))
+            share = ((edges[ii, 0] == edges[jj, 0]) | (edges[ii, 0] == edges[jj, 1])
+                     | (edges[ii, 1] == edges[jj, 0]) | (edges[ii, 1] == edges[jj, 1]))
+            assert np.all(hit & box & ~share), (name, u, bit)
+        # the unit through the kernels (filter on the rest + sub-full blocks)
+        oc, od = O.crossing_scan_tiles(g.xy, edges, IDEAL, tile, [(ti, tj)])
+        gc, gd = rec.partial(IDEAL, int(u), int(u) + 1).tolist()
+        assert int(gc) == oc and strict_close(gd, od), (name, u, gc, oc)
+        assert int(rec.partial(None, int(u), int(u) + 1)[0].item()) == oc

@@ -95,12 +95,15 @@ def run(dg, g, p, es, want, label, reps=2):
         b.record()
         torch.cuda.synchronize()
         ec = a.elapsed_time(b)
-        sub = rec.sub[:rec.n_mixed].to(torch.int32) & 0xFFFF
-        bits = sum(int(((sub >> k) & 1).sum().item()) for k in range(16))
+        from paper_2411_09809_b200 import _lib
+        nbk = 2 * _lib.lib().glr_crossing_sub_quarters()
+        sub = rec.sub[:rec.n_mixed].to(torch.int64)
+        bits = sum(int(((sub >> k) & 1).sum().item()) for k in range(nbk))
+        fbits = sum(int(((sub >> (nbk + k)) & 1).sum().item()) for k in range(nbk))
         ok = int(c) == want["ec"] and int(c0) == want["ec"] and abs(d - want["dev"]) <= 1e-9 * want["dev"]
         print(json.dumps({"order": label, "rep": r, "prep_class_ms": round(build * 1e3, 1),
                           "fused_ms": round(fused, 1), "ec_ms": round(ec, 1), "mixed": rec.n_mixed,
-                          "full": rec.n_full, "sub_bits_set": bits,
+                          "full": rec.n_full, "sub_none": bits, "sub_full": fbits, "sub_blocks": nbk * rec.n_mixed,
                           "dense_units": M.crossing_units(g.num_edges), "golden_ok": ok}), flush=True)
         del rec
 
