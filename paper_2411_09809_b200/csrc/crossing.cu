@@ -2194,23 +2194,6 @@ __device__ inline int unit_class(const PQBox &A, const PQBox &B) {
   return kUnitMixed;
 }
 
-// "none" half of unit_class: B's endpoints strictly on one side of every line
-// of A (A-lines first; B-lines only when those do not decide).
-__device__ inline bool block_none(const PQBox &A, const PQBox &B) {
-  const double x0 = fmin(fmin(A.px0, A.qx0), fmin(B.px0, B.qx0));
-  const double x1 = fmax(fmax(A.px1, A.qx1), fmax(B.px1, B.qx1));
-  const double y0 = fmin(fmin(A.py0, A.qy0), fmin(B.py0, B.qy0));
-  const double y1 = fmax(fmax(A.py1, A.qy1), fmax(B.py1, B.qy1));
-  const double thr = __dadd_ru(__dmul_ru(__dmul_ru(__dsub_ru(x1, x0), __dsub_ru(y1, y0)),
-                                         kClassMargin * (1.0 + 0x1p-20)),
-                               0x1p-1000);
-  double lo[2], hi[2];
-  orient_ranges(A, B, lo, hi);
-  if ((lo[0] > thr && lo[1] > thr) || (hi[0] < -thr && hi[1] < -thr)) return true;
-  orient_ranges(B, A, lo, hi);
-  return (lo[0] > thr && lo[1] > thr) || (hi[0] < -thr && hi[1] < -thr);
-}
-
 // Sub-unit masks of the mixed part of a classified list: thread (u, b)
 // classifies block b of unit u -- warp-slice b / kSubQuarters of tile ti
 // against j-quarter b % kSubQuarters of tile tj -- with unit_class on the
@@ -2320,25 +2303,112 @@ __global__ void __launch_bounds__(kTile) tile_theta_sum_kernel(const double *__r
   if (threadIdx.x == 0) ts[blockIdx.x] = s;
 }
 
+// Per NB-block of edges: theta of the real edges sorted ascending (pads
+// +inf, at the end) and the exclusive prefix sums of the sorted values --
+// what piecewise_dev needs.  One CTA of NB threads per block, bitonic network
+// in shared memory (comparisons and moves only), Hillis-Steele scan.
+template <int NB>
+__global__ void __launch_bounds__(NB)
+theta_sort_kernel(const double *__restrict__ theta, int64_t m, double *__restrict__ ts,
+                  double *__restrict__ tp) {
+  __shared__ double v[NB];
+  __shared__ double sc[2][NB];
+  const int t = (int)threadIdx.x;
+  const int64_t e = (int64_t)blockIdx.x * NB + t;
+  v[t] = e < m ? theta[e] : INFINITY;
+  __syncthreads();
+  for (int k = 2; k <= NB; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int p = t ^ j;
+      if (p > t) {
+        const double a = v[t], b = v[p];
+        const bool up = (t & k) == 0;
+        if ((a > b) == up) { v[t] = b; v[p] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  const double x = v[t];
+  int cur = 0;
+  sc[0][t] = isfinite(x) ? x : 0.0;  // theta is finite in [0, pi]
+  __syncthreads();
+  for (int o = 1; o < NB; o <<= 1) {
+    const double a = sc[cur][t], b = t >= o ? sc[cur][t - o] : 0.0;
+    sc[cur ^ 1][t] = t >= o ? __dadd_rn(b, a) : a;
+    cur ^= 1;
+    __syncthreads();
+  }
+  ts[e] = x;
+  tp[e] = t > 0 ? sc[cur][t - 1] : 0.0;  // exclusive
+}
+
+// sum over j of |ideal - min(|d|, pi - |d|)|, d = s[j] - ti, for the n sorted
+// angles s[0..n) with exclusive prefix sums pre[] and total tot: the
+// deviation (geometry.py:107-110, exact.py:219-221) is piecewise linear in d
+// on (-pi, pi) with kinks at 0, +-ideal, +-pi/2, +-(pi - ideal), so seven
+// binary searches cut the sorted angles into eight runs on which it is c +
+// sg * d, and each run contributes cnt * c + sg * (sum of its angles - cnt *
+// ti).  The value is continuous at the kinks, so an angle within an ulp of
+// one may fall on either side.  Absolute error <= ~1e-12 per call (sums of
+// <= 256 angles); callers re-evaluate per pair when the mean deviation is
+// small (kPiecewiseMeanDev).
+constexpr double kPiecewiseMeanDev = 0x1p-12;
+__device__ inline int lower_bound_f64(const double *s, int n, double x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ inline double piecewise_dev(double ti, const double *s, const double *pre, int n,
+                                       double tot, double ideal) {
+  const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
+  const double pmi = __dsub_rn(PI, ideal);
+  const double bp[7] = {-pmi, -HALF_PI, -ideal, 0.0, ideal, HALF_PI, pmi};
+  const double c[8] = {-pmi, pmi, -ideal, ideal, ideal, -ideal, pmi, -pmi};
+  int a = 0;
+  double pa = 0.0, acc = 0.0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int b = p < 7 ? lower_bound_f64(s, n, __dadd_rn(ti, bp[p])) : n;
+    const int bb = b < a ? a : b;  // monotone whatever the roundings
+    const double pb = bb < n ? pre[bb] : tot;
+    const double cnt = (double)(bb - a);
+    const double lin = __dsub_rn(__dsub_rn(pb, pa), __dmul_rn(cnt, ti));
+    const double v = __dadd_rn(__dmul_rn(cnt, c[p]), (p & 1) ? lin : -lin);
+    acc = __dadd_rn(acc, v > 0.0 ? v : 0.0);
+    a = bb;
+    pa = pb;
+  }
+  return acc;
+}
+
 // Full units (every pair crosses, tile_class_kernel): na * nb crossings and
 // the deviation sum.  Units whose theta ranges give unit_shift's signed form
 // take it in closed form from the tiles' theta sums,
 //   sum_ij |theta_j - theta_i - s| = sigma (na sum_j theta_j - nb sum_i
 //   theta_i - na nb s),
 // (each term at least kSignMargin, so the cancellation costs < 1e-12
-// relative); the others evaluate the reference's per-pair formula
-// (angle_dev) for all na * nb pairs -- FP64 only, no predicate.  Same chunk
-// ownership as the pair kernels; the slice sums go to exact accumulators.
+// relative); the others sum the piecewise-linear deviation over the j-tile's
+// sorted angles (piecewise_dev: seven binary searches per i-edge instead of
+// nb per-pair evaluations), falling back to the reference's per-pair formula
+// (angle_dev) when the unit's mean deviation is below kPiecewiseMeanDev.
+// FP64 only, no predicate.  Same chunk ownership as the pair kernels; the
+// sums go to exact accumulators.
 constexpr int kFullThreads = kTile;  // thread t: i-edge t of the unit
 template <bool ANGLE>
 __global__ void __launch_bounds__(kFullThreads)
 cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ theta,
-                  const double *__restrict__ tsum, const int2 *__restrict__ flist, uint64_t fbeg,
-                  uint64_t fend, uint64_t chunk, unsigned srank, unsigned sworld, int64_t m,
-                  double ideal, unsigned long long *__restrict__ cta_cnt,
+                  const double *__restrict__ tsum, const double *__restrict__ tsorted,
+                  const double *__restrict__ tprefix, const int2 *__restrict__ flist,
+                  uint64_t fbeg, uint64_t fend, uint64_t chunk, unsigned srank, unsigned sworld,
+                  int64_t m, double ideal, unsigned long long *__restrict__ cta_cnt,
                   unsigned long long *__restrict__ cta_acc) {
   constexpr int kWarps = kFullThreads / 32;
-  __shared__ double sth[kTile];
+  __shared__ double sth[ANGLE ? kTile : 1], spre[ANGLE ? kTile : 1];
+  __shared__ double red[kWarps];
+  __shared__ int per_pair;
   __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
   const unsigned lane = threadIdx.x & 31;
   const int warp = (int)(threadIdx.x >> 5);
@@ -2370,12 +2440,31 @@ cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ t
       }
       continue;
     }
-    __syncthreads();  // the previous unit's theta_j are consumed
-    sth[threadIdx.x] = theta[(int64_t)tj * kTile + threadIdx.x];
+    // piecewise-linear sums over the j-tile's sorted angles (piecewise_dev)
+    __syncthreads();  // the previous unit's angles are consumed
+    sth[threadIdx.x] = tsorted[(int64_t)tj * kTile + threadIdx.x];
+    spre[threadIdx.x] = tprefix[(int64_t)tj * kTile + threadIdx.x];
     __syncthreads();
+    const double t = (int)threadIdx.x < na ? theta[(int64_t)ti * kTile + threadIdx.x] : 0.0;
+    {
+      const double tot = __dadd_rn(sth[nb - 1], spre[nb - 1]);
+      double d = (int)threadIdx.x < na ? piecewise_dev(t, sth, spre, nb, tot, ideal) : 0.0;
+      for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
+      if (lane == 0) red[warp] = d;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < kWarps; ++w) v = __dadd_rn(v, red[w]);
+        // small mean deviation: the per-pair formula below (bit-identical
+        // to numpy's for each pair) instead
+        per_pair = v < (double)na * (double)nb * kPiecewiseMeanDev ? 1 : 0;
+        if (!per_pair) xacc_add(wacc[0], v);
+      }
+      __syncthreads();
+    }
+    if (!per_pair) continue;
     double d = 0.0;
     if ((int)threadIdx.x < na) {
-      const double t = theta[(int64_t)ti * kTile + threadIdx.x];
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       int j = 0;
       for (; j + 4 <= nb; j += 4) {
@@ -2471,7 +2560,8 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
                      const int2 *__restrict__ ulist, const SubMask *__restrict__ usub,
                      uint64_t ubeg, uint64_t uend, uint64_t chunk, unsigned srank, unsigned sworld,
                      int64_t m, const double *__restrict__ theta,
-                     const SubStat *__restrict__ sstat, double ideal,
+                     const SubStat *__restrict__ sstat, const double *__restrict__ qsorted,
+                     const double *__restrict__ qprefix, double ideal,
                      unsigned long long *__restrict__ cta_cnt,
                      unsigned long long *__restrict__ cta_acc) {
   if (hdr->fast != kModeFilter || !filter_ok) return;
@@ -2480,6 +2570,7 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
   constexpr int kSliceBlocks = kSliceEdges / kSubJ;
   constexpr int kPer = kTile / kSubJ;
   __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
+  __shared__ double wsrt[ANGLE ? kWarps : 1][ANGLE ? kSubJ : 1], wpre[ANGLE ? kWarps : 1][ANGLE ? kSubJ : 1];
   __shared__ unsigned long long acc_cnt;
   const unsigned lane = threadIdx.x & 31;
   const int warp = (int)(threadIdx.x >> 5);
@@ -2535,24 +2626,43 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
           }
           continue;
         }
-        // per-pair: lane l takes i-edges l, l + 32, ... of the slice
-        double d[kFK];
+        // lane l takes i-edges l, l + 32, ... of the slice: piecewise-linear
+        // sums over the j-quarter's sorted angles (piecewise_dev), or the
+        // per-pair formula when the block's mean deviation is small
         double ti[kFK];
 #pragma unroll
-        for (int k = 0; k < kFK; ++k) {
-          d[k] = 0.0;
+        for (int k = 0; k < kFK; ++k)
           ti[k] = (int)lane + 32 * k < ni ? theta[i0 + lane + 32 * k] : 0.0;
+        __syncwarp();
+        for (int j = (int)lane; j < kSubJ; j += 32) {
+          wsrt[warp][j] = qsorted[j0 + j];
+          wpre[warp][j] = qprefix[j0 + j];
         }
-        for (int j = 0; j < nj; ++j) {
-          const double tj = theta[j0 + j];
-#pragma unroll
-          for (int k = 0; k < kFK; ++k) d[k] = __dadd_rn(d[k], angle_dev(ti[k], tj, ideal));
-        }
+        __syncwarp();
+        const double tot = __dadd_rn(wsrt[warp][nj - 1], wpre[warp][nj - 1]);
         double ds = 0.0;
 #pragma unroll
         for (int k = 0; k < kFK; ++k)
-          if ((int)lane + 32 * k < ni) ds = __dadd_rn(ds, d[k]);
+          if ((int)lane + 32 * k < ni)
+            ds = __dadd_rn(ds, piecewise_dev(ti[k], wsrt[warp], wpre[warp], nj, tot, ideal));
         for (int o = 16; o > 0; o >>= 1) ds = __dadd_rn(ds, __shfl_down_sync(0xffffffffu, ds, o));
+        ds = __shfl_sync(0xffffffffu, ds, 0);
+        if (ds < (double)ni * (double)nj * kPiecewiseMeanDev) {
+          double d[kFK];
+#pragma unroll
+          for (int k = 0; k < kFK; ++k) d[k] = 0.0;
+          for (int j = 0; j < nj; ++j) {
+            const double tj = wsrt[warp][j];
+#pragma unroll
+            for (int k = 0; k < kFK; ++k) d[k] = __dadd_rn(d[k], angle_dev(ti[k], tj, ideal));
+          }
+          ds = 0.0;
+#pragma unroll
+          for (int k = 0; k < kFK; ++k)
+            if ((int)lane + 32 * k < ni) ds = __dadd_rn(ds, d[k]);
+          for (int o = 16; o > 0; o >>= 1)
+            ds = __dadd_rn(ds, __shfl_down_sync(0xffffffffu, ds, o));
+        }
         if (lane == 0) xacc_add(wacc[warp], ds);
       }
     }
@@ -2779,8 +2889,11 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
   const size_t a_acc = (size_t)nacc * kAccWords * sizeof(unsigned long long);
   const size_t a_ts = (with_angle && fspan > 0) ? al256((size_t)(m_pad / kTile) * sizeof(double)) : 0;
   const size_t a_ss = (with_angle && sgrid > 0) ? al256((size_t)(m_pad / kSubJ) * sizeof(SubStat)) : 0;
+  // sorted angles + prefix sums per tile (full units) and per j-quarter (full blocks)
+  const size_t a_srt = al256((size_t)m_pad * sizeof(double));
+  const int n_srt = with_angle ? (fspan > 0 ? 2 : 0) + (sgrid > 0 ? 2 : 0) : 0;
   Scratch scr((size_t)(ncta + agrid) * (sizeof(unsigned long long) + sizeof(double)) + a_acc +
-                  a_fix + a_ts + a_ss + 768,
+                  a_fix + a_ts + a_ss + n_srt * a_srt + 1024,
               st);
   GLR_CUDA(scr.err);
   unsigned long long *cc = scr.as<unsigned long long>();
@@ -2794,6 +2907,12 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
       (reinterpret_cast<uintptr_t>(fix) + a_fix + 255) & ~(uintptr_t)255);
   SubStat *sstat = reinterpret_cast<SubStat *>(
       (reinterpret_cast<uintptr_t>(tsum) + a_ts + 255) & ~(uintptr_t)255);
+  char *srt = reinterpret_cast<char *>(
+      (reinterpret_cast<uintptr_t>(sstat) + a_ss + 255) & ~(uintptr_t)255);
+  double *tsort = reinterpret_cast<double *>(srt);
+  double *tpre = reinterpret_cast<double *>(srt + a_srt);
+  double *qsort = reinterpret_cast<double *>(srt + (fspan > 0 ? 2 : 0) * a_srt);
+  double *qpre = reinterpret_cast<double *>(srt + (fspan > 0 ? 3 : 1) * a_srt);
   // only the kernel of the records' mode writes its CTA slots
   GLR_CUDA(cudaMemsetAsync(cc, 0, (size_t)ncta * sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(cd, 0, (size_t)ncta * sizeof(double), st));
@@ -2802,14 +2921,18 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
     if (with_angle) {
       tile_theta_sum_kernel<<<(unsigned)(m_pad / kTile), kTile, 0, st>>>(rv.theta, m, tsum);
       GLR_LAUNCHED("tile_theta_sum_kernel");
+      theta_sort_kernel<kTile><<<(unsigned)(m_pad / kTile), kTile, 0, st>>>(rv.theta, m, tsort,
+                                                                            tpre);
+      GLR_LAUNCHED("theta_sort_kernel");
       cross_full_kernel<true><<<ggrid, kFullThreads, 0, st>>>(
-          rv.tbox, rv.theta, tsum, d_full, fbeg, fend, fchunk, (unsigned)srank, (unsigned)sworld,
-          m, ideal, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
+          rv.tbox, rv.theta, tsum, tsort, tpre, d_full, fbeg, fend, fchunk, (unsigned)srank,
+          (unsigned)sworld, m, ideal, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
       GLR_LAUNCHED("cross_full_kernel<angle>");
     } else {
       cross_full_kernel<false><<<ggrid, kFullThreads, 0, st>>>(
-          rv.tbox, rv.theta, nullptr, d_full, fbeg, fend, fchunk, (unsigned)srank,
-          (unsigned)sworld, m, 0.0, cc + cgrid, xa + (size_t)(cgrid + xgrid) * kAccWords);
+          rv.tbox, rv.theta, nullptr, nullptr, nullptr, d_full, fbeg, fend, fchunk,
+          (unsigned)srank, (unsigned)sworld, m, 0.0, cc + cgrid,
+          xa + (size_t)(cgrid + xgrid) * kAccWords);
       GLR_LAUNCHED("cross_full_kernel");
     }
   }
@@ -2822,14 +2945,17 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
       constexpr int kNT = kSubJ < 32 ? 32 : kSubJ;
       sub_stat_kernel<<<(unsigned)(m_pad / kNT), kNT, 0, st>>>(rv.theta, m, sstat);
       GLR_LAUNCHED("sub_stat_kernel");
+      theta_sort_kernel<kSubJ><<<(unsigned)(m_pad / kSubJ), kSubJ, 0, st>>>(rv.theta, m, qsort,
+                                                                            qpre);
+      GLR_LAUNCHED("theta_sort_kernel<sub>");
       cross_subfull_kernel<true><<<sgrid, kSubfullThreads, 0, st>>>(
           rv.hdr, filter_ok_s, d_list, d_sub, ubeg, uend, chunk_s, (unsigned)srank,
-          (unsigned)sworld, m, rv.theta, sstat, ideal, scc, sxa);
+          (unsigned)sworld, m, rv.theta, sstat, qsort, qpre, ideal, scc, sxa);
       GLR_LAUNCHED("cross_subfull_kernel<angle>");
     } else {
       cross_subfull_kernel<false><<<sgrid, kSubfullThreads, 0, st>>>(
           rv.hdr, filter_ok_s, d_list, d_sub, ubeg, uend, chunk_s, (unsigned)srank,
-          (unsigned)sworld, m, rv.theta, nullptr, 0.0, scc, sxa);
+          (unsigned)sworld, m, rv.theta, nullptr, nullptr, nullptr, 0.0, scc, sxa);
       GLR_LAUNCHED("cross_subfull_kernel");
     }
   }

@@ -216,7 +216,10 @@ __global__ void edge_box_keys_kernel(const double2 *__restrict__ xy,
 #define GLR_XK 2
 #endif
 constexpr int kKdTile = GLR_XTHREADS * GLR_XK;  // crossing.cu's kTile
-constexpr int kKdLeaf = kKdTile / 4;            // crossing.cu's kSubJ (j-quarter)
+#ifndef GLR_XSUBQ
+#define GLR_XSUBQ 4
+#endif
+constexpr int kKdLeaf = kKdTile / GLR_XSUBQ;    // crossing.cu's kSubJ (j-quarter)
 // tuning / cross-check knob (glr_spatial_set_kd): 0 keeps the Morton order
 int &kd_flag() {
   static int f = 1;
