@@ -2102,10 +2102,12 @@ enum UnitClass { kUnitNone = 0, kUnitMixed = 1, kUnitFull = 2 };
 // one CTA of NB threads per block of NB consecutive edges (NB = kTile:
 // tiles; NB = kSubJ: the sub-blocks of the sub-unit masks)
 template <int NB>
-__global__ void __launch_bounds__(NB) tile_pq_kernel(const EdgeRec *__restrict__ rec, int64_t m,
-                                                     PQBox *__restrict__ out) {
-  __shared__ double red[8][NB / 32];
-  const int64_t e = (int64_t)blockIdx.x * NB + threadIdx.x;
+__global__ void __launch_bounds__(NB < 32 ? 32 : NB)
+tile_pq_kernel(const EdgeRec *__restrict__ rec, int64_t m, PQBox *__restrict__ out) {
+  constexpr int kNT = NB < 32 ? 32 : NB;  // a warp holds 32 / NB blocks when NB < 32
+  constexpr int kW = NB < 32 ? NB : 32;   // lanes combined by shuffles
+  __shared__ double red[8][kNT / 32];
+  const int64_t e = (int64_t)blockIdx.x * kNT + threadIdx.x;
   // v[0..3]: -P.x, P.x, -P.y, P.y maxima; v[4..7] the same for Q
   double v[8];
 #pragma unroll
@@ -2120,15 +2122,25 @@ __global__ void __launch_bounds__(NB) tile_pq_kernel(const EdgeRec *__restrict__
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    for (int o = 16; o > 0; o >>= 1) v[i] = fmax(v[i], __shfl_down_sync(0xffffffffu, v[i], o));
+    for (int o = kW / 2; o > 0; o >>= 1)
+      v[i] = fmax(v[i], __shfl_down_sync(0xffffffffu, v[i], o, kW));
+  if (NB < 32) {
+    // even slots hold -min: negate back (an empty block gets lo = +inf, hi = -inf)
+    if (threadIdx.x % kW == 0) {
+      double *o = reinterpret_cast<double *>(out + (int64_t)blockIdx.x * (kNT / NB) +
+                                             threadIdx.x / kW);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (i & 1) ? v[i] : -v[i];
+    }
+    return;
+  }
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
     for (int i = 0; i < 8; ++i) red[i][threadIdx.x >> 5] = v[i];
   __syncthreads();
   if (threadIdx.x < 8) {
     double x = red[threadIdx.x][0];
-    for (int w = 1; w < NB / 32; ++w) x = fmax(x, red[threadIdx.x][w]);
-    // even slots hold -min: negate back (an empty tile gets lo = +inf, hi = -inf)
+    for (int w = 1; w < kNT / 32; ++w) x = fmax(x, red[threadIdx.x][w]);
     reinterpret_cast<double *>(out + blockIdx.x)[threadIdx.x] = (threadIdx.x & 1) ? x : -x;
   }
 }
@@ -3122,7 +3134,9 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
     if (d_sub != nullptr) {
       GLR_CUDA(cudaMemsetAsync(d_sub, 0, (size_t)(tot[0] + tot[1]) * sizeof(SubMask), st));
       if (tot[0] > 0) {
-        tile_pq_kernel<kSubJ><<<(unsigned)(m_pad / kSubJ), kSubJ, 0, st>>>(rv.rec, m, pqs);
+        constexpr int kPqThreads = kSubJ < 32 ? 32 : kSubJ;
+        tile_pq_kernel<kSubJ><<<(unsigned)(m_pad / kPqThreads), kPqThreads, 0, st>>>(rv.rec, m,
+                                                                                     pqs);
         GLR_LAUNCHED("tile_pq_kernel<sub>");
         sub_mask_kernel<<<blocks_for((int64_t)(tot[0] * kSubBits), 256, 16), 256, 0, st>>>(
             rv.hdr, d_list, tot[0], pqs, d_sub);
