@@ -48,11 +48,12 @@ STRATEGIES = ("auto", "dense", "culled")
 CULL_FRACTION = 0.25      # auto (occlusion): cull when candidates <= this share of tile pairs
 # auto (crossing): a culled unit costs about as much as a dense one (the
 # dense pass has the one-DADD angle in most units, the culled list does not,
-# but needs no band order); C5 keeps 54% of the tile pairs: 2.9 s vs 5.1 s
+# but needs no band order); C5 keeps 35% of the tile pairs as mixed units: 1.6 s vs 4.5 s
 CROSS_CULL_FRACTION = 0.75
-#: cost of a certified full unit (no predicate; closed form or FP64 deviations
-#: only) relative to a mixed one, for the auto decision and balanced shards
-FULL_UNIT_WEIGHT = 0.25
+#: cost of a certified full unit (no predicate; closed form or piecewise-linear
+#: sums over sorted angles) relative to a mixed one, for the auto decision and
+#: balanced shards (C5: 10.3 M full units in ~15 ms, 42.7 M mixed in ~1.4 s)
+FULL_UNIT_WEIGHT = 0.05
 AUTO_MIN_EDGES = 20_000   # auto: below this the dense pass is microseconds
 # theta order: vertices of at least this degree get their own edge group
 # (glr_theta_sort_edges; 0 = the library default).  Tuning knob only.

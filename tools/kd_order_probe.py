@@ -100,10 +100,15 @@ def run(dg, g, p, es, want, label, reps=2):
         sub = rec.sub[:rec.n_mixed].to(torch.int64)
         bits = sum(int(((sub >> k) & 1).sum().item()) for k in range(nbk))
         fbits = sum(int(((sub >> (nbk + k)) & 1).sum().item()) for k in range(nbk))
+        dec = (sub | (sub >> nbk)) & ((1 << nbk) - 1)
+        act = torch.zeros_like(dec)
+        for k in range(nbk):
+            act += 1 - ((dec >> k) & 1)
+        hist = torch.bincount(act, minlength=nbk + 1).tolist()
         ok = int(c) == want["ec"] and int(c0) == want["ec"] and abs(d - want["dev"]) <= 1e-9 * want["dev"]
         print(json.dumps({"order": label, "rep": r, "prep_class_ms": round(build * 1e3, 1),
                           "fused_ms": round(fused, 1), "ec_ms": round(ec, 1), "mixed": rec.n_mixed,
-                          "full": rec.n_full, "sub_none": bits, "sub_full": fbits, "sub_blocks": nbk * rec.n_mixed,
+                          "full": rec.n_full, "sub_none": bits, "sub_full": fbits, "sub_blocks": nbk * rec.n_mixed, "active_blocks_hist": hist,
                           "dense_units": M.crossing_units(g.num_edges), "golden_ok": ok}), flush=True)
         del rec
 
