@@ -1778,7 +1778,8 @@ __global__ void __launch_bounds__(kFixThreads)
 cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict__ rec,
                    const FTile *__restrict__ ftile, const JRec *__restrict__ jrec,
                    const TileBox *__restrict__ tbox, const double *__restrict__ theta,
-                   const int2 *__restrict__ ids, const int2 *__restrict__ ulist, uint64_t T,
+                   const int2 *__restrict__ ids, const int2 *__restrict__ ulist,
+                   const SubMask *__restrict__ usub, uint64_t T,
                    uint64_t W, uint64_t ubeg, uint64_t nbits, double ideal, double kappa,
                    int filter_ok, const unsigned *__restrict__ fixup,
                    unsigned long long *__restrict__ cta_acc) {
@@ -1837,11 +1838,21 @@ cross_fixup_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict_
                                                     ideal, kappa, rec, ids, theta, ibase, jbase,
                                                     wq, qn, qc);
       } else {
+        // the j-quarters the filter kernel skipped for this slice (certified
+        // empty, or full: cross_subfull_kernel owns those deviations)
+        unsigned skip = 0u;
+        if (usub != nullptr) {
+          const uint64_t sm = (uint64_t)usub[u];
+          skip = (unsigned)((sm | (sm >> kSubBits)) >> (kSubQuarters * slice)) & kSubQuarterMask;
+        }
+        for (int q = 0; q < kSubQuarters; ++q) {
+          if (skip & (1u << q)) continue;
 #pragma unroll 1
-        for (int jj = 0; jj < kTile; jj += kFilterBlock)
-          filter_block<true, false, kFilterBlock, 3>(R, th, jr, jth, jj, islot, thr, cnt, dev,
-                                                     A2, ideal, kappa, rec, ids, theta, ibase,
-                                                     jbase, wq, qn, qc);
+          for (int jj = q * kSubJ; jj < (q + 1) * kSubJ; jj += kFilterBlock)
+            filter_block<true, false, kFilterBlock, 3>(R, th, jr, jth, jj, islot, thr, cnt, dev,
+                                                       A2, ideal, kappa, rec, ids, theta, ibase,
+                                                       jbase, wq, qn, qc);
+        }
       }
       if (qn != 0)
         drain_queue<true>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
@@ -2996,8 +3007,8 @@ int crossing_pairs(const void *d_records, int64_t n, int64_t m, int with_angle, 
             sb, se, chunk, r, g, ideal, kappa, filter_ok, cc, xa, fix);
         GLR_LAUNCHED("cross_filter_kernel<angle>");
         cross_fixup_kernel<<<xgrid, kFixThreads, 0, st>>>(
-            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, T, W, sb, nbits,
-            ideal, kappa, filter_ok, fix, xa + (size_t)cgrid * kAccWords);
+            rv.hdr, rv.rec, rv.ftile, rv.jrec, rv.tbox, rv.theta, rv.ids, d_list, d_sub, T, W, sb,
+            nbits, ideal, kappa, filter_ok, fix, xa + (size_t)cgrid * kAccWords);
         GLR_LAUNCHED("cross_fixup_kernel");
       }
       adj_kernel<true><<<agrid, kAdjTile, 0, st>>>(rv.hdr, rv.theta, rv.inc, rv.offs, rv.wofs,

@@ -126,3 +126,40 @@ def test_large_and_small_terms_mixed(gpu):
     c, d = G._crossing_scan(g, ideal)
     assert c == c_ref == 8
     assert abs(d - d_ref) <= 1e-12 * d_ref
+
+
+def full_grid(h: int = 600, v: int = 600):
+    """h horizontal edges crossing v vertical ones everywhere (h * v crossings
+    at the angle fl(pi/2), every theta exactly 0 or fl(pi/2)): in the culled
+    plan most of them sit in certified-full units and blocks, whose
+    deviations come from closed forms or piecewise-linear sums
+    (cross_full_kernel / cross_subfull_kernel) unless the mean is small."""
+    L = 2.0**12
+    xy, pairs = [], []
+    for i in range(h):
+        base = len(xy)
+        xy += [(0.0, 1.0 + i), (2.0 * L, 1.0 + i)]
+        pairs.append((base, base + 1))
+    for j in range(v):
+        base = len(xy)
+        xy += [(L / 2 + j, 0.0), (L / 2 + j, 2.0 * L)]
+        pairs.append((base, base + 1))
+    return xy, pairs
+
+
+@pytest.mark.parametrize("delta", [1e-12, 2.0**-30, 1e-5, 2.0**-12 * 0.9, 2.0**-12 * 1.1, 1e-3, 0.3])
+def test_full_units_small_and_large_deviations(gpu, delta):
+    """dev_sum of certified-full units at 1e-9 relative (no floor) from tiny
+    to ordinary deviations, on both sides of the per-pair fallback's
+    threshold (mean deviation 2^-12)."""
+    from paper_2411_09809_b200 import metrics as M
+
+    xy, pairs = full_grid()
+    g = _graph(xy, pairs)
+    ideal = HALF_PI - delta
+    c, d, d_ref = _check(g, ideal, "culled")
+    assert c == 600 * 600
+    rec = M.CrossingRecords(M.DeviceGraph.from_graph(g), "culled")
+    assert rec.n_full > 0
+    if delta < 2.0**-13:
+        assert d == d_ref  # per-pair fallback: every term exact, exact accumulation
