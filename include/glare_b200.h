@@ -228,6 +228,16 @@ int glr_crossing_pairs_list(const void *d_records, int64_t n, int64_t m,
 int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t m,
                                        void *d_list, void *d_sub, uint64_t capacity,
                                        uint64_t *h_counts, void *stream);
+/* The same list restricted to the tile rows ti = rank (mod world): rank's
+ * share of the classified plan when the ROWS are dealt to the ranks, so that
+ * each rank classifies only its own rows (the plan build shards with the
+ * pass; no rank ever holds the whole list).  The world lists partition the
+ * full list; each rank scans its own with glr_crossing_pairs_classified as
+ * rank 0 of 1 and the partials sum to the dense result
+ * (glr_allreduce_sum_f64 or any allreduce). */
+int glr_crossing_candidates_rows(const void *d_records, int64_t n, int64_t m,
+                                 void *d_list, void *d_sub, uint64_t capacity,
+                                 uint64_t *h_counts, int rank, int world, void *stream);
 /* Layout of d_sub: bytes per mask (2, 4 or 8) and j-quarters per tile. */
 int glr_crossing_sub_mask_bytes(void);
 int glr_crossing_sub_quarters(void);

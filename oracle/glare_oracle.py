@@ -389,6 +389,18 @@ def crossing_scan_interleaved(xy, edges, ideal, tile: int, rank: int, world: int
     return total, dev
 
 
+def crossing_scan_rows(xy, edges, ideal, tile: int, rank: int, world: int):
+    """(count, dev_sum) of the tile pairs (ti <= tj) whose row ti = rank (mod
+    world): row ownership of the culled plan (glr_crossing_candidates_rows --
+    the ranks' lists partition the classified list by rows, and the dropped
+    tile pairs hold no crossing, so the ranks' shares partition the dense
+    triangle the same way)."""
+    m = len(edges)
+    T = max(1, -(-m // tile))
+    pairs = [(ti, tj) for ti in range(rank, T, world) for tj in range(ti, T)]
+    return crossing_scan_tiles(xy, edges, ideal, tile, pairs)
+
+
 def node_occlusion_units(xy, r, tile: int, ubeg: int, uend: int) -> int:
     """Occluding pairs restricted to vertex tile-pair units [ubeg, uend)."""
     n = len(xy)

@@ -120,6 +120,11 @@ SIGNATURES = {
         [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p, _c.c_uint64,
          _c.POINTER(_c.c_uint64), _c.c_void_p],
     ),
+    "glr_crossing_candidates_rows": (
+        _c.c_int,
+        [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_void_p, _c.c_void_p, _c.c_uint64,
+         _c.POINTER(_c.c_uint64), _c.c_int, _c.c_int, _c.c_void_p],
+    ),
     "glr_crossing_pairs_classified": (
         _c.c_int,
         [_c.c_void_p, _c.c_int64, _c.c_int64, _c.c_int, _c.c_double, _c.c_void_p, _c.c_void_p,

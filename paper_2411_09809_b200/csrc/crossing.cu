@@ -2271,13 +2271,20 @@ constexpr int kClassThreads = 256;
 template <bool FILL>
 __global__ void __launch_bounds__(kClassThreads)
 tile_class_kernel(const RecHeader *__restrict__ hdr, const int4 *__restrict__ box,
-                  const PQBox *__restrict__ pq, int64_t T,
+                  const PQBox *__restrict__ pq, int64_t T, int row_rank, int row_world,
                   unsigned long long *__restrict__ cnt_m, unsigned long long *__restrict__ cnt_f,
                   const unsigned long long *__restrict__ off_m,
                   const unsigned long long *__restrict__ off_f, int2 *__restrict__ list) {
   constexpr int kWarps = kClassThreads / 32;
   __shared__ unsigned wm[kWarps], wf[kWarps];
   const int64_t ti = blockIdx.x;
+  if (ti % row_world != row_rank) {  // another rank's row (glr_crossing_candidates_rows)
+    if (!FILL && threadIdx.x == 0) {
+      cnt_m[ti] = 0;
+      cnt_f[ti] = 0;
+    }
+    return;
+  }
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool classify = hdr->admissible != 0;
   const int4 a = box[ti];
@@ -3087,8 +3094,9 @@ int crossing_candidates(const void *d_records, int64_t n, int64_t m, int2 *d_lis
 // each part row-major; none-certified units are dropped.
 int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, int2 *d_list,
                                    SubMask *d_sub, uint64_t capacity, uint64_t *h_counts,
-                                   cudaStream_t st) {
-  if (d_records == nullptr || h_counts == nullptr || m < 0 || n < 0) {
+                                   cudaStream_t st, int row_rank = 0, int row_world = 1) {
+  if (d_records == nullptr || h_counts == nullptr || m < 0 || n < 0 || row_world < 1 ||
+      row_rank < 0 || row_rank >= row_world) {
     set_error("glr_crossing_candidates_classified: invalid arguments");
     return GLR_EARG;
   }
@@ -3120,9 +3128,8 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
   GLR_LAUNCHED("tile_pq_kernel");
   GLR_CUDA(cudaMemsetAsync(cnt_m + T, 0, sizeof(unsigned long long), st));
   GLR_CUDA(cudaMemsetAsync(cnt_f + T, 0, sizeof(unsigned long long), st));
-  tile_class_kernel<false><<<(unsigned)T, kClassThreads, 0, st>>>(rv.hdr, box, pq, T, cnt_m,
-                                                                   cnt_f, nullptr, nullptr,
-                                                                   nullptr);
+  tile_class_kernel<false><<<(unsigned)T, kClassThreads, 0, st>>>(
+      rv.hdr, box, pq, T, row_rank, row_world, cnt_m, cnt_f, nullptr, nullptr, nullptr);
   GLR_LAUNCHED("tile_class_kernel<count>");
   size_t tb = t_scan;
   GLR_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt_m, off_m, (int)(T + 1), st));
@@ -3139,8 +3146,8 @@ int crossing_candidates_classified(const void *d_records, int64_t n, int64_t m, 
   h_counts[0] = tot[0];
   h_counts[1] = tot[1];
   if (d_list != nullptr && capacity >= tot[0] + tot[1] && tot[0] + tot[1] > 0) {
-    tile_class_kernel<true><<<(unsigned)T, kClassThreads, 0, st>>>(rv.hdr, box, pq, T, nullptr,
-                                                                    nullptr, off_m, off_f, d_list);
+    tile_class_kernel<true><<<(unsigned)T, kClassThreads, 0, st>>>(
+        rv.hdr, box, pq, T, row_rank, row_world, nullptr, nullptr, off_m, off_f, d_list);
     GLR_LAUNCHED("tile_class_kernel<fill>");
     if (d_sub != nullptr) {
       GLR_CUDA(cudaMemsetAsync(d_sub, 0, (size_t)(tot[0] + tot[1]) * sizeof(SubMask), st));
@@ -3241,6 +3248,14 @@ int glr_crossing_candidates_classified(const void *d_records, int64_t n, int64_t
   return glr::crossing_candidates_classified(d_records, n, m, reinterpret_cast<int2 *>(d_list),
                                              reinterpret_cast<glr::SubMask *>(d_sub), capacity,
                                              h_counts, glr::as_stream(stream));
+}
+
+int glr_crossing_candidates_rows(const void *d_records, int64_t n, int64_t m, void *d_list,
+                                 void *d_sub, uint64_t capacity, uint64_t *h_counts, int rank,
+                                 int world, void *stream) {
+  return glr::crossing_candidates_classified(d_records, n, m, reinterpret_cast<int2 *>(d_list),
+                                             reinterpret_cast<glr::SubMask *>(d_sub), capacity,
+                                             h_counts, glr::as_stream(stream), rank, world);
 }
 
 int glr_crossing_pairs_classified(const void *d_records, int64_t n, int64_t m, int with_angle,

@@ -125,23 +125,39 @@ def _check_strategy(strategy: str) -> str:
     return strategy
 
 
-def _classified_candidates(buf: torch.Tensor, n: int, m: int):
-    """glr_crossing_candidates_classified: ([mixed | full] list, sub-unit
-    masks, mixed, full)."""
+def _classified_candidates(buf: torch.Tensor, n: int, m: int, rows: tuple[int, int] | None = None):
+    """glr_crossing_candidates_classified / _rows: ([mixed | full] list,
+    sub-unit masks, mixed, full); ``rows = (rank, world)`` keeps the tile rows
+    ti = rank (mod world) only."""
     L = _lib.lib()
+    rank, world = rows if rows is not None else (0, 1)
     counts = (ctypes.c_uint64 * 2)()
-    _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, None, None, 0, counts,
-                                                    _stream()),
-               "glr_crossing_candidates_classified")
+    _lib.check(L.glr_crossing_candidates_rows(_ptr(buf), n, m, None, None, 0, counts, rank, world,
+                                              _stream()),
+               "glr_crossing_candidates_rows")
     mixed, full = int(counts[0]), int(counts[1])
     lst = torch.empty((max(mixed + full, 1), 2), dtype=torch.int32, device=buf.device)
     sub_dtype = {2: torch.int16, 4: torch.int32, 8: torch.int64}[L.glr_crossing_sub_mask_bytes()]
     sub = torch.zeros(max(mixed + full, 1), dtype=sub_dtype, device=buf.device)
     if mixed + full:
-        _lib.check(L.glr_crossing_candidates_classified(_ptr(buf), n, m, _ptr(lst), _ptr(sub),
-                                                        mixed + full, counts, _stream()),
-                   "glr_crossing_candidates_classified")
+        _lib.check(L.glr_crossing_candidates_rows(_ptr(buf), n, m, _ptr(lst), _ptr(sub),
+                                                  mixed + full, counts, rank, world, _stream()),
+                   "glr_crossing_candidates_rows")
     return lst[:mixed + full], sub, mixed, full
+
+
+def _global_cost(cost: float, world: int, device) -> float:
+    """Sum of the ranks' plan costs (torch.distributed when initialised;
+    otherwise this rank's cost times world -- single-process callers that
+    walk the ranks one after the other should name the strategy instead of
+    "auto", since their estimates may differ near the threshold)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() == world:
+        t = torch.tensor([cost], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+    return cost * world
 
 
 def _candidates(fn, *args) -> torch.Tensor:
@@ -250,14 +266,19 @@ class CrossingRecords:
 
     ORDERS = ("input", "theta")
 
-    def __init__(self, dg: DeviceGraph, strategy: str = "dense", order: str = "input"):
+    def __init__(self, dg: DeviceGraph, strategy: str = "dense", order: str = "input",
+                 rows: tuple[int, int] | None = None):
         strategy = _check_strategy(strategy)
         if order not in self.ORDERS:
             raise ParameterError(f"order must be one of {self.ORDERS}, got {order!r}")
+        if rows is not None and not (rows[1] >= 1 and 0 <= rows[0] < rows[1]):
+            raise ParameterError(f"rows must be (rank, world) with 0 <= rank < world, got {rows!r}")
         self.m = dg.num_edges
         self.n = dg.num_vertices
         self.list = self.sub = None
         self.n_mixed = self.n_full = 0
+        #: (rank, world) when a culled plan holds only this rank's tile rows
+        self.rows = None
         if strategy != "dense" and self.m >= 2 and (strategy == "culled"
                                                     or self.m >= AUTO_MIN_EDGES):
             L = _lib.lib()
@@ -266,10 +287,16 @@ class CrossingRecords:
                                                 _ptr(es), _stream()),
                        "glr_spatial_sort_edges")
             self._prepare(dg.xy, es)
-            lst, sub, mixed, full = _classified_candidates(self.buf, self.n, self.m)
+            if rows is not None and rows[1] == 1:
+                rows = None
+            lst, sub, mixed, full = _classified_candidates(self.buf, self.n, self.m, rows)
             cost = mixed + FULL_UNIT_WEIGHT * full
+            if rows is not None:
+                # every rank must take the same decision: sum the ranks' costs
+                cost = _global_cost(cost, rows[1], self.buf.device)
             if strategy == "culled" or cost <= CROSS_CULL_FRACTION * crossing_units(self.m):
                 self.list, self.sub, self.n_mixed, self.n_full = lst, sub, mixed, full
+                self.rows = rows
                 return
             if order == "input":
                 # auto chose the dense pass: results never depend on the edge
@@ -336,6 +363,12 @@ class CrossingRecords:
         if out is None:
             out = torch.empty(2, dtype=torch.float64, device=self.buf.device)
         if self.culled:
+            if self.rows is not None:
+                # the plan already holds this rank's rows only: scan all of it
+                if (int(rank), int(world)) != tuple(self.rows):
+                    raise ParameterError(
+                        f"plan built for rows {self.rows}, asked for rank {rank} of {world}")
+                rank, world = 0, 1
             if len(self.list) == 0:
                 return out.zero_()
             rc = _lib.lib().glr_crossing_pairs_classified(

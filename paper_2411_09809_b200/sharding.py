@@ -69,8 +69,11 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
     """Compute this rank's partial (count, dev_sum, occlusions) on the current
     CUDA device into a device float64[3] tensor and allreduce it.  Returns the
     tensor (summed over ranks); no host synchronisation.  ``strategy`` as in
-    metrics (dense unit triangle or culled candidate list); every rank builds
-    the same plan, so the unit spaces agree."""
+    metrics (dense unit triangle or culled candidate list).  Dense: every rank
+    holds the same unit triangle and takes interleaved chunks of it.  Culled:
+    rank g classifies and scans the tile rows ti = g (mod world) of the
+    classified list (``CrossingRecords(rows=...)``); with ``"auto"`` the ranks
+    agree on the strategy through one small allreduce of their plan costs."""
     import torch
 
     from . import metrics as M
@@ -80,8 +83,11 @@ def sharded_evaluate(dg, radius: float | None, ideal: float | None, rank: int, w
     else:
         out.zero_()
     if with_crossing and dg.num_edges >= 2:
+        # culled plans are dealt to the ranks by tile rows, so the plan build
+        # (classes, masks) shards with the pass; dense passes by unit chunks
         rec = records if records is not None else M.CrossingRecords(
-            dg, strategy, "input" if ideal is None else "theta")
+            dg, strategy, "input" if ideal is None else "theta",
+            rows=(rank, world) if world > 1 else None)
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
     if radius is not None and dg.num_vertices >= 2:
         plan = M.OcclusionPlan(dg, radius, strategy)

@@ -318,3 +318,36 @@ def test_sub_full_blocks_cross_everywhere(plan):
         gc, gd = rec.partial(IDEAL, int(u), int(u) + 1).tolist()
         assert int(gc) == oc and strict_close(gd, od), (name, u, gc, oc)
         assert int(rec.partial(None, int(u), int(u) + 1)[0].item()) == oc
+
+
+def test_row_dealt_plans_partition_the_list(plan):
+    """glr_crossing_candidates_rows: the ranks' lists partition the full
+    classified list by tile row, each rank's partial equals the oracle's
+    share of those rows, and the partials sum to the whole."""
+    from oracle import glare_oracle as O
+    from paper_2411_09809_b200 import _lib, metrics as M
+
+    name, g, dg, rec, edges = plan
+    tile = _lib.lib().glr_crossing_tile()
+    whole = rec.partial(IDEAL, 0, rec.units).tolist()
+    full_list = {(int(a), int(b)) for a, b in rec.list.cpu().numpy()}
+    for world in (2, 3, 8):
+        seen = set()
+        cs, ds = 0, 0.0
+        for r in range(world):
+            part = M.CrossingRecords(dg, "culled", rows=(r, world))
+            assert part.rows == (r, world)
+            lst = {(int(a), int(b)) for a, b in part.list.cpu().numpy()} if part.units else set()
+            assert all(a % world == r for a, _ in lst)
+            assert not (seen & lst)
+            seen |= lst
+            pc, pd = part.partial_interleaved(IDEAL, r, world).tolist()
+            if g.num_edges <= 20000 and world == 3:
+                oc, od = O.crossing_scan_rows(g.xy, edges, IDEAL, tile, r, world)
+                assert int(pc) == oc and strict_close(pd, od), (name, world, r)
+            cs += int(pc)
+            ds += pd
+            with pytest.raises(Exception):
+                part.partial_interleaved(IDEAL, (r + 1) % world, world)
+        assert seen == full_list, (name, world)
+        assert cs == int(whole[0]) and strict_close(ds, whole[1]), (name, world)

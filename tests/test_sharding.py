@@ -93,6 +93,73 @@ def test_gloo_world2_partials_sum_to_oracle():
         assert ro == occ == 9588
 
 
+def _rows_worker(rank, world, port, q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import cases
+        from conftest import graph_from
+        from oracle import glare_oracle as O
+        from paper_2411_09809_b200 import metrics as M
+
+        g = graph_from(cases.lattice_stress)
+        # row ownership of the culled plan (32-edge tiles: 188 rows to deal)
+        c, d = O.crossing_scan_rows(g.xy, g.edges, IDEAL, 32, rank, world)
+        buf = torch.tensor([float(c), d, 0.0], dtype=torch.float64)
+        sharding.allreduce_partials(buf)
+        # the ranks' agreement on "auto": the summed plan cost is the same everywhere
+        cost = M._global_cost(100.0 + rank, world, torch.device("cpu"))
+        q.put((rank, buf.tolist(), cost))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_row_ownership_sums_to_oracle():
+    """Culled plans deal tile ROWS to the ranks (sharding.sharded_evaluate,
+    glr_crossing_candidates_rows): the oracle's restatement of that rule over
+    two gloo ranks gives the whole result, and both ranks see one plan cost."""
+    import cases
+    from conftest import graph_from
+    from oracle import glare_oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = {r: (b, c) for r, b, c in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = graph_from(cases.lattice_stress)
+    c, d = O.crossing_scan(g.xy, g.edges, IDEAL)
+    for rank in (0, 1):
+        (rc, rd, _), cost = results[rank]
+        assert rc == c == 4194903
+        assert abs(rd - d) <= 1e-9 * abs(d)
+        assert cost == 201.0
+
+
+def test_row_ownership_partitions_the_triangle():
+    from oracle import glare_oracle as O
+
+    rng = np.random.default_rng(4)
+    xy = rng.integers(0, 64, (300, 2)).astype(np.float64)
+    e = rng.integers(0, 300, (700, 2))
+    e = e[np.any(xy[e[:, 0]] != xy[e[:, 1]], axis=1)]
+    want = O.crossing_scan(xy, e, IDEAL)
+    for world in (1, 2, 3, 8):
+        parts = [O.crossing_scan_rows(xy, e, IDEAL, 64, r, world) for r in range(world)]
+        assert sum(p[0] for p in parts) == want[0]
+        assert abs(sum(p[1] for p in parts) - want[1]) <= 1e-9 * want[1]
+
+
 def test_balanced_triangle_and_weighted_ranges():
     rng = np.random.default_rng(0)
     for T in (1, 2, 7, 60):
