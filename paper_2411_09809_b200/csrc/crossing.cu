@@ -2439,6 +2439,8 @@ cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ t
   __shared__ double sth[ANGLE ? kTile : 1], spre[ANGLE ? kTile : 1];
   __shared__ double red[kWarps];
   __shared__ int per_pair;
+  __shared__ int wneed[kWarps];
+  __shared__ int2 todo[ANGLE ? kFullThreads : 1];
   __shared__ unsigned long long wacc[ANGLE ? kWarps : 1][ANGLE ? kAccWords : 1];
   const unsigned lane = threadIdx.x & 31;
   const int warp = (int)(threadIdx.x >> 5);
@@ -2452,65 +2454,96 @@ cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ t
   __syncthreads();
   const bool shift_ok = ANGLE && ideal >= 0x1p-100;
   unsigned long long total = 0;
-  for (uint64_t uq = 0;; ++uq) {
-    uint64_t ti, tj;
-    if (!cu.at(uq, &ti, &tj)) break;
-    const int64_t ra = m - (int64_t)ti * kTile, rb = m - (int64_t)tj * kTile;
-    const int na = (int)(ra < kTile ? ra : kTile), nb = (int)(rb < kTile ? rb : kTile);
-    if (threadIdx.x == 0) total += (unsigned long long)na * (unsigned long long)nb;
+  // Batches of kFullThreads units.  Phase 1: thread t looks at unit uq0 + t
+  // -- its pair count, and its deviation sum if the closed form applies
+  // (warp sums go to the exact accumulators).  Phase 2: the other units are
+  // compacted into shared memory and taken one at a time by the whole CTA.
+  for (uint64_t uq0 = 0;; uq0 += kFullThreads) {
+    uint64_t ti = 0, tj = 0;
+    const bool valid = cu.at(uq0 + threadIdx.x, &ti, &tj);
+    if (!__syncthreads_or(valid ? 1 : 0)) break;  // also orders the reuse of todo[]
+    bool need = false;
+    double cf = 0.0;
+    if (valid) {
+      const int64_t ra = m - (int64_t)ti * kTile, rb = m - (int64_t)tj * kTile;
+      const int na = (int)(ra < kTile ? ra : kTile), nb = (int)(rb < kTile ? rb : kTile);
+      total += (unsigned long long)na * (unsigned long long)nb;
+      if (ANGLE) {
+        const TileBox bi = tbox[ti], bj = tbox[tj];
+        double sh = 0.0, sigma = 1.0;
+        if (shift_ok && unit_shift(bi, bj, ideal, &sh, &sigma) == 1) {
+          const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)na, tsum[tj]),
+                                                       __dmul_rn((double)nb, tsum[ti])),
+                                             __dmul_rn((double)na * (double)nb, sh));
+          cf = v > 0.0 ? v : 0.0;
+        } else {
+          need = true;
+        }
+      }
+    }
     if (!ANGLE) continue;
-    const TileBox bi = tbox[ti], bj = tbox[tj];
-    double sh = 0.0, sigma = 1.0;
-    if (shift_ok && unit_shift(bi, bj, ideal, &sh, &sigma) == 1) {
-      if (threadIdx.x == 0) {
-        const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)na, tsum[tj]),
-                                                     __dmul_rn((double)nb, tsum[ti])),
-                                           __dmul_rn((double)na * (double)nb, sh));
-        xacc_add(wacc[0], v > 0.0 ? v : 0.0);
-      }
-      continue;
-    }
-    // piecewise-linear sums over the j-tile's sorted angles (piecewise_dev)
-    __syncthreads();  // the previous unit's angles are consumed
-    sth[threadIdx.x] = tsorted[(int64_t)tj * kTile + threadIdx.x];
-    spre[threadIdx.x] = tprefix[(int64_t)tj * kTile + threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) cf = __dadd_rn(cf, __shfl_down_sync(0xffffffffu, cf, o));
+    if (lane == 0 && cf > 0.0) xacc_add(wacc[warp], cf);
+    const unsigned bal = __ballot_sync(0xffffffffu, need);
+    if (lane == 0) wneed[warp] = __popc(bal);
     __syncthreads();
-    const double t = (int)threadIdx.x < na ? theta[(int64_t)ti * kTile + threadIdx.x] : 0.0;
-    {
-      const double tot = __dadd_rn(sth[nb - 1], spre[nb - 1]);
-      double d = (int)threadIdx.x < na ? piecewise_dev(t, sth, spre, nb, tot, ideal) : 0.0;
+    int off = 0, ntodo = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      if (w < warp) off += wneed[w];
+      ntodo += wneed[w];
+    }
+    if (need) todo[off + __popc(bal & ((1u << lane) - 1u))] = make_int2((int)ti, (int)tj);
+    __syncthreads();
+    for (int k = 0; k < ntodo; ++k) {
+      const int2 unit = todo[k];
+      const int64_t ra = m - (int64_t)unit.x * kTile, rb = m - (int64_t)unit.y * kTile;
+      const int na = (int)(ra < kTile ? ra : kTile), nb = (int)(rb < kTile ? rb : kTile);
+      // piecewise-linear sums over the j-tile's sorted angles (piecewise_dev)
+      __syncthreads();  // the previous unit's angles are consumed
+      sth[threadIdx.x] = tsorted[(int64_t)unit.y * kTile + threadIdx.x];
+      spre[threadIdx.x] = tprefix[(int64_t)unit.y * kTile + threadIdx.x];
+      __syncthreads();
+      const double t =
+          (int)threadIdx.x < na ? theta[(int64_t)unit.x * kTile + threadIdx.x] : 0.0;
+      {
+        const double tot = __dadd_rn(sth[nb - 1], spre[nb - 1]);
+        double d = (int)threadIdx.x < na ? piecewise_dev(t, sth, spre, nb, tot, ideal) : 0.0;
+        for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
+        if (lane == 0) red[warp] = d;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double v = 0.0;
+          for (int w = 0; w < kWarps; ++w) v = __dadd_rn(v, red[w]);
+          // small mean deviation: the per-pair formula below (bit-identical
+          // to numpy's for each pair) instead
+          per_pair = v < (double)na * (double)nb * kPiecewiseMeanDev ? 1 : 0;
+          if (!per_pair) xacc_add(wacc[0], v);
+        }
+        __syncthreads();
+      }
+      if (!per_pair) continue;
+      double d = 0.0;
+      if ((int)threadIdx.x < na) {
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= nb; j += 4) {
+          d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
+          d1 = __dadd_rn(d1, angle_dev(t, sth[j + 1], ideal));
+          d2 = __dadd_rn(d2, angle_dev(t, sth[j + 2], ideal));
+          d3 = __dadd_rn(d3, angle_dev(t, sth[j + 3], ideal));
+        }
+        for (; j < nb; ++j) d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
+        d = __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3));
+      }
       for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
-      if (lane == 0) red[warp] = d;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double v = 0.0;
-        for (int w = 0; w < kWarps; ++w) v = __dadd_rn(v, red[w]);
-        // small mean deviation: the per-pair formula below (bit-identical
-        // to numpy's for each pair) instead
-        per_pair = v < (double)na * (double)nb * kPiecewiseMeanDev ? 1 : 0;
-        if (!per_pair) xacc_add(wacc[0], v);
-      }
-      __syncthreads();
+      if (lane == 0) xacc_add(wacc[warp], d);
     }
-    if (!per_pair) continue;
-    double d = 0.0;
-    if ((int)threadIdx.x < na) {
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-      int j = 0;
-      for (; j + 4 <= nb; j += 4) {
-        d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
-        d1 = __dadd_rn(d1, angle_dev(t, sth[j + 1], ideal));
-        d2 = __dadd_rn(d2, angle_dev(t, sth[j + 2], ideal));
-        d3 = __dadd_rn(d3, angle_dev(t, sth[j + 3], ideal));
-      }
-      for (; j < nb; ++j) d0 = __dadd_rn(d0, angle_dev(t, sth[j], ideal));
-      d = __dadd_rn(__dadd_rn(d0, d1), __dadd_rn(d2, d3));
-    }
-    for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
-    if (lane == 0) xacc_add(wacc[warp], d);
   }
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_down_sync(0xffffffffu, total, o);
   __shared__ unsigned long long acc_cnt;
-  if (threadIdx.x == 0) acc_cnt = total;
+  if (threadIdx.x == 0) acc_cnt = 0;
+  __syncthreads();
+  if (lane == 0) atomicAdd(&acc_cnt, total);
   if (ANGLE && lane == 0) xacc_normalize(wacc[warp]);
   __syncthreads();
   if (threadIdx.x == 0) cta_cnt[blockIdx.x] += acc_cnt;
@@ -2618,23 +2651,22 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
     uint64_t fm = 0;
     if (mine < uend && ((mine - ubeg) / chunk) % sworld == srank)
       fm = ((uint64_t)usub[mine] >> kSubBits) & fullmask;
-    unsigned have = __ballot_sync(0xffffffffu, fm != 0);
-    while (have) {
-      const int src = __ffs(have) - 1;
-      have &= have - 1;
-      const uint64_t u = base + src;
-      uint64_t bits = __shfl_sync(0xffffffffu, fm, src);
-      const int2 p = ulist[u];
-      const int64_t ib = (int64_t)p.x * kTile, jb = (int64_t)p.y * kTile;
+    // Phase 1, one lane per unit: pair counts of its full blocks, and their
+    // deviation sums where the closed form applies (pm: the other blocks)
+    uint64_t pm = 0;
+    double cf = 0.0;
+    if (fm != 0) {
+      const int2 p = ulist[mine];
+      uint64_t bits = fm;
       while (bits) {
         const int b = __ffsll((long long)bits) - 1;
         bits &= bits - 1;
         const int sl = b / kSubQuarters, q = b % kSubQuarters;
-        const int64_t i0 = ib + (int64_t)sl * kSliceEdges, j0 = jb + (int64_t)q * kSubJ;
-        const int64_t ri = m - i0, rj = m - j0;
+        const int64_t ri = m - ((int64_t)p.x * kTile + (int64_t)sl * kSliceEdges);
+        const int64_t rj = m - ((int64_t)p.y * kTile + (int64_t)q * kSubJ);
         const int ni = (int)(ri < 0 ? 0 : ri < kSliceEdges ? ri : kSliceEdges);
         const int nj = (int)(rj < 0 ? 0 : rj < kSubJ ? rj : kSubJ);
-        if (lane == 0) total += (unsigned long long)ni * (unsigned long long)nj;
+        total += (unsigned long long)ni * (unsigned long long)nj;
         if (!ANGLE || ni == 0 || nj == 0) continue;
         const SubStat sj = sstat[(int64_t)p.y * kPer + q];
         float ilo = INFINITY, ihi = -INFINITY;
@@ -2648,14 +2680,35 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
         }
         double sh = 0.0, sigma = 1.0;
         if (shift_ok && range_shift(ilo, ihi, sj.thlo, sj.thhi, ideal, &sh, &sigma) == 1) {
-          if (lane == 0) {
-            const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)ni, sj.tsum),
-                                                         __dmul_rn((double)nj, isum)),
-                                               __dmul_rn((double)ni * (double)nj, sh));
-            xacc_add(wacc[warp], v > 0.0 ? v : 0.0);
-          }
-          continue;
+          const double v = sigma * __dsub_rn(__dsub_rn(__dmul_rn((double)ni, sj.tsum),
+                                                       __dmul_rn((double)nj, isum)),
+                                             __dmul_rn((double)ni * (double)nj, sh));
+          cf = __dadd_rn(cf, v > 0.0 ? v : 0.0);
+        } else {
+          pm |= 1ull << b;
         }
+      }
+    }
+    if (!ANGLE) continue;
+    for (int o = 16; o > 0; o >>= 1) cf = __dadd_rn(cf, __shfl_down_sync(0xffffffffu, cf, o));
+    if (lane == 0 && cf > 0.0) xacc_add(wacc[warp], cf);
+    // Phase 2, the warp per remaining block
+    unsigned have = __ballot_sync(0xffffffffu, pm != 0);
+    while (have) {
+      const int src = __ffs(have) - 1;
+      have &= have - 1;
+      const uint64_t u = base + src;
+      uint64_t bits = __shfl_sync(0xffffffffu, pm, src);
+      const int2 p = ulist[u];
+      const int64_t ib = (int64_t)p.x * kTile, jb = (int64_t)p.y * kTile;
+      while (bits) {
+        const int b = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        const int sl = b / kSubQuarters, q = b % kSubQuarters;
+        const int64_t i0 = ib + (int64_t)sl * kSliceEdges, j0 = jb + (int64_t)q * kSubJ;
+        const int64_t ri = m - i0, rj = m - j0;
+        const int ni = (int)(ri < kSliceEdges ? ri : kSliceEdges);
+        const int nj = (int)(rj < kSubJ ? rj : kSubJ);
         // lane l takes i-edges l, l + 32, ... of the slice: piecewise-linear
         // sums over the j-quarter's sorted angles (piecewise_dev), or the
         // per-pair formula when the block's mean deviation is small
@@ -2697,6 +2750,7 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
       }
     }
   }
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_down_sync(0xffffffffu, total, o);
   if (lane == 0) {
     atomicAdd(&acc_cnt, total);
     if (ANGLE) xacc_normalize(wacc[warp]);

@@ -77,7 +77,7 @@ def run(dg, g, p, es, want, label, reps=2):
     for r in range(reps):
         rec = M.CrossingRecords.__new__(M.CrossingRecords)
         rec.m, rec.n = dg.num_edges, dg.num_vertices
-        rec.list = rec.sub = None
+        rec.list = rec.sub = rec.rows = None
         torch.cuda.synchronize()
         t = time.perf_counter()
         rec._prepare(dg.xy, es)
