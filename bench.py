@@ -235,6 +235,20 @@ def _occ_roofline(rate, sm_mhz):
             "kernel": "occlusion_filter_kernel"}
 
 
+def _culled_filter(info, pass_ms, sm_mhz):
+    """Pairs the certified filter actually evaluates in the culled pass (the
+    blocks neither dropped nor counted whole) against the pass time -- a lower
+    bound of cross_filter_kernel's own rate (the pass also runs the full-unit
+    kernels, ~8% of it on C5) -- and the FMA-pipe fraction at that rate."""
+    if "blocks_filtered" not in info:
+        return None
+    pairs = info["blocks_filtered"] * info["block_pairs"]
+    rate = pairs / (pass_ms * 1e-3)
+    peak = FMA_LANES_PER_CLK_SM * 148 * sm_mhz * 1e6
+    return {"pairs": pairs, "pairs_per_s": rate, "fma_frac": FMA_PER_PAIR * rate / peak,
+            "kernel": "cross_filter_kernel<angle> over the mixed units"}
+
+
 def _config_desc(g, p, world):
     return {"workload": "C5: Chung-Lu gamma 2.3, 4,000,000 edges / 1,500,000 vertices on the "
                         "2^16 integer lattice (fp64); E_c + E_ca fused pass; N_c at r=8",
@@ -367,27 +381,48 @@ def main():
     occ_culled_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / args.steps)
     assert out[2].item() == occ_count, (out[2].item(), occ_count)
 
-    # ---- crossing, culled plan (4-D bbox Morton order + candidate tile
-    # pairs; what strategy="auto" runs on C5) -- effective rate, same result
-    def crossing_culled_step():
-        rec = M.CrossingRecords(dg, "culled")
+    # ---- crossing, culled plan (k-d order + classified tile pairs and
+    # blocks; what strategy="auto" runs on C5; tile rows dealt to the ranks
+    # for world > 1, as sharded_evaluate does) -- effective rate, same result
+    rows = (rank, world) if world > 1 else None
+    culled_pass = []
+
+    def crossing_culled_step(stats=False):
+        rec = M.CrossingRecords(dg, "culled", rows=rows)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
         rec.partial_interleaved(ideal, rank, world, out=out[0:2])
+        k1.record(stream)
         sharding.allreduce_partials(out[0:2])
-        units = (rec.units, rec.n_mixed, rec.n_full)
+        culled_pass.append((k0, k1))
+        info = {"units": rec.units, "mixed": rec.n_mixed, "full": rec.n_full}
+        if stats and rec.n_mixed:
+            q = L.glr_crossing_sub_quarters()
+            nb = (L.glr_crossing_tile() // 128) * q
+            sub = rec.sub[:rec.n_mixed].to(torch.int64)
+            none = sum(int(((sub >> k) & 1).sum().item()) for k in range(nb))
+            fullb = sum(int(((sub >> (nb + k)) & 1).sum().item()) for k in range(nb))
+            info.update(blocks_per_unit=nb, block_pairs=128 * (L.glr_crossing_tile() // q),
+                        blocks_none=none, blocks_full=fullb,
+                        blocks_filtered=nb * rec.n_mixed - none - fullb)
         del rec
-        return units
+        return info
 
     for _ in range(min(args.warmup, 1)):
         crossing_culled_step()
     barrier()
     torch.cuda.synchronize()
+    culled_pass.clear()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cross_units = crossing_culled_step()
+        cross_info = crossing_culled_step()
     torch.cuda.synchronize()
     barrier()
     cross_culled_ms = max_over_ranks(1e3 * (time.perf_counter() - t0) / args.steps)
+    cross_pass_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in culled_pass))
     assert out[0].item() == count, (out[0].item(), count)
+    cross_info = crossing_culled_step(stats=True)  # block statistics, untimed
+    cross_units = (cross_info["units"], cross_info["mixed"], cross_info["full"])
 
     # ---- fr_layout: repulsion pairs/s, rank 0 ----
     layout = None
@@ -498,14 +533,19 @@ def main():
                                          "candidate tile pairs (incl. plan build)"}},
         "crossing_culled": {"metric": "edge-pair crossing tests/s (E_c+E_ca fused), culled plan",
                             "value": P_E / (cross_culled_ms * 1e-3), "unit": "pairs/s",
-                            "ms_per_step": cross_culled_ms, "candidate_units": cross_units[0],
+                            "ms_per_step": cross_culled_ms, "pass_ms": cross_pass_ms,
+                            "candidate_units": cross_units[0],
                             "mixed_units": cross_units[1], "full_units": cross_units[2],
                             "dense_units": M.crossing_units(m),
+                            "blocks": {k: v for k, v in cross_info.items()
+                                       if k.startswith("block")},
+                            "filter": _culled_filter(cross_info, cross_pass_ms, sm_mhz),
                             "note": "effective rate (m(m-1)/2 / time): same count and sum, "
-                                    "(orientation, 4-D bbox Morton) order + classified tile "
-                                    "pairs -- certified-empty pairs dropped, certified-full "
-                                    "pairs counted without a predicate (incl. plan build); "
-                                    "the public API's strategy='auto' on C5"},
+                                    "(orientation, k-d tree over the endpoints) order + "
+                                    "classified tile pairs and slice x quarter blocks -- "
+                                    "certified-empty ones dropped, certified-full ones counted "
+                                    "without a predicate (incl. plan build); the public API's "
+                                    "strategy='auto' on C5; this rank's tile rows for N > 1"},
         "layout": layout,
         "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": peak_run,
                      "unit": "T lane-op/s (FP32 FFMA/FMUL on the FMA pipe)",
@@ -545,7 +585,8 @@ def main():
         "e2e": {"value": e2e_value, "unit": "pairs/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 3 * 8,
                 "strategy": "auto: what edge_crossing_angle(g) runs -- on C5 the culled plan "
-                            "(plan build included); the line's top-level value is the dense "
+                            "(k-d order, classified tile pairs and blocks; plan build "
+                            "included); the line's top-level value is the dense "
                             "theta-ordered pass, device-resident"},
         "gpu_launches": launches,
         "clocks": clk,
