@@ -158,8 +158,8 @@ int glr_crossing_tile_weights(const void *d_records, int64_t n, int64_t m,
  * edges (mean bbox half-perimeter >= 1/32 of the domain's): (hub group,
  * diagonal orientation), then a balanced k-d tree over the endpoints (P.x,
  * P.y, Q.x, Q.y) whose cells are the 256-edge tiles, 128-edge warp slices and
- * 64-edge quarters (spatial.cu); one 8-byte read back decides between the
- * two, so the call synchronises the stream.  The metrics do not depend on
+ * 64-edge quarters (spatial.cu), from 131,072 edges on; one 8-byte read back
+ * decides between the two, so the call then synchronises the stream.  The metrics do not depend on
  * edge order (exact.py:145-222 visits every unordered pair once); compact
  * tiles let glr_crossing_candidates* skip or certify most tile pairs. */
 int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
@@ -180,8 +180,10 @@ int glr_theta_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges,
                          int64_t m, int64_t hub_degree, int64_t *d_edges_out, void *stream);
 
 /* Tuning / cross-check knob for glr_spatial_sort_edges: on = 0 keeps the
- * Morton order for long edges too, 1 (default) the k-d order, < 0 only
- * queries.  Returns the previous setting.  Results never depend on it. */
+ * Morton order for long edges too, 1 (default) takes the k-d order from
+ * 131,072 edges on (below that the tree's small launches cost more than the
+ * pass), 2 takes it for any size, < 0 only queries.  Returns the previous
+ * setting.  Results never depend on it. */
 int glr_spatial_set_kd(int on);
 
 /* Writes to d_xy_out the vertex positions reordered by Morton code (node

@@ -2162,20 +2162,35 @@ __device__ inline void orient_ranges(const PQBox &L, const PQBox &R, double (&lo
                                      double (&hi)[2]) {
   lo[0] = lo[1] = INFINITY;
   hi[0] = hi[1] = -INFINITY;
+  // Differences r - P for the two values of each P coordinate, hoisted out
+  // of the corner loop: u[k][y][0..1] = (ry0, ry1) - py, w[k][x][0..1] =
+  // (rx0, rx1) - px; u0 <= u1 and w0 <= w1 by monotone rounding.
   const double rb[2][4] = {{R.px0, R.px1, R.py0, R.py1}, {R.qx0, R.qx1, R.qy0, R.qy1}};
-#pragma unroll 1
+  double u[2][2][2], w[2][2][2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    u[k][0][0] = __dsub_rn(rb[k][2], L.py0); u[k][0][1] = __dsub_rn(rb[k][3], L.py0);
+    u[k][1][0] = __dsub_rn(rb[k][2], L.py1); u[k][1][1] = __dsub_rn(rb[k][3], L.py1);
+    w[k][0][0] = __dsub_rn(rb[k][0], L.px0); w[k][0][1] = __dsub_rn(rb[k][1], L.px0);
+    w[k][1][0] = __dsub_rn(rb[k][0], L.px1); w[k][1][1] = __dsub_rn(rb[k][1], L.px1);
+  }
+#pragma unroll
   for (int c = 0; c < 16; ++c) {
-    const double px = (c & 1) ? L.px1 : L.px0, py = (c & 2) ? L.py1 : L.py0;
+    const int xs = c & 1, ys = (c >> 1) & 1;
+    const double px = xs ? L.px1 : L.px0, py = ys ? L.py1 : L.py0;
     const double qx = (c & 4) ? L.qx1 : L.qx0, qy = (c & 8) ? L.qy1 : L.qy0;
     const double a = __dsub_rn(qx, px), b = __dsub_rn(qy, py);
+    // min / max of a product with an ordered pair is picked by the factor's
+    // sign (multiplication by a fixed factor is monotone under rounding):
+    // the same values as min(a u0, a u1) etc.
+    const bool an = a < 0.0, bn = b < 0.0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const double t1a = __dmul_rn(a, __dsub_rn(rb[k][2], py));
-      const double t1b = __dmul_rn(a, __dsub_rn(rb[k][3], py));
-      const double t2a = __dmul_rn(b, __dsub_rn(rb[k][0], px));
-      const double t2b = __dmul_rn(b, __dsub_rn(rb[k][1], px));
-      lo[k] = fmin(lo[k], __dsub_rn(fmin(t1a, t1b), fmax(t2a, t2b)));
-      hi[k] = fmax(hi[k], __dsub_rn(fmax(t1a, t1b), fmin(t2a, t2b)));
+      const double u0 = u[k][ys][0], u1 = u[k][ys][1], w0 = w[k][xs][0], w1 = w[k][xs][1];
+      const double t1lo = __dmul_rn(a, an ? u1 : u0), t1hi = __dmul_rn(a, an ? u0 : u1);
+      const double t2lo = __dmul_rn(b, bn ? w1 : w0), t2hi = __dmul_rn(b, bn ? w0 : w1);
+      lo[k] = fmin(lo[k], __dsub_rn(t1lo, t2hi));
+      hi[k] = fmax(hi[k], __dsub_rn(t1hi, t2lo));
     }
   }
 }

@@ -220,12 +220,19 @@ constexpr int kKdTile = GLR_XTHREADS * GLR_XK;  // crossing.cu's kTile
 #define GLR_XSUBQ 4
 #endif
 constexpr int kKdLeaf = kKdTile / GLR_XSUBQ;    // crossing.cu's kSubJ (j-quarter)
-// tuning / cross-check knob (glr_spatial_set_kd): 0 keeps the Morton order
+// tuning / cross-check knob (glr_spatial_set_kd): 0 keeps the Morton order,
+// 1 (default) builds the tree from kKdMinEdges edges on -- below that the
+// dense pass costs a millisecond or two and the tree's ~1 ms of small
+// launches is not repaid (C2, 40k edges: auto 2.5 ms with it, 1.4 without)
+// -- 2 builds it for any size (tests)
+constexpr int64_t kKdMinEdges = (int64_t)1 << 17;
 int &kd_flag() {
   static int f = 1;
   return f;
 }
-inline bool kd_long_edges() { return kd_flag() != 0; }
+inline bool kd_long_edges(int64_t m) {
+  return kd_flag() == 2 || (kd_flag() == 1 && m >= kKdMinEdges);
+}
 
 __device__ inline unsigned quant32(double v, double lo, double scale) {
   double q = (v - lo) * scale;  // scale = (2^32 - 1) / (hi - lo), or 0 for a flat axis
@@ -686,9 +693,11 @@ int keyed_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
     // long edges take the k-d order (one 8-byte read back decides; the culled
     // plan synchronises for its candidate count anyway)
     unsigned long long lsum = 0;
-    GLR_CUDA(cudaMemcpyAsync(&lsum, b + 4, 8, cudaMemcpyDeviceToHost, st));
-    GLR_CUDA(cudaStreamSynchronize(st));
-    if (kd_long_edges() && lsum >= (unsigned long long)GLR_LONG_EDGE_EXTENT * (unsigned long long)m)
+    if (kd_long_edges(m)) {
+      GLR_CUDA(cudaMemcpyAsync(&lsum, b + 4, 8, cudaMemcpyDeviceToHost, st));
+      GLR_CUDA(cudaStreamSynchronize(st));
+    }
+    if (kd_long_edges(m) && lsum >= (unsigned long long)GLR_LONG_EDGE_EXTENT * (unsigned long long)m)
       return kd_sort(d_xy, n, d_edges, m, hub_degree, deg, b, d_out, st);
     edge_box_keys_kernel<<<grid_of(m), 256, 0, st>>>(reinterpret_cast<const double2 *>(d_xy), e2,
                                                      m, b, deg, hub_degree, b + 4, keys, idx);
@@ -738,7 +747,7 @@ int glr_spatial_sort_edges(const double *d_xy, int64_t n, const int64_t *d_edges
 
 int glr_spatial_set_kd(int on) {
   const int was = glr::kd_flag();
-  if (on >= 0) glr::kd_flag() = on ? 1 : 0;
+  if (on >= 0) glr::kd_flag() = on > 2 ? 1 : on;
   return was;
 }
 

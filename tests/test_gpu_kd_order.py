@@ -67,7 +67,7 @@ def _sort(dg, kd):
     from paper_2411_09809_b200 import _lib
 
     L = _lib.lib()
-    was = L.glr_spatial_set_kd(1 if kd else 0)
+    was = L.glr_spatial_set_kd(2 if kd else 0)
     try:
         es = torch.empty_like(dg.edges)
         rc = L.glr_spatial_sort_edges(dg.xy.data_ptr(), dg.num_vertices, dg.edges.data_ptr(),
@@ -147,7 +147,7 @@ def test_plans_on_kd_order_match_oracle(case):
     else:
         want_c, want_d = O.crossing_scan(g.xy, g.edges, IDEAL)
     L = _lib.lib()
-    for kd in (1, 0):
+    for kd in (2, 0):
         was = L.glr_spatial_set_kd(kd)
         try:
             rec = M.CrossingRecords(dg, "culled")
@@ -166,7 +166,7 @@ def test_kd_beats_morton_on_classification():
     dg = M.DeviceGraph.from_graph(g)
     L = _lib.lib()
     mixed = {}
-    for kd in (1, 0):
+    for kd in (2, 0):
         was = L.glr_spatial_set_kd(kd)
         try:
             rec = M.CrossingRecords(dg, "culled")
@@ -175,6 +175,29 @@ def test_kd_beats_morton_on_classification():
         finally:
             L.glr_spatial_set_kd(was)
         mixed[("res", kd)] = res
-    assert mixed[1] < mixed[0], mixed
-    assert mixed[("res", 1)][0] == mixed[("res", 0)][0]
-    assert strict_close(mixed[("res", 1)][1], mixed[("res", 0)][1])
+    assert mixed[2] < mixed[0], mixed
+    assert mixed[("res", 2)][0] == mixed[("res", 0)][0]
+    assert strict_close(mixed[("res", 2)][1], mixed[("res", 0)][1])
+
+
+def test_kd_default_threshold():
+    """Default setting: the tree is built from 131,072 edges on (the Morton
+    order below), and the knob reports its previous value."""
+    from paper_2411_09809_b200 import _lib, metrics as M
+
+    L = _lib.lib()
+    assert L.glr_spatial_set_kd(-1) == 1
+    small = M.DeviceGraph.from_graph(uniform(11, 3000, 20000))
+    big = M.DeviceGraph.from_graph(uniform(12, 60000, 140000))
+    import torch
+
+    def default_sort(dg):
+        es = torch.empty_like(dg.edges)
+        assert L.glr_spatial_sort_edges(dg.xy.data_ptr(), dg.num_vertices, dg.edges.data_ptr(),
+                                        dg.num_edges, es.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream) == 0
+        return es.cpu().numpy()
+
+    assert np.array_equal(default_sort(small), _sort(small, False))
+    assert np.array_equal(default_sort(big), _sort(big, True))
+    assert not np.array_equal(default_sort(big), _sort(big, False))

@@ -27,12 +27,15 @@ def pq(xy, edges):
     return np.concatenate([P, Q], axis=1)  # px py qx qy
 
 
-def kd_order(xy, edges, rule, groups=True, hub=HUB):
+def kd_order(xy, edges, rule, groups=True, hub=HUB, theta_w=0.0):
     m = len(edges)
     c = pq(xy, edges)
     ext = c.max(axis=0) - c.min(axis=0)
     ext[ext == 0] = 1.0
     cn = (c - c.min(axis=0)) / ext
+    if theta_w > 0:  # a fifth coordinate: the direction, weighted
+        th = np.mod(np.arctan2(c[:, 3] - c[:, 1], c[:, 2] - c[:, 0]), np.pi) / np.pi
+        cn = np.concatenate([cn, theta_w * th[:, None]], axis=1)
     up = ((c[:, 2] - c[:, 0]) * (c[:, 3] - c[:, 1]) >= 0).astype(np.int64)
     deg = np.bincount(edges.ravel(), minlength=len(xy))
     du, dv = deg[edges[:, 0]], deg[edges[:, 1]]
@@ -136,9 +139,11 @@ def main():
             import re
             global LEAF
             mleaf, mhub = re.search(r"leaf(\d+)", v), re.search(r"hub(\d+)", v)
+            mth = re.search(r"theta([0-9.]+)", v)
             LEAF = int(mleaf.group(1)) if mleaf else 64
             perm = kd_order(g.xy, g.edges, "cycle" if "cycle" in v else "extent",
-                            groups="nogrp" not in v, hub=int(mhub.group(1)) if mhub else HUB)
+                            groups="nogrp" not in v, hub=int(mhub.group(1)) if mhub else HUB,
+                            theta_w=float(mth.group(1)) if mth else 0.0)
             print(v, "host order s", round(time.perf_counter() - t, 1), flush=True)
             es = torch.from_numpy(np.ascontiguousarray(g.edges[perm])).to(dg.edges.device)
         run(dg, g, p, es, want, v)
