@@ -2398,26 +2398,36 @@ theta_sort_kernel(const double *__restrict__ theta, int64_t m, double *__restric
 // <= 256 angles); callers re-evaluate per pair when the mean deviation is
 // small (kPiecewiseMeanDev).
 constexpr double kPiecewiseMeanDev = 0x1p-12;
-__device__ inline int lower_bound_f64(const double *s, int n, double x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (s[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
+// NB: the block size (a power of two); s[n..NB) hold +inf, so the branchless
+// searches -- all seven advanced together, one shared-memory load each per
+// step -- never pass n.
+template <int NB>
 __device__ inline double piecewise_dev(double ti, const double *s, const double *pre, int n,
                                        double tot, double ideal) {
   const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
   const double pmi = __dsub_rn(PI, ideal);
   const double bp[7] = {-pmi, -HALF_PI, -ideal, 0.0, ideal, HALF_PI, pmi};
   const double c[8] = {-pmi, pmi, -ideal, ideal, ideal, -ideal, pmi, -pmi};
+  double x[7];
+  int pos[7];
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    x[p] = __dadd_rn(ti, bp[p]);
+    pos[p] = 0;
+  }
+#pragma unroll
+  for (int step = NB / 2; step >= 1; step >>= 1) {
+#pragma unroll
+    for (int p = 0; p < 7; ++p) pos[p] += s[pos[p] + step - 1] < x[p] ? step : 0;
+  }
+#pragma unroll
+  for (int p = 0; p < 7; ++p) pos[p] += s[pos[p]] < x[p] ? 1 : 0;  // pos <= NB - 1 here
   int a = 0;
   double pa = 0.0, acc = 0.0;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
-    const int b = p < 7 ? lower_bound_f64(s, n, __dadd_rn(ti, bp[p])) : n;
-    const int bb = b < a ? a : b;  // monotone whatever the roundings
+    const int b = p < 7 ? pos[p] : n;
+    const int bb = b < a ? a : (b > n ? n : b);  // monotone whatever the roundings
     const double pb = bb < n ? pre[bb] : tot;
     const double cnt = (double)(bb - a);
     const double lin = __dsub_rn(__dsub_rn(pb, pa), __dmul_rn(cnt, ti));
@@ -2522,7 +2532,7 @@ cross_full_kernel(const TileBox *__restrict__ tbox, const double *__restrict__ t
           (int)threadIdx.x < na ? theta[(int64_t)unit.x * kTile + threadIdx.x] : 0.0;
       {
         const double tot = __dadd_rn(sth[nb - 1], spre[nb - 1]);
-        double d = (int)threadIdx.x < na ? piecewise_dev(t, sth, spre, nb, tot, ideal) : 0.0;
+        double d = (int)threadIdx.x < na ? piecewise_dev<kTile>(t, sth, spre, nb, tot, ideal) : 0.0;
         for (int o = 16; o > 0; o >>= 1) d = __dadd_rn(d, __shfl_down_sync(0xffffffffu, d, o));
         if (lane == 0) red[warp] = d;
         __syncthreads();
@@ -2742,7 +2752,7 @@ cross_subfull_kernel(const RecHeader *__restrict__ hdr, int filter_ok,
 #pragma unroll
         for (int k = 0; k < kFK; ++k)
           if ((int)lane + 32 * k < ni)
-            ds = __dadd_rn(ds, piecewise_dev(ti[k], wsrt[warp], wpre[warp], nj, tot, ideal));
+            ds = __dadd_rn(ds, piecewise_dev<kSubJ>(ti[k], wsrt[warp], wpre[warp], nj, tot, ideal));
         for (int o = 16; o > 0; o >>= 1) ds = __dadd_rn(ds, __shfl_down_sync(0xffffffffu, ds, o));
         ds = __shfl_sync(0xffffffffu, ds, 0);
         if (ds < (double)ni * (double)nj * kPiecewiseMeanDev) {
