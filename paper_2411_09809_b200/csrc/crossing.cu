@@ -187,6 +187,10 @@ constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
 #ifndef GLR_XSUBQ
 #define GLR_XSUBQ 4
 #endif
+// one-kink angle form in the fused filter kernel (range_kink)
+#ifndef GLR_XKINK
+#define GLR_XKINK 1
+#endif
 constexpr int kSubQuarters = GLR_XSUBQ;
 constexpr int kSubJ = kTile / kSubQuarters;
 constexpr unsigned kSubQuarterMask = (kSubQuarters >= 32) ? 0xffffffffu : (1u << kSubQuarters) - 1u;
@@ -934,6 +938,46 @@ __device__ inline int unit_shift(const TileBox &a, const TileBox &b, double idea
   return range_shift(a.thlo, a.thhi, b.thlo, b.thhi, ideal, s, sigma);
 }
 
+// One-kink units.  The deviation f(dt) = |ideal - min(|dt|, pi - |dt|)| is
+// piecewise linear on (-pi, pi) with kinks at 0, +-ideal, +-pi/2, +-(pi -
+// ideal).  A unit whose dt range holds at most ONE kink beta and keeps
+// kSignMargin away from beta's two neighbours has, for every pair,
+//   f = |dt - beta|                    beta = +-ideal, +-(pi - ideal)
+//   f = f(beta) - |dt - beta|          beta = 0 (f(beta) = ideal), +-pi/2
+//                                      (f(beta) = pi/2 - ideal),
+// so with x_k = theta_i_k + beta a pair costs v = theta_j - x_k and |v| in
+// the accumulate (2 DADD instead of the general formula's 4), and the
+// second kind finishes as hits * f(beta) - sum |v| (every term f(beta) - |v|
+// >= kSignMargin: the cancellation costs < 2^-44 relative).  Rounding
+// differs from exact.py's by a few ulps of pi per pair; a slice whose mean
+// deviation per hit is below kFixupMeanDev is re-evaluated with the
+// reference formula like every fast-formula slice (cross_fixup_kernel).
+// Returns 1 and (*beta, *fbeta, *minus) or 0.
+__device__ inline int range_kink(float athlo, float athhi, float bthlo, float bthhi,
+                                 double ideal, double *beta, double *fbeta, int *minus) {
+  const double HALF_PI = 1.5707963267948966, PI = 3.141592653589793;
+  const double lo = (double)bthlo - (double)athhi, hi = (double)bthhi - (double)athlo;
+  if (!(lo <= hi)) return 0;
+  const double pmi = __dsub_rn(PI, ideal), hmi = __dsub_rn(HALF_PI, ideal);
+  // kinks in ascending order, -pi and pi as outer neighbours (not kinks of f
+  // on (-pi, pi): no margin there); written out so that nothing is indexed
+  const double mg = kSignMargin;
+#define GLR_KINK(LEFT, B, RIGHT, MINUS, FB)                      \
+  if (lo >= (LEFT) && hi <= (RIGHT)) {                           \
+    *beta = (B); *minus = (MINUS); *fbeta = (FB);                \
+    return 1;                                                    \
+  }
+  GLR_KINK(-PI, -pmi, -HALF_PI - mg, 0, hmi)
+  GLR_KINK(-pmi + mg, -HALF_PI, -ideal - mg, 1, hmi)
+  GLR_KINK(-HALF_PI + mg, -ideal, -mg, 0, hmi)
+  GLR_KINK(-ideal + mg, 0.0, ideal - mg, 1, ideal)
+  GLR_KINK(mg, ideal, HALF_PI - mg, 0, hmi)
+  GLR_KINK(ideal + mg, HALF_PI, pmi - mg, 1, hmi)
+  GLR_KINK(HALF_PI + mg, pmi, PI, 0, hmi)
+#undef GLR_KINK
+  return 0;
+}
+
 // Exact reference predicate for one pair (general semantics: doubles
 // compared directly, ids tested), used for the filter's uncertain pairs.
 // Returns -1 for no hit, else the pair's angle deviation (0 without ANGLE).
@@ -1184,7 +1228,8 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
         // from the masked sum by a relative 2^-265 at most (DADD, no zeroing
         // MOV or {0,1} multiplier per pair).
         double v = AM == 3 ? angle_dev_signed(th[k], thj, ideal)
-                           : angle_dev_fast_signed(th[k], thj, kappa);
+                   : AM == 1 ? __dsub_rn(thj, th[k])  // one-kink units (range_kink)
+                             : angle_dev_fast_signed(th[k], thj, kappa);
         if (FOLD) {  // hit <=> M's sign bit (an integer test: -0 is a hit)
           asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi;\n\t"
               "setp.lt.s32 p, %2, 0;\n\t"
@@ -1243,8 +1288,10 @@ __device__ __forceinline__ void filter_block(const FIRegs &R, const double (&th)
     if (qn + total > kQCap) {  // total <= 32 * NJ * kFK <= kQCap
       // queued hits: the signed form's C_k multiply x_k, so they count
       // apart (qc); their deviations go to dev[0], unused by that form
+      // (one-kink units, AM 1: their filter hits multiply f(beta), so the
+      // queued ones count apart too, deviations in A2[0], unused there)
       drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal,
-                         SIGNED ? qc : cnt[0], dev[0]);
+                         (SIGNED || AM == 1) ? qc : cnt[0], AM == 1 ? A2[0] : dev[0]);
       qn = 0;
     }
     unsigned pos = qn + incl - n;
@@ -1609,11 +1656,17 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
       skip = (unsigned)((sm | (sm >> kSubBits)) >> (kSubQuarters * slice)) & kSubQuarterMask;
     }
     double th[kFK];
-    int am = 0;  // angle mode: 0 general (reference formula), 2 signed
-    double sigma = 1.0;
+    int am = 0;  // angle mode: 0 general formula, 1 one kink, 2 signed
+    double sigma = 1.0, fbeta = 0.0;
+    int kminus = 0;
     if (ANGLE) {
       double sh = 0.0;
       if (ti != tj && shift_ok && unit_shift(bi, bj, ideal, &sh, &sigma) == 1) am = 2;
+#if GLR_XKINK
+      else if (ti != tj && shift_ok &&
+               range_kink(bi.thlo, bi.thhi, bj.thlo, bj.thhi, ideal, &sh, &fbeta, &kminus) == 1)
+        am = 1;
+#endif
       const double *tt = ftile[ti].theta;
 #pragma unroll
       for (int k = 0; k < kFK; ++k) th[k] = tt[islot + 32 * k];
@@ -1665,6 +1718,24 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
                                                               theta, ibase, jbase, wq, qn, qc);
         }
       }
+    } else if (ANGLE && am == 1) {
+      for (int q = 0; q < kSubQuarters; ++q) {
+        if (skip & (1u << q)) continue;
+        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+        if (thr == 1.0f) {
+#pragma unroll kJUnrollC
+          for (int jj = j0; jj < j1; jj += kNJ)
+            filter_block<ANGLE, false, kNJ, 1, true>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                                     ideal, kappa, rec, ids, theta, ibase, jbase,
+                                                     wq, qn, qc);
+        } else {
+#pragma unroll 1
+          for (int jj = j0; jj < j1; jj += kNJ)
+            filter_block<ANGLE, false, kNJ, 1>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2,
+                                               ideal, kappa, rec, ids, theta, ibase, jbase, wq,
+                                               qn, qc);
+        }
+      }
     } else {
       for (int q = 0; q < kSubQuarters; ++q) {
         if (skip & (1u << q)) continue;
@@ -1703,6 +1774,8 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
     if (qn != 0) {
       if (ANGLE && am == 2)
         drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, dev[0]);
+      else if (ANGLE && am == 1)
+        drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, qc, A2[0]);
       else
         drain_queue<ANGLE>(wq, qn, lane, rec, ids, theta, ibase, jbase, ideal, cnt[0], dev[0]);
     }
@@ -1724,6 +1797,15 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
 #pragma unroll
         for (int k = 0; k < kFK; ++k) s = __dadd_rn(s, dev[k]);
         s = s < 0x1p-900 ? 0.0 : s;  // only cleared-miss leftovers (< 2^-1031)
+        if (am == 1) {
+          // one-kink units: the filter's hits (c - qc) give hits * f(beta) -
+          // sum |v| or sum |v|; + the queued hits' deviations (A2[0])
+          if (kminus) {
+            const double t = __dsub_rn(__dmul_rn((double)(c - qc), fbeta), s);
+            s = t > 0.0 ? t : 0.0;
+          }
+          s = __dadd_rn(s, A2[0]);
+        }
       }
       // warp sums in a fixed shuffle tree; lane 0 adds the deviation sum
       // exactly, unless the slice's mean deviation per hit is below 2^-16

@@ -70,3 +70,50 @@ def test_straddling_units_are_not_classified():
     assert unit_shift(0.1, 0.2, 0.3, 0.4, 0.5) == (0, 0.5)
     assert unit_shift(2.9, 3.0, 0.1, 0.2, 0.5) == (3, 0.5 - PI)
     assert unit_shift(float("inf"), -float("inf"), 0.1, 0.2, 0.5) is None  # empty tile
+
+
+SIGN_MARGIN = 2.0 ** -8
+
+
+def range_kink(lo_i, hi_i, lo_j, hi_j, ideal):
+    """crossing.cu range_kink on tile theta bounds: (beta, f(beta), minus) of
+    the one kink the unit's dt range may hold, or None."""
+    lo, hi = lo_j - hi_i, hi_j - lo_i
+    if not lo <= hi:
+        return None
+    pmi, hmi, mg = PI - ideal, HALF_PI - ideal, SIGN_MARGIN
+    table = ((-PI, -pmi, -HALF_PI - mg, 0, hmi), (-pmi + mg, -HALF_PI, -ideal - mg, 1, hmi),
+             (-HALF_PI + mg, -ideal, -mg, 0, hmi), (-ideal + mg, 0.0, ideal - mg, 1, ideal),
+             (mg, ideal, HALF_PI - mg, 0, hmi), (ideal + mg, HALF_PI, pmi - mg, 1, hmi),
+             (HALF_PI + mg, pmi, PI, 0, hmi))
+    for left, beta, right, minus, fbeta in table:
+        if lo >= left and hi <= right:
+            return beta, fbeta, minus
+    return None
+
+
+@pytest.mark.parametrize("ideal", [1e-6, 0.02, 0.3, math.radians(70.0), 1.3, HALF_PI - 1e-3, HALF_PI])
+def test_one_kink_units_match_reference(ideal):
+    """Every pair of a unit range_kink accepts: |theta_j - (theta_i + beta)|
+    (or f(beta) minus it) equals the reference deviation to a few ulps of pi,
+    the second kind's terms stay >= the margin, and all seven kinks occur."""
+    rng = np.random.default_rng(int(ideal * 1e6) % 2**32 + 7)
+    seen = set()
+    for _ in range(6000):
+        wi, wj = rng.uniform(0, 0.5, 2) * rng.choice([1e-4, 1e-2, 1.0], 2)
+        ci, cj = rng.uniform(0, PI, 2)
+        ti = np.clip(ci + rng.uniform(0, wi, 48), 0, np.nextafter(PI, 0))
+        tj = np.clip(cj + rng.uniform(0, wj, 48), 0, np.nextafter(PI, 0))
+        cls = range_kink(ti.min(), ti.max(), tj.min(), tj.max(), ideal)
+        if cls is None:
+            continue
+        beta, fbeta, minus = cls
+        seen.add(round(beta, 9))
+        v = np.abs(tj[None, :] - (ti[:, None] + beta))
+        got = fbeta - v if minus else v
+        want = reference_dev(ti[:, None], tj[None, :], ideal)
+        assert np.max(np.abs(got - want)) <= 4e-15, (ideal, beta, minus)
+        if minus:
+            assert got.min() >= SIGN_MARGIN * (1 - 1e-9)
+    if 0.02 <= ideal <= 1.3:  # nearer 0 or pi/2 some kinks sit inside their neighbours' margins
+        assert len(seen) == 7, seen
