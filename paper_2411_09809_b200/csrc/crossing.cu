@@ -1701,9 +1701,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         filter_block<ANGLE, true, kNJ, 0>(R, th, jr, jth, jj, islot, thr, cnt, dev, A2, ideal, kappa,
                                           rec, ids, theta, ibase, jbase, wq, qn, qc);
     } else if (ANGLE && am == 2) {
-      for (int q = 0; q < kSubQuarters; ++q) {
-        if (skip & (1u << q)) continue;
-        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+      // runs of consecutive j-quarters that are not skipped (the whole tile
+      // without masks: one loop, as in a dense pass)
+      for (unsigned act = ~skip & kSubQuarterMask; act != 0u;) {
+        const int q0 = __ffs(act) - 1;
+        const int len = __ffs(~(act >> q0)) - 1;
+        act &= ~(((1u << len) - 1u) << q0);
+        const int j0 = q0 * kSubJ, j1 = j0 + len * kSubJ;
         if (thr == 1.0f) {
 #pragma unroll kJUnrollS
           for (int jj = j0; jj < j1; jj += kFilterBlockSigned)
@@ -1719,9 +1723,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         }
       }
     } else if (ANGLE && am == 1) {
-      for (int q = 0; q < kSubQuarters; ++q) {
-        if (skip & (1u << q)) continue;
-        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+      // runs of consecutive j-quarters that are not skipped (the whole tile
+      // without masks: one loop, as in a dense pass)
+      for (unsigned act = ~skip & kSubQuarterMask; act != 0u;) {
+        const int q0 = __ffs(act) - 1;
+        const int len = __ffs(~(act >> q0)) - 1;
+        act &= ~(((1u << len) - 1u) << q0);
+        const int j0 = q0 * kSubJ, j1 = j0 + len * kSubJ;
         if (thr == 1.0f) {
 #pragma unroll kJUnrollC
           for (int jj = j0; jj < j1; jj += kNJ)
@@ -1737,9 +1745,13 @@ cross_filter_kernel(const RecHeader *__restrict__ hdr, const EdgeRec *__restrict
         }
       }
     } else {
-      for (int q = 0; q < kSubQuarters; ++q) {
-        if (skip & (1u << q)) continue;
-        const int j0 = q * kSubJ, j1 = j0 + kSubJ;
+      // runs of consecutive j-quarters that are not skipped (the whole tile
+      // without masks: one loop, as in a dense pass)
+      for (unsigned act = ~skip & kSubQuarterMask; act != 0u;) {
+        const int q0 = __ffs(act) - 1;
+        const int len = __ffs(~(act >> q0)) - 1;
+        act &= ~(((1u << len) - 1u) << q0);
+        const int j0 = q0 * kSubJ, j1 = j0 + len * kSubJ;
         if (thr == 1.0f) {  // general units too: FOLD products with an immediate t
 #pragma unroll kJUnrollC
           for (int jj = j0; jj < j1; jj += kNJ)
