@@ -2492,9 +2492,12 @@ theta_sort_kernel(const double *__restrict__ theta, int64_t m, double *__restric
 // <= 256 angles); callers re-evaluate per pair when the mean deviation is
 // small (kPiecewiseMeanDev).
 constexpr double kPiecewiseMeanDev = 0x1p-12;
-// NB: the block size (a power of two); s[n..NB) hold +inf, so the branchless
-// searches -- all seven advanced together, one shared-memory load each per
-// step -- never pass n.
+// NB: the block size (a power of two); s[n..NB) hold +inf, so a branchless
+// search never passes n.  A block's angles span a fraction of a radian, so
+// most kinks fall outside [s[0], s[n-1]] and are placed by two comparisons;
+// only the one or two inside are searched, and only non-empty runs are
+// evaluated (the lanes of a warp mostly agree on which: their theta_i lie in
+// one tile's narrow range).
 template <int NB>
 __device__ inline double piecewise_dev(double ti, const double *s, const double *pre, int n,
                                        double tot, double ideal) {
@@ -2502,33 +2505,33 @@ __device__ inline double piecewise_dev(double ti, const double *s, const double 
   const double pmi = __dsub_rn(PI, ideal);
   const double bp[7] = {-pmi, -HALF_PI, -ideal, 0.0, ideal, HALF_PI, pmi};
   const double c[8] = {-pmi, pmi, -ideal, ideal, ideal, -ideal, pmi, -pmi};
-  double x[7];
-  int pos[7];
-#pragma unroll
-  for (int p = 0; p < 7; ++p) {
-    x[p] = __dadd_rn(ti, bp[p]);
-    pos[p] = 0;
-  }
-#pragma unroll
-  for (int step = NB / 2; step >= 1; step >>= 1) {
-#pragma unroll
-    for (int p = 0; p < 7; ++p) pos[p] += s[pos[p] + step - 1] < x[p] ? step : 0;
-  }
-#pragma unroll
-  for (int p = 0; p < 7; ++p) pos[p] += s[pos[p]] < x[p] ? 1 : 0;  // pos <= NB - 1 here
+  const double s0 = s[0], sl = s[n - 1];
   int a = 0;
   double pa = 0.0, acc = 0.0;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
-    const int b = p < 7 ? pos[p] : n;
-    const int bb = b < a ? a : (b > n ? n : b);  // monotone whatever the roundings
-    const double pb = bb < n ? pre[bb] : tot;
-    const double cnt = (double)(bb - a);
-    const double lin = __dsub_rn(__dsub_rn(pb, pa), __dmul_rn(cnt, ti));
-    const double v = __dadd_rn(__dmul_rn(cnt, c[p]), (p & 1) ? lin : -lin);
-    acc = __dadd_rn(acc, v > 0.0 ? v : 0.0);
-    a = bb;
-    pa = pb;
+    int b = n;
+    if (p < 7) {
+      const double x = __dadd_rn(ti, bp[p]);
+      if (!(s0 < x)) {
+        b = 0;  // no angle below x
+      } else if (!(sl < x)) {
+        int pos = 0;  // number of angles below x
+#pragma unroll
+        for (int step = NB / 2; step >= 1; step >>= 1) pos += s[pos + step - 1] < x ? step : 0;
+        pos += s[pos] < x ? 1 : 0;
+        b = pos > n ? n : pos;
+      }
+    }
+    if (b > a) {
+      const double pb = b < n ? pre[b] : tot;
+      const double cnt = (double)(b - a);
+      const double lin = __dsub_rn(__dsub_rn(pb, pa), __dmul_rn(cnt, ti));
+      const double v = __dadd_rn(__dmul_rn(cnt, c[p]), (p & 1) ? lin : -lin);
+      acc = __dadd_rn(acc, v > 0.0 ? v : 0.0);
+      a = b;
+      pa = pb;
+    }
   }
   return acc;
 }
