@@ -245,9 +245,12 @@ int glr_crossing_sub_mask_bytes(void);
 int glr_crossing_sub_quarters(void);
 
 /* Units [unit_begin, unit_end) of a classified list (unit u = d_list[u]; u <
- * mixed_len: the pair kernels; otherwise a full unit: na * nb crossings and
- * the reference's per-pair deviation, or its closed form where the unit's
- * theta ranges fix the formula's branch), under interleaved chunk ownership
+ * mixed_len: the pair kernels, which skip the blocks d_sub marks -- the full
+ * ones are counted whole like full units; otherwise a full unit: na * nb
+ * crossings and the pairs' deviations (exact.py:217-221) from a closed form
+ * where the unit's theta ranges fix the formula's branch, else from
+ * piecewise-linear sums over the j-tile's sorted angles, else -- small mean
+ * deviation -- pair by pair), under interleaved chunk ownership
  * for rank of world (0 of 1: the whole range).  Partials over a disjoint
  * cover of [0, mixed_len + full_len), or over all ranks, sum to the dense
  * result. */

@@ -351,3 +351,21 @@ def test_row_dealt_plans_partition_the_list(plan):
                 part.partial_interleaved(IDEAL, (r + 1) % world, world)
         assert seen == full_list, (name, world)
         assert cs == int(whole[0]) and strict_close(ds, whole[1]), (name, world)
+
+
+def test_rows_bad_arguments(gpu, plan):
+    """glr_crossing_candidates_rows rejects rank >= world and world < 1."""
+    import ctypes
+
+    import torch
+
+    from paper_2411_09809_b200 import _lib
+
+    name, g, dg, rec, edges = plan
+    L = _lib.lib()
+    counts = (ctypes.c_uint64 * 2)()
+    st = torch.cuda.current_stream().cuda_stream
+    for rank, world in ((2, 2), (-1, 2), (0, 0)):
+        rc = L.glr_crossing_candidates_rows(rec.buf.data_ptr(), rec.n, rec.m, None, None, 0,
+                                            counts, rank, world, st)
+        assert rc == _lib.GLR_EARG, (rank, world)
