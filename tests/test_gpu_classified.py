@@ -369,3 +369,25 @@ def test_rows_bad_arguments(gpu, plan):
         rc = L.glr_crossing_candidates_rows(rec.buf.data_ptr(), rec.n, rec.m, None, None, 0,
                                             counts, rank, world, st)
         assert rc == _lib.GLR_EARG, (rank, world)
+
+
+@pytest.mark.parametrize("ideal", [2.0 ** -120, 1e-9, math.pi / 2])
+def test_classified_extreme_ideal_angles(plan, ideal):
+    """Ideal angles at the ends of (0, pi/2]: below 2^-100 the filter kernel
+    stands down (the FP64 sign kernel scans the mixed units, masks ignored,
+    full blocks not counted apart); at pi/2 three kinks of the deviation
+    coincide.  Totals must still equal the oracle's."""
+    from oracle import glare_oracle as O
+
+    name, g, dg, rec, _ = plan
+    if g.num_edges > 20000:
+        from oracle import sweep
+
+        want_c, want_d = sweep.crossing_scan(g.xy, g.edges, ideal)
+    else:
+        want_c, want_d = O.crossing_scan(g.xy, g.edges, ideal)
+    c, d = rec.partial(ideal, 0, rec.units).tolist()
+    assert int(c) == want_c and strict_close(d, want_d), (name, ideal, c, want_c, d, want_d)
+    parts = [rec.partial_interleaved(ideal, r, 2).tolist() for r in range(2)]
+    assert sum(int(p[0]) for p in parts) == want_c
+    assert strict_close(sum(p[1] for p in parts), want_d)
