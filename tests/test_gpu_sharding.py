@@ -168,3 +168,84 @@ def test_two_processes_build_the_same_auto_plan(gpu):
         c, d = S.crossing_scan(g.xy, g.edges, IDEAL)
         assert int(a[3][0] + b[3][0]) == c
         assert strict_close(a[3][1] + b[3][1], d)
+
+
+def _big_long_random():
+    """Long random edges above the k-d order's threshold (131,072 edges)."""
+    from paper_2411_09809_b200.model import LayoutGraph, normalize_edges
+
+    rng = np.random.default_rng(21)
+    n, m = 50000, 150000
+    xy = rng.integers(0, 2 ** 16, (n, 2)).astype(np.float64)
+    pairs = rng.integers(0, n, (m, 2))
+    pairs = pairs[np.any(xy[pairs[:, 0]] != xy[pairs[:, 1]], axis=1)]
+    e, _, _ = normalize_edges(pairs)
+    return LayoutGraph.from_normalized(xy, e)
+
+
+E2E_GRAPHS = {"local_lattice": lambda: _plan_graph("local_lattice"), "big_long": _big_long_random}
+
+
+def _e2e_worker(rank, world, port, q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_09809_b200 import metrics as M, sharding
+
+        torch.cuda.set_device(0)
+        out = {}
+        for name, make in E2E_GRAPHS.items():
+            g = make()
+            dg = M.DeviceGraph.from_graph(g)
+            for strategy in ("auto", "culled", "dense"):
+                # gloo reduces host tensors: combine the device partial on the host
+                res = torch.zeros(3, dtype=torch.float64, device="cuda")
+                rec = M.CrossingRecords(dg, strategy, "theta",
+                                        rows=(rank, world) if strategy != "dense" else None)
+                rec.partial_interleaved(IDEAL, rank, world, out=res[0:2])
+                host = res.cpu()
+                dist.all_reduce(host)
+                out[(name, strategy)] = (host.tolist(), rec.culled, rec.rows)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_row_dealt_plans_end_to_end(gpu):
+    """Two processes (gloo, one device, never waiting on each other's kernels)
+    run the multi-rank path of sharded_evaluate: culled plans dealt by tile
+    rows -- with "auto" agreeing through the allreduce of plan costs -- and
+    dense interleaved chunks; every strategy's combined result equals the C
+    oracle's."""
+    import torch.multiprocessing as mp
+
+    from oracle import sweep as S
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_e2e_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for name, make in E2E_GRAPHS.items():
+        g = make()
+        c, d = S.crossing_scan(g.xy, g.edges, IDEAL)
+        for strategy in ("auto", "culled", "dense"):
+            (r0, culled0, rows0), (r1, culled1, rows1) = (results[k][(name, strategy)] for k in (0, 1))
+            assert r0 == r1, (name, strategy)               # both ranks hold the sum
+            assert culled0 == culled1, (name, strategy)     # ... and took the same plan
+            assert int(r0[0]) == c and strict_close(r0[1], d), (name, strategy, r0, c, d)
+            if strategy == "culled":
+                assert culled0 and rows0 == (0, 2) and rows1 == (1, 2)
