@@ -187,6 +187,18 @@ constexpr int kFSlices = kTile / (32 * kFK);  // warp slices per unit
 #ifndef GLR_XSUBQ
 #define GLR_XSUBQ 4
 #endif
+// unroll of orient_ranges' corner loop (a multiple of 4 keeps the hoisted
+// differences in registers)
+#ifndef GLR_XCORNERUNROLL
+#define GLR_XCORNERUNROLL 16
+#endif
+constexpr int kCornerUnroll = GLR_XCORNERUNROLL;
+// CTAs per SM of the classification kernels (register cap: 1 -> 255, 2 -> 128
+// with ~200 B of spills, 3 -> 80): C5 classes + masks 53.3 / 43.7 ms at 1 / 2
+// (tools/classtime.sh); corner-loop unroll 4 / 8 / 16: 60.1 / 53.2 / 53.3 ms
+#ifndef GLR_XCLASSMINB
+#define GLR_XCLASSMINB 2
+#endif
 // one-kink angle form in the fused filter kernel (range_kink)
 #ifndef GLR_XKINK
 #define GLR_XKINK 1
@@ -2268,7 +2280,7 @@ __device__ inline void orient_ranges(const PQBox &L, const PQBox &R, double (&lo
     w[k][0][0] = __dsub_rn(rb[k][0], L.px0); w[k][0][1] = __dsub_rn(rb[k][1], L.px0);
     w[k][1][0] = __dsub_rn(rb[k][0], L.px1); w[k][1][1] = __dsub_rn(rb[k][1], L.px1);
   }
-#pragma unroll
+#pragma unroll kCornerUnroll
   for (int c = 0; c < 16; ++c) {
     const int xs = c & 1, ys = (c >> 1) & 1;
     const double px = xs ? L.px1 : L.px0, py = ys ? L.py1 : L.py0;
@@ -2333,7 +2345,7 @@ __device__ inline int unit_class(const PQBox &A, const PQBox &B) {
 // closed bboxes, is empty too); the unit's bits are gathered with two
 // ballots.  Diagonal units and inadmissible inputs keep 0.
 static_assert(32 % kSubBits == 0, "a warp covers whole units");
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GLR_XCLASSMINB)
 sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list,
                 uint64_t mixed, const PQBox *__restrict__ pqs, SubMask *__restrict__ sub) {
   constexpr int kPer = kTile / kSubJ;             // sub-blocks per tile
@@ -2378,7 +2390,7 @@ sub_mask_kernel(const RecHeader *__restrict__ hdr, const int2 *__restrict__ list
 // off_m[ti] and full units at off_m[T] + off_f[ti] (both parts row-major).
 constexpr int kClassThreads = 256;
 template <bool FILL>
-__global__ void __launch_bounds__(kClassThreads)
+__global__ void __launch_bounds__(kClassThreads, GLR_XCLASSMINB)
 tile_class_kernel(const RecHeader *__restrict__ hdr, const int4 *__restrict__ box,
                   const PQBox *__restrict__ pq, int64_t T, int row_rank, int row_world,
                   unsigned long long *__restrict__ cnt_m, unsigned long long *__restrict__ cnt_f,
