@@ -474,7 +474,8 @@ int theta_sort(const double *d_xy, int64_t n, const int64_t *d_edges, int64_t m,
 // anchored at the hub, so only hubs whose shared-vertex pairs would cost more
 // fallbacks than their boxes cost candidate units get a group (C5 culled:
 // 3.70 s at 256, 3.19 s at 1024, 2.98 s at 4096, 2.92 s at 16384, 3.05 s
-// with none; tools/cull_probe.py).
+// with none; tools/cull_probe.py; with the k-d order and the final kernels:
+// 1447 ms at 8192, 1439 at 16384, 1444 at 32768, 1457 with none).
 #ifndef GLR_BOX_HUB_DEGREE
 #define GLR_BOX_HUB_DEGREE 16384
 #endif
